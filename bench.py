@@ -1,0 +1,295 @@
+"""MHAR chain-step throughput on B200 (BASELINE.json metric).
+
+A "step" is one iterate of every walk on every rank (the reference's
+step(), proj/src/sampler.cpp:235-272), so
+
+    value = walks_total x K / max-over-ranks device time   [chain-steps/s]
+
+on the largest single-GPU BASELINE configuration: config 5, n = 2000,
+m_I = 200000 unit-norm Gaussian rows, 4096 walks per GPU, fp64.  The
+polytope (3.2 GB) is larger than L2, so no explicit flush is needed.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; N > 1 under
+torch.distributed.run (one rank per GPU, NCCL).  --impl reference times the
+CPU restatement of the reference (oracle/, the reference itself cannot be
+built here) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_FILE = os.path.join(ROOT, "profiles", "fp64_peaks_r01.json")
+METRIC = "MHAR chain-steps/sec at n=2000,m_I=2e5 fp64"
+
+
+def fp64_peak():
+    """Measured fp64 DMMA peak (tools/microbench_fp64.cu on this pool's
+    B200; MEASURED_PEAKS.json carries no fp64 entry)."""
+    best = None
+    with open(PEAKS_FILE) as f:
+        for line in f:
+            d = json.loads(line)
+            for k, v in d.items():
+                if k.startswith("dmma_") and k.endswith("_tflops"):
+                    best = v if best is None else max(best, v)
+    return best
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.sw_power_cap,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.out = out
+        else:
+            self.out = ""
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for line in self.out.strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def cpu_sample(w, z_sample: int, iters: int, threads: int):
+    """The oracle (CPU restatement of the reference step) on a bounded
+    sample of the same workload: z_sample walks x iters iterates."""
+    import oracle
+    L = oracle.lib()
+    L.orc_set_threads(threads)
+    p = w.polytope
+    X = np.zeros((p.dim(), z_sample), order="F")
+    X[:] = w.x0[:, None]
+    rng = oracle.WalkRng(1234, z_sample)
+    P = None
+    if p.num_equalities():
+        st, P, _ = oracle.compute_projection(p.a_eq)
+    st, _, _ = oracle.step(p.a_in, p.b_in, P, 1e-11, rng, X)  # warm-up
+    t0 = time.perf_counter()
+    for _ in range(iters):
+        st, _, _ = oracle.step(p.a_in, p.b_in, P, 1e-11, rng, X)
+        assert st == 0
+    dt = time.perf_counter() - t0
+    return z_sample * iters / dt, dt
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2104_07097_b200 import workloads
+    w = workloads.config(args.config, z=args.z)
+    threads = os.cpu_count() or 1
+    steps = []
+    for _ in range(args.warmup):
+        cpu_sample(w, args.cpu_walks, 1, threads)
+    for _ in range(args.steps):
+        v, _ = cpu_sample(w, args.cpu_walks, 1, threads)
+        steps.append(v)
+    value = statistics.median(steps)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "chain-steps/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * args.cpu_walks / value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "n": w.polytope.dim(), "m_I": w.polytope.num_inequalities(),
+                   "m_E": w.polytope.num_equalities(), "walks_per_step": args.cpu_walks},
+        "cpu_baseline": {"value": value, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.cpu_walks} walks x 1 iterate per step of the config-"
+                                   f"{args.config} polytope (oracle/mhar_oracle.c, OpenMP GEMM)"},
+        "e2e": {"value": value, "unit": "chain-steps/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_engine(args, world, rank, local):
+    import paper_2104_07097_b200 as mh
+    from paper_2104_07097_b200 import workloads
+
+    w = workloads.config(args.config, z=args.z)
+    p = w.polytope
+    z = w.z
+    projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
+    reproject = args.reproject if p.num_equalities() else 0
+    eng = mh.Engine(p, z, seed=args.seed, projector=projector, slack=args.slack,
+                    refresh_every=args.refresh, device=local, chain_offset=rank * z)
+    X0 = np.zeros((p.dim(), z), order="F")
+    X0[:] = w.x0[:, None]
+    eng.set_state(X0)
+
+    # warm-up
+    eng.step_timed(args.warmup, reproject)
+
+    # timed, device-resident inputs
+    eng.reset_stats()
+    eng.set_timing(True)
+    barrier(world)
+    with ClockSampler(local) as clk:
+        ms = eng.step_timed(args.steps, reproject)
+    eng.set_timing(False)
+    st = eng.stats()
+    ms = max_over_ranks(ms, world)
+    value = z * world * args.steps / (ms * 1e-3)
+
+    # e2e: reference-facing C-ABI call with host buffers each step
+    # (set_state from host, one iterate, get_state to host)
+    Xh = eng.get_state()
+    barrier(world)
+    t_e2e = []
+    for i in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        eng.set_state(Xh)
+        eng.step(1, reproject)
+        Xh = eng.get_state()
+        t_e2e.append(time.perf_counter() - t0)
+    e2e_s = max_over_ranks(sum(t_e2e), world)
+    e2e_value = z * world * args.e2e_steps / e2e_s
+    bytes_state = p.dim() * z * 8
+
+    fpi = eng.flops_per_iterate()
+    chord_avg_ms = st["chord_ms"] / max(st["chord_timed"], 1)
+    achieved = st["chord_flops"] / max(st["chord_ms"] * 1e-3, 1e-30) / 1e12
+    peak = fp64_peak()
+    eng.close()
+
+    if rank != 0:
+        return
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        v, dt = cpu_sample(w, args.cpu_walks, args.cpu_iters, threads)
+        cpu = {"value": v, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+               "sample": f"{args.cpu_walks} walks x {args.cpu_iters} iterates of the same polytope "
+                         f"({dt:.1f} s; oracle/mhar_oracle.c restating proj/src/sampler.cpp, "
+                         f"OpenMP AVX-512 GEMM)"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "chain-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded unit-norm Gaussian rows, BASELINE config %d)" % args.config,
+        "config": {"workload": w.name, "n": p.dim(), "m_I": p.num_inequalities(),
+                   "m_E": p.num_equalities(), "walks_per_gpu": z, "walks_total": z * world,
+                   "slack_mode": args.slack, "refresh_every": args.refresh, "rng": "philox",
+                   "parallelism": f"walk-sharded x{world}",
+                   "l2": "inputs larger than L2 (A_I is %.1f GB)" % (p.a_in.nbytes / 1e9)},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "kernel": "chord_kernel (DMMA A_I [X|D] / A_I D + fused chord reduce)",
+                     "avg_launch_ms": chord_avg_ms, "launches": st["chord_timed"],
+                     "peak_source": "fp64 DMMA microbench, profiles/fp64_peaks_r01.json"},
+        "reference_equivalent_tflops": value * fpi / z / 1e12 / world,
+        "e2e": {"value": e2e_value, "unit": "chain-steps/s", "h2d_bytes_per_step": bytes_state,
+                "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
+        "gpu_launches": st["kernel_launches"],
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--z", type=int, default=None)
+    ap.add_argument("--seed", type=int, default=2021)
+    ap.add_argument("--slack", default="incremental", choices=["incremental", "recompute"])
+    ap.add_argument("--refresh", type=int, default=128)
+    ap.add_argument("--reproject", type=int, default=1000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-walks", type=int, default=256)
+    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+    else:
+        run_engine(args, world, rank, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

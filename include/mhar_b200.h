@@ -1,0 +1,213 @@
+/*
+ * mhar_b200.h -- C ABI of the B200-native MHAR (Matrix Hit-and-Run) chain-step
+ * engine.  Plain pointers and sizes only; no CUDA, torch or C++ types.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj, paths below relative to it):
+ *
+ *   reference interface                                   replaced by
+ *   ----------------------------------------------------  -------------------------
+ *   mhar::Polytope (include/mhar/polytope.hpp:12-25)       mhar_polytope + ctx upload
+ *   mhar::SamplerConfig (include/mhar/sampler.hpp:16-25)   mhar_options / mhar_run_config
+ *   mhar::WalkRng (include/mhar/rng.hpp:42-55)             device counters (Philox or the
+ *                                                          reference SplitMix streams)
+ *   mhar::WalkState (include/mhar/sampler.hpp:69-74)       mhar_set_state / mhar_get_state
+ *   mhar::step (include/mhar/sampler.hpp:79-80,            mhar_step
+ *               src/sampler.cpp:235-272)
+ *   mhar::compute_lambda_intervals (sampler.hpp:53-58,     mhar_lambda_intervals
+ *               src/sampler.cpp:150-208)
+ *   mhar::run (include/mhar/sampler.hpp:99,                mhar_run (+ warm start x0,
+ *               src/sampler.cpp:274-335)                   which replaces :276)
+ *   mhar::compute_projection (include/mhar/projection.hpp:33,
+ *               src/projection.cpp:9-34)                   mhar_compute_projection (host)
+ *   mhar::reproject_points (projection.hpp:35)             inside mhar_step / mhar_run
+ *   mhar::contains (polytope.hpp:57, src/polytope.cpp:177) mhar_check_state
+ *   mhar::Error / ErrorCode (include/mhar/errors.hpp)      int status + mhar_last_error
+ *
+ * Matrices are column-major doubles (the reference's Eigen::MatrixXd layout,
+ * include/mhar/linalg.hpp:7-10) unless stated.  Every function returns an int
+ * status: MHAR_OK (0) or 1 + the reference ErrorCode ordinal; MHAR_ERR_CUDA
+ * for a device/runtime failure, which the reference has no code for.
+ * mhar_last_error() returns the thread-local message of the last failure.
+ * A context is bound to one CUDA device and is not thread-safe.
+ */
+#ifndef MHAR_B200_H
+#define MHAR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: 1 + mhar::ErrorCode ordinal (errors.hpp:10-24) ------- */
+#define MHAR_OK 0
+#define MHAR_ERR_INVALID_ARGUMENT 1
+#define MHAR_ERR_DIMENSION_MISMATCH 2
+#define MHAR_ERR_SINGULAR_MATRIX 3
+#define MHAR_ERR_RANK_DEFICIENT_EQ 4
+#define MHAR_ERR_EMPTY_POLYTOPE 5
+#define MHAR_ERR_NO_INTERIOR 6
+#define MHAR_ERR_UNBOUNDED_POLYTOPE 7
+#define MHAR_ERR_DIRECTION_DEGENERATE 8
+#define MHAR_ERR_RETRY_EXHAUSTED 9
+#define MHAR_ERR_CYCLE_SUSPECTED 10
+#define MHAR_ERR_DEGENERATE_TEST 11
+#define MHAR_ERR_NUMERICAL_FAILURE 12
+#define MHAR_ERR_IO_FAILURE 13
+#define MHAR_ERR_CUDA 100
+
+/* ---- per-walk flag bits (mhar_step_injected / mhar_lambda_intervals) ----- */
+#define MHAR_FLAG_DEGENERATE 1      /* LambdaIntervals::degenerate (sampler.hpp:33-37) */
+#define MHAR_FLAG_HAS_UPPER 2       /* some rate > eps_dir (chord_scan has_pos) */
+#define MHAR_FLAG_HAS_LOWER 4       /* some rate < -eps_dir (chord_scan has_neg) */
+#define MHAR_FLAG_COLLAPSED 8       /* ||P h|| <= 1e-12 (projection.hpp:25) */
+#define MHAR_FLAG_THETA_MIDPOINT 16 /* theta hit an endpoint; midpoint taken */
+
+/* ---- options ------------------------------------------------------------- */
+#define MHAR_RNG_PHILOX 0    /* Philox4x32-10 keyed (seed, global walk, iterate, attempt) */
+#define MHAR_RNG_REFERENCE 1 /* the reference's SplitMix64 streams, bit-exact uniforms
+                                (rng.cpp:13-21,101-113); single device only */
+
+#define MHAR_SLACK_RECOMPUTE 0   /* every iterate: one fused pass A_I [X | D] + chord reduce */
+#define MHAR_SLACK_INCREMENTAL 1 /* A_I D + streamed slack b - A_I X, refreshed by a fused
+                                    pass every refresh_every iterates */
+
+typedef struct {
+  int64_t n;          /* dimension */
+  int64_t m_in;       /* inequality rows */
+  int64_t m_eq;       /* equality rows (0 = full dimensional) */
+  const double* a_in; /* m_in x n, column-major */
+  const double* b_in; /* m_in */
+  const double* a_eq; /* m_eq x n, column-major; NULL when m_eq == 0 */
+  const double* b_eq; /* m_eq */
+} mhar_polytope;
+
+typedef struct {
+  int64_t z;             /* walks on this device (the shard) */
+  int64_t chain_offset;  /* global id of local walk 0; RNG is keyed on global ids */
+  uint64_t seed;         /* SamplerConfig::seed */
+  double eps_dir;        /* SamplerConfig::eps_dir (1e-11) */
+  double eps_feas;       /* SamplerConfig::eps_feas (1e-9) */
+  int rng;               /* MHAR_RNG_* */
+  int slack_mode;        /* MHAR_SLACK_* */
+  int64_t refresh_every; /* incremental mode: fused refresh cadence (0 = default 64) */
+  int device;            /* CUDA ordinal */
+} mhar_options;
+
+/* Fills o with the reference defaults (sampler.hpp:16-25): eps_dir 1e-11,
+ * eps_feas 1e-9, Philox, incremental slack, device 0. */
+void mhar_default_options(mhar_options* o);
+
+typedef struct mhar_ctx mhar_ctx;
+
+/* Uploads the polytope (the device copy is re-laid out for the tensor-core
+ * tiles), the projector P = I - A_E'(A_E A_E')^-1 A_E and G = (A_E A_E')^-1
+ * (projection.hpp:11-15; NULL both to have them computed on the host with
+ * mhar_compute_projection), allocates the z-walk state.  The state starts at
+ * 0; set it with mhar_set_state. */
+int mhar_ctx_create(const mhar_polytope* p, const double* projector, const double* gram_inverse,
+                    const mhar_options* opt, mhar_ctx** out);
+int mhar_ctx_destroy(mhar_ctx* ctx);
+
+/* WalkState.x (sampler.hpp:70): n x z column-major host buffer. */
+int mhar_set_state(mhar_ctx* ctx, const double* x);
+int mhar_get_state(mhar_ctx* ctx, double* x);
+/* Row-major z x n copy of the state into device memory owned by the caller
+ * (the sample layout of SampleSet::samples, sampler.hpp:83); used to gather
+ * samples across ranks without a host round trip. */
+int mhar_get_state_rows_device(mhar_ctx* ctx, double* dev_rows);
+
+/* `iters` iterates of every walk (step(), sampler.cpp:235-272).  When the
+ * polytope has equalities and reproject_every > 0, walks are pulled back onto
+ * {A_E x = b_E} whenever the context's global iterate count is a multiple of
+ * reproject_every (run(), sampler.cpp:304-311).  Kernels are queued without a
+ * host sync; the first device-side error (lowest walk of the earliest phase,
+ * sampler.cpp ordering) is returned by the next synchronising call. */
+int mhar_step(mhar_ctx* ctx, int64_t iters, int64_t reproject_every);
+/* Waits for queued work and reports a pending device-side error. */
+int mhar_sync(mhar_ctx* ctx);
+/* mhar_step bracketed by CUDA events on the context's stream; *device_ms is
+ * the device time of the `iters` iterates (synchronises). */
+int mhar_step_timed(mhar_ctx* ctx, int64_t iters, int64_t reproject_every, double* device_ms);
+
+/* Test hook: one iterate with the normals H (n x z, column-major) and chord
+ * positions U (z) injected from the host instead of the device RNG.  D = P H
+ * (or H); chords as compute_lambda_intervals; flagged walks stay put; other
+ * walks take theta = lower + U[k] (upper - lower) (an endpoint hit takes the
+ * midpoint) and x += theta d.  Outputs may be NULL.  Always a fresh fused
+ * pass (never the incremental slack). */
+int mhar_step_injected(mhar_ctx* ctx, const double* h, const double* u, double* lower,
+                       double* upper, double* theta, uint8_t* flags);
+
+/* compute_lambda_intervals for host X and D (n x z each) against the
+ * context's polytope; does not move the state.  degenerate gets
+ * MHAR_FLAG_* bits.  UNBOUNDED_POLYTOPE names the first one-sided walk. */
+int mhar_lambda_intervals(mhar_ctx* ctx, const double* x, const double* d, double* lower,
+                          double* upper, uint8_t* flags);
+
+/* contains() (polytope.cpp:177-190) for every walk of the current state:
+ * *first_bad = lowest walk outside by more than eps (or -1); max_viol gets
+ * max_i (A_I x - b_I)_i and max_eq max |A_E x - b_E| per walk (z each, may be
+ * NULL). */
+int mhar_check_state(mhar_ctx* ctx, double eps, int64_t* first_bad, double* max_viol,
+                     double* max_eq);
+
+typedef struct {
+  int64_t phi;             /* iterates between collections */
+  int64_t windows;         /* collections; SampleSet::windows */
+  int64_t burn_in;         /* iterates before the first window */
+  int64_t reproject_every; /* 0 = off */
+} mhar_run_config;
+
+typedef struct {
+  int64_t iterate_count; /* z * phi * windows (burn-in excluded), sampler.cpp:332 */
+  int64_t windows;
+  int64_t redraw_count;  /* direction redraw attempts, sampler.cpp:110 */
+  int64_t err_walk;      /* walk named by a failure, else -1 */
+  double seconds;        /* device time of the walk section (CUDA events) */
+} mhar_run_stats;
+
+/* run() with a warm start (sampler.cpp:274-335 with x0 in place of the
+ * Chebyshev center, :276/:300): state <- x0 replicated, burn-in, then per
+ * window phi iterates, a contains(eps_feas) check of every walk
+ * (NUMERICAL_FAILURE otherwise) and collection of the z walks as rows of
+ * samples ((windows*z) x n row-major, collection order).  samples may be NULL
+ * (throughput runs). */
+int mhar_run(mhar_ctx* ctx, const mhar_run_config* cfg, const double* x0, double* samples,
+             mhar_run_stats* stats);
+
+/* Host-side projector (projection.cpp:9-34 with linalg.cpp:21-52 LU + one
+ * refinement pass): P (n x n) and G = (A_E A_E')^-1 (m_eq x m_eq). */
+int mhar_compute_projection(const double* a_eq, int64_t m_eq, int64_t n, double* p, double* g);
+
+typedef struct {
+  int64_t iterations;      /* iterates executed by this context */
+  int64_t redraw_count;    /* total redraw attempts */
+  int64_t kernel_launches; /* kernels this library launched */
+  int64_t chord_launches;  /* launches of the chord (tensor-core) kernel */
+  double chord_ms;         /* summed device time of timed chord launches */
+  int64_t chord_timed;     /* chord launches covered by chord_ms */
+  double chord_flops;      /* algorithmic flops of those timed launches */
+  int64_t refreshes;       /* fused refresh passes (incremental mode) */
+  int64_t z, z_padded, m_padded, n_padded;
+} mhar_ctx_stats;
+
+int mhar_get_stats(mhar_ctx* ctx, mhar_ctx_stats* out);
+/* 1 = record CUDA events around every chord launch (on the launching stream) */
+int mhar_set_timing(mhar_ctx* ctx, int enabled);
+int mhar_reset_stats(mhar_ctx* ctx);
+
+/* Algorithmic flops of one iterate of this context's walks (4 m n z, + 2 n^2 z
+ * with equalities) and of its dominant chord launch. */
+double mhar_flops_per_iterate(mhar_ctx* ctx);
+
+const char* mhar_last_error(void);
+const char* mhar_version(void);
+int mhar_device_count(int* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,520 @@
+"""B200-native MHAR (Matrix Hit-and-Run) chain-step engine.
+
+Python mirror of the reference sampler interface
+(/root/reference/proj/include/mhar/{polytope,sampler,projection,errors}.hpp)
+over the engine's C ABI (include/mhar_b200.h, libmhar_b200.so).  Every
+computation runs in the CUDA library; there is no CPU fallback -- importing
+this package without the built library raises.
+
+    p = make_hypercube(10)
+    cfg = resolve(SamplerConfig(z=100, phi=1, t_target=100_000, burn_in=1000), p)
+    out = run(p, cfg, x0=np.zeros(10))          # SampleSet, like mhar::run
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "MharError", "ErrorCode", "Polytope", "SamplerConfig", "ProjectionOperator", "SampleSet",
+    "LambdaIntervals", "Engine", "WalkState", "resolve", "compute_projection", "run", "step",
+    "make_hypercube", "make_simplex", "contains", "library_path", "FLAG_DEGENERATE",
+    "FLAG_HAS_UPPER", "FLAG_HAS_LOWER", "FLAG_COLLAPSED", "FLAG_THETA_MIDPOINT",
+    "kDegenerateWidth", "kMaxDirectionRetries", "kNearZeroDirection",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(HERE, "lib", "libmhar_b200.so")
+
+# Constants mirrored from the reference headers.
+kDegenerateWidth = 1e-14      # sampler.hpp:40
+kMaxDirectionRetries = 16     # sampler.hpp:43
+kNearZeroDirection = 1e-12    # projection.hpp:25
+
+FLAG_DEGENERATE = 1
+FLAG_HAS_UPPER = 2
+FLAG_HAS_LOWER = 4
+FLAG_COLLAPSED = 8
+FLAG_THETA_MIDPOINT = 16
+
+RNG_PHILOX = 0
+RNG_REFERENCE = 1
+SLACK_RECOMPUTE = 0
+SLACK_INCREMENTAL = 1
+
+
+class ErrorCode:
+    """mhar::ErrorCode (proj/include/mhar/errors.hpp:10-24); status = 1 + ordinal."""
+    invalid_argument = 1
+    dimension_mismatch = 2
+    singular_matrix = 3
+    rank_deficient_eq = 4
+    empty_polytope = 5
+    no_interior = 6
+    unbounded_polytope = 7
+    direction_degenerate = 8
+    retry_exhausted = 9
+    cycle_suspected = 10
+    degenerate_test = 11
+    numerical_failure = 12
+    io_failure = 13
+    cuda = 100
+
+    NAMES = {1: "INVALID_ARGUMENT", 2: "DIMENSION_MISMATCH", 3: "SINGULAR_MATRIX",
+             4: "RANK_DEFICIENT_EQ", 5: "EMPTY_POLYTOPE", 6: "NO_INTERIOR",
+             7: "UNBOUNDED_POLYTOPE", 8: "DIRECTION_DEGENERATE", 9: "RETRY_EXHAUSTED",
+             10: "CYCLE_SUSPECTED", 11: "DEGENERATE_TEST", 12: "NUMERICAL_FAILURE",
+             13: "IO_FAILURE", 100: "CUDA_ERROR"}
+
+
+class MharError(RuntimeError):
+    """mhar::Error (errors.hpp:30-37): carries the ErrorCode status."""
+
+    def __init__(self, code: int, message: str):
+        super().__init__(message)
+        self.code = code
+
+    @property
+    def name(self) -> str:
+        return ErrorCode.NAMES.get(self.code, "UNKNOWN")
+
+
+# ------------------------------------------------------------ C ABI -------
+
+class _Polytope(C.Structure):
+    _fields_ = [("n", C.c_int64), ("m_in", C.c_int64), ("m_eq", C.c_int64),
+                ("a_in", C.POINTER(C.c_double)), ("b_in", C.POINTER(C.c_double)),
+                ("a_eq", C.POINTER(C.c_double)), ("b_eq", C.POINTER(C.c_double))]
+
+
+class _Options(C.Structure):
+    _fields_ = [("z", C.c_int64), ("chain_offset", C.c_int64), ("seed", C.c_uint64),
+                ("eps_dir", C.c_double), ("eps_feas", C.c_double), ("rng", C.c_int),
+                ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int)]
+
+
+class _RunConfig(C.Structure):
+    _fields_ = [("phi", C.c_int64), ("windows", C.c_int64), ("burn_in", C.c_int64),
+                ("reproject_every", C.c_int64)]
+
+
+class _RunStats(C.Structure):
+    _fields_ = [("iterate_count", C.c_int64), ("windows", C.c_int64),
+                ("redraw_count", C.c_int64), ("err_walk", C.c_int64), ("seconds", C.c_double)]
+
+
+class _CtxStats(C.Structure):
+    _fields_ = [("iterations", C.c_int64), ("redraw_count", C.c_int64),
+                ("kernel_launches", C.c_int64), ("chord_launches", C.c_int64),
+                ("chord_ms", C.c_double), ("chord_timed", C.c_int64),
+                ("chord_flops", C.c_double), ("refreshes", C.c_int64),
+                ("z", C.c_int64), ("z_padded", C.c_int64), ("m_padded", C.c_int64),
+                ("n_padded", C.c_int64)]
+
+
+_dp = C.POINTER(C.c_double)
+_u8p = C.POINTER(C.c_uint8)
+_i64p = C.POINTER(C.c_int64)
+
+# Every symbol include/mhar_b200.h declares (checked by tests/test_abi_exports.py).
+EXPORTED_SYMBOLS = [
+    "mhar_default_options", "mhar_ctx_create", "mhar_ctx_destroy", "mhar_set_state",
+    "mhar_get_state", "mhar_get_state_rows_device", "mhar_step", "mhar_sync", "mhar_step_timed",
+    "mhar_step_injected", "mhar_lambda_intervals", "mhar_check_state", "mhar_run",
+    "mhar_compute_projection", "mhar_get_stats", "mhar_set_timing", "mhar_reset_stats",
+    "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
+]
+
+_lib = None
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def lib():
+    """Loads libmhar_b200.so.  Raises if it is missing: no fallback path."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing; build it with "
+                          "`python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(_LIB_PATH)
+    L.mhar_default_options.argtypes = [C.POINTER(_Options)]
+    L.mhar_default_options.restype = None
+    L.mhar_ctx_create.argtypes = [C.POINTER(_Polytope), _dp, _dp, C.POINTER(_Options),
+                                  C.POINTER(C.c_void_p)]
+    L.mhar_ctx_destroy.argtypes = [C.c_void_p]
+    L.mhar_set_state.argtypes = [C.c_void_p, _dp]
+    L.mhar_get_state.argtypes = [C.c_void_p, _dp]
+    L.mhar_get_state_rows_device.argtypes = [C.c_void_p, C.c_void_p]
+    L.mhar_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+    L.mhar_sync.argtypes = [C.c_void_p]
+    L.mhar_step_timed.argtypes = [C.c_void_p, C.c_int64, C.c_int64, _dp]
+    L.mhar_step_injected.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _dp, _u8p]
+    L.mhar_lambda_intervals.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _u8p]
+    L.mhar_check_state.argtypes = [C.c_void_p, C.c_double, _i64p, _dp, _dp]
+    L.mhar_run.argtypes = [C.c_void_p, C.POINTER(_RunConfig), _dp, _dp, C.POINTER(_RunStats)]
+    L.mhar_compute_projection.argtypes = [_dp, C.c_int64, C.c_int64, _dp, _dp]
+    L.mhar_get_stats.argtypes = [C.c_void_p, C.POINTER(_CtxStats)]
+    L.mhar_set_timing.argtypes = [C.c_void_p, C.c_int]
+    L.mhar_reset_stats.argtypes = [C.c_void_p]
+    L.mhar_flops_per_iterate.argtypes = [C.c_void_p]
+    L.mhar_flops_per_iterate.restype = C.c_double
+    L.mhar_last_error.restype = C.c_char_p
+    L.mhar_version.restype = C.c_char_p
+    L.mhar_device_count.argtypes = [C.POINTER(C.c_int)]
+    for name in ("mhar_ctx_create", "mhar_ctx_destroy", "mhar_set_state", "mhar_get_state",
+                 "mhar_get_state_rows_device", "mhar_step", "mhar_sync", "mhar_step_timed",
+                 "mhar_step_injected",
+                 "mhar_lambda_intervals", "mhar_check_state", "mhar_run",
+                 "mhar_compute_projection", "mhar_get_stats", "mhar_set_timing",
+                 "mhar_reset_stats", "mhar_device_count"):
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != 0:
+        msg = lib().mhar_last_error().decode(errors="replace")
+        raise MharError(status, msg)
+
+
+def _d(a):
+    return None if a is None else a.ctypes.data_as(_dp)
+
+
+def _f(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+# -------------------------------------------------------------- types ------
+
+class Polytope:
+    """{x : a_in x <= b_in, a_eq x = b_eq} (polytope.hpp:12-25)."""
+
+    def __init__(self, a_in, b_in, a_eq=None, b_eq=None):
+        self.a_in = _f(a_in)
+        self.b_in = np.ascontiguousarray(b_in, dtype=np.float64).reshape(-1)
+        n = self.a_in.shape[1]
+        if a_eq is None:
+            self.a_eq = np.zeros((0, n), order="F")
+            self.b_eq = np.zeros(0)
+        else:
+            self.a_eq = _f(a_eq)
+            self.b_eq = np.ascontiguousarray(b_eq, dtype=np.float64).reshape(-1)
+
+    def dim(self) -> int:
+        return self.a_in.shape[1]
+
+    def num_inequalities(self) -> int:
+        return self.a_in.shape[0]
+
+    def num_equalities(self) -> int:
+        return self.a_eq.shape[0]
+
+
+def make_hypercube(n: int) -> Polytope:
+    """[-1, 1]^n as 2n rows (polytope.cpp:192-199)."""
+    if n < 1:
+        raise MharError(ErrorCode.invalid_argument, "make_hypercube: n must be >= 1")
+    return Polytope(np.vstack([np.eye(n), -np.eye(n)]), np.ones(2 * n))
+
+
+def make_simplex(n: int) -> Polytope:
+    """{x >= 0, sum x = 1} (polytope.cpp:201-208)."""
+    if n < 2:
+        raise MharError(ErrorCode.invalid_argument, "make_simplex: n must be >= 2")
+    return Polytope(-np.eye(n), np.zeros(n), np.ones((1, n)), np.ones(1))
+
+
+@dataclasses.dataclass
+class SamplerConfig:
+    """mhar::SamplerConfig (sampler.hpp:16-25); 0 / -1 sentinels resolve."""
+    z: int = 0
+    phi: int = 0
+    t_target: int = 1
+    seed: int = 0
+    eps_dir: float = 1e-11
+    eps_feas: float = 1e-9
+    reproject_every: int = -1
+    burn_in: int = -1
+
+
+def resolve(cfg: SamplerConfig, p: Polytope) -> SamplerConfig:
+    """resolve() (sampler.cpp:127-141)."""
+    r = dataclasses.replace(cfg)
+    n = p.dim()
+    walk_dim = n - p.num_equalities()
+    if r.z == 0:
+        r.z = max(p.num_inequalities(), n) + 1
+    if r.phi == 0:
+        r.phi = walk_dim ** 3
+    if r.burn_in < 0:
+        r.burn_in = r.phi
+    if r.reproject_every < 0:
+        r.reproject_every = r.phi
+    if r.z < 1:
+        raise MharError(ErrorCode.invalid_argument, "config: z must be >= 1")
+    if r.phi < 1:
+        raise MharError(ErrorCode.invalid_argument, "config: phi must be >= 1")
+    if r.t_target < 1:
+        raise MharError(ErrorCode.invalid_argument, "config: t_target must be >= 1")
+    if not r.eps_dir > 0.0:
+        raise MharError(ErrorCode.invalid_argument, "config: eps_dir must be > 0")
+    if not r.eps_feas > 0.0:
+        raise MharError(ErrorCode.invalid_argument, "config: eps_feas must be > 0")
+    return r
+
+
+@dataclasses.dataclass
+class ProjectionOperator:
+    """projection.hpp:11-15."""
+    p: np.ndarray
+    gram_inverse: np.ndarray
+    source_eq: np.ndarray
+
+
+def compute_projection(a_eq) -> ProjectionOperator:
+    """compute_projection (projection.cpp:9-34), host side as in the reference."""
+    a_eq = _f(a_eq)
+    me, n = a_eq.shape
+    if me == 0:
+        raise MharError(ErrorCode.invalid_argument,
+                        "compute_projection: equality matrix is empty")
+    P = np.empty((n, n), order="F")
+    G = np.empty((me, me), order="F")
+    _check(lib().mhar_compute_projection(_d(a_eq), me, n, _d(P), _d(G)))
+    return ProjectionOperator(P, G, a_eq.copy(order="F"))
+
+
+@dataclasses.dataclass
+class LambdaIntervals:
+    """sampler.hpp:33-37 (+ the MHAR_FLAG_* bits per walk)."""
+    lower: np.ndarray
+    upper: np.ndarray
+    degenerate: np.ndarray
+    flags: np.ndarray
+
+
+@dataclasses.dataclass
+class WalkState:
+    """sampler.hpp:69-74."""
+    x: np.ndarray
+    t: int = 0
+    j: int = 0
+    redraws: int = 0
+
+
+@dataclasses.dataclass
+class SampleSet:
+    """sampler.hpp:82-91."""
+    samples: np.ndarray
+    config: SamplerConfig
+    start: np.ndarray
+    start_radius: float
+    seconds: float
+    iterate_count: int
+    windows: int
+    redraw_count: int
+
+
+# ------------------------------------------------------------- engine ------
+
+class Engine:
+    """One device context: the polytope resident in HBM plus z walks.
+
+    rng: "philox" (default; keyed on global walk ids so shards are
+    independent of the GPU count) or "reference" (the reference's SplitMix
+    streams: column stream k and the shared theta stream, rng.hpp:42-55).
+    slack: "incremental" (default) or "recompute" (one fused A_I[X|D] pass
+    per iterate).
+    """
+
+    def __init__(self, p: Polytope, z: int, seed: int = 0, projector: Optional[ProjectionOperator] = None,
+                 eps_dir: float = 1e-11, eps_feas: float = 1e-9, rng: str = "philox",
+                 slack: str = "incremental", refresh_every: int = 128, device: int = 0,
+                 chain_offset: int = 0):
+        L = lib()
+        self.p = p
+        self.n = p.dim()
+        self.z = int(z)
+        self._keep = []
+        poly = _Polytope()
+        poly.n = self.n
+        poly.m_in = p.num_inequalities()
+        poly.m_eq = p.num_equalities()
+        poly.a_in = _d(p.a_in)
+        poly.b_in = _d(p.b_in)
+        if poly.m_eq > 0:
+            poly.a_eq = _d(p.a_eq)
+            poly.b_eq = _d(p.b_eq)
+        opt = _Options()
+        L.mhar_default_options(C.byref(opt))
+        opt.z = self.z
+        opt.chain_offset = int(chain_offset)
+        opt.seed = int(seed) & (2**64 - 1)
+        opt.eps_dir = eps_dir
+        opt.eps_feas = eps_feas
+        opt.rng = {"philox": RNG_PHILOX, "reference": RNG_REFERENCE}[rng]
+        opt.slack_mode = {"recompute": SLACK_RECOMPUTE, "incremental": SLACK_INCREMENTAL}[slack]
+        opt.refresh_every = int(refresh_every)
+        opt.device = int(device)
+        P = G = None
+        if projector is not None:
+            P = _f(projector.p)
+            G = _f(projector.gram_inverse)
+        h = C.c_void_p()
+        _check(L.mhar_ctx_create(C.byref(poly), _d(P), _d(G), C.byref(opt), C.byref(h)))
+        self._h = h
+        self.eps_feas = eps_feas
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mhar_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # state
+    def set_state(self, x):
+        x = _f(x)
+        if x.shape != (self.n, self.z):
+            raise MharError(ErrorCode.dimension_mismatch,
+                            f"set_state: x is {x.shape}, expected {(self.n, self.z)}")
+        _check(lib().mhar_set_state(self._h, _d(x)))
+
+    def get_state(self) -> np.ndarray:
+        x = np.empty((self.n, self.z), order="F")
+        _check(lib().mhar_get_state(self._h, _d(x)))
+        return x
+
+    def state_rows_to_device(self, dev_ptr: int):
+        """Row-major z x n copy of the walks into caller-owned device memory."""
+        _check(lib().mhar_get_state_rows_device(self._h, C.c_void_p(dev_ptr)))
+
+    # iterates
+    def step(self, iters: int = 1, reproject_every: int = 0, sync: bool = True):
+        _check(lib().mhar_step(self._h, int(iters), int(reproject_every)))
+        if sync:
+            self.sync()
+
+    def sync(self):
+        _check(lib().mhar_sync(self._h))
+
+    def step_timed(self, iters: int = 1, reproject_every: int = 0) -> float:
+        """Iterates bracketed by CUDA events on the engine's stream; device ms."""
+        ms = C.c_double(0.0)
+        _check(lib().mhar_step_timed(self._h, int(iters), int(reproject_every), C.byref(ms)))
+        return ms.value
+
+    def step_injected(self, H, U):
+        """Test hook: returns (lower, upper, theta, flags); moves the state."""
+        H = _f(H)
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        lo, hi, th = np.empty(self.z), np.empty(self.z), np.empty(self.z)
+        fl = np.empty(self.z, np.uint8)
+        _check(lib().mhar_step_injected(self._h, _d(H), _d(U), _d(lo), _d(hi), _d(th),
+                                        fl.ctypes.data_as(_u8p)))
+        return lo, hi, th, fl
+
+    def lambda_intervals(self, X, D) -> LambdaIntervals:
+        X, D = _f(X), _f(D)
+        lo, hi = np.empty(self.z), np.empty(self.z)
+        fl = np.empty(self.z, np.uint8)
+        _check(lib().mhar_lambda_intervals(self._h, _d(X), _d(D), _d(lo), _d(hi),
+                                           fl.ctypes.data_as(_u8p)))
+        return LambdaIntervals(lo, hi, (fl & FLAG_DEGENERATE).astype(np.uint8), fl)
+
+    def check_state(self, eps: float):
+        """(first_bad or -1, max_i (A x - b)_i per walk, max |A_E x - b_E| per walk)."""
+        fb = C.c_int64(-1)
+        mv, me = np.empty(self.z), np.empty(self.z)
+        _check(lib().mhar_check_state(self._h, eps, C.byref(fb), _d(mv), _d(me)))
+        return fb.value, mv, me
+
+    def run(self, x0, phi: int, windows: int, burn_in: int = 0, reproject_every: int = 0,
+            collect: bool = True):
+        cfg = _RunConfig(int(phi), int(windows), int(burn_in), int(reproject_every))
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        samples = np.empty((windows * self.z, self.n)) if collect else None
+        st = _RunStats()
+        _check(lib().mhar_run(self._h, C.byref(cfg), _d(x0), _d(samples), C.byref(st)))
+        return samples, st
+
+    def stats(self) -> dict:
+        s = _CtxStats()
+        _check(lib().mhar_get_stats(self._h, C.byref(s)))
+        return {f[0]: getattr(s, f[0]) for f in s._fields_}
+
+    def set_timing(self, on: bool):
+        _check(lib().mhar_set_timing(self._h, 1 if on else 0))
+
+    def reset_stats(self):
+        _check(lib().mhar_reset_stats(self._h))
+
+    def flops_per_iterate(self) -> float:
+        return lib().mhar_flops_per_iterate(self._h)
+
+
+# ------------------------------------------------ reference-style calls ----
+
+def step(p: Polytope, projector: Optional[ProjectionOperator], cfg: SamplerConfig,
+         engine: Engine, state: WalkState):
+    """step() (sampler.hpp:79-80) on an engine holding the walks' RNG:
+    state.x is uploaded, advanced one iterate on the device, and read back."""
+    engine.set_state(state.x)
+    before = engine.stats()["redraw_count"]
+    engine.step(1)
+    state.x = engine.get_state()
+    state.j += 1
+    state.redraws += engine.stats()["redraw_count"] - before
+
+
+def contains(p: Polytope, x, eps: float) -> bool:
+    """contains() (polytope.cpp:177-190), evaluated on the host for one point
+    (API completeness; the engine checks every walk on the device)."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape[0] != p.dim():
+        raise MharError(ErrorCode.dimension_mismatch, "contains: dimension mismatch")
+    if p.num_inequalities() and (p.a_in @ x - p.b_in).max() > eps:
+        return False
+    if p.num_equalities() and np.abs(p.a_eq @ x - p.b_eq).max() > eps:
+        return False
+    return True
+
+
+def run(p: Polytope, cfg: SamplerConfig, x0=None, rng: str = "philox", slack: str = "incremental",
+        device: int = 0) -> SampleSet:
+    """run() (sampler.cpp:274-335) on one B200.  x0 is the warm start that
+    replaces the reference's Chebyshev-center LP (sampler.cpp:276); it is
+    required (the dense-tableau LP does not scale to the target configs)."""
+    rc = resolve(cfg, p)
+    if x0 is None:
+        raise MharError(ErrorCode.invalid_argument,
+                        "run: a warm start x0 is required (Chebyshev centering is out of scope)")
+    projector = compute_projection(p.a_eq) if p.num_equalities() > 0 else None
+    windows = (rc.t_target + rc.z - 1) // rc.z
+    with Engine(p, rc.z, seed=rc.seed, projector=projector, eps_dir=rc.eps_dir,
+                eps_feas=rc.eps_feas, rng=rng, slack=slack, device=device) as eng:
+        samples, st = eng.run(x0, rc.phi, windows, rc.burn_in,
+                              rc.reproject_every if projector is not None else 0)
+    return SampleSet(samples=samples, config=rc, start=np.asarray(x0, dtype=np.float64),
+                     start_radius=0.0, seconds=st.seconds, iterate_count=st.iterate_count,
+                     windows=st.windows, redraw_count=st.redraw_count)

@@ -1,0 +1,933 @@
+// abi.cu -- the C ABI (include/mhar_b200.h): context, device memory, and
+// the per-iterate launch sequence of the MHAR engine on one B200.
+//
+// One iterate (reference step(), /root/reference/proj/src/sampler.cpp:235-272):
+//   normals (Philox | reference streams) -> [project P H, collapse flags]
+//   -> chord kernel (DMMA A_I [X|D] or A_I D + slack cache, fused bounds)
+//   -> finalize (intervals, unbounded check, redraw queue)
+//   -> redraw (slow path, usually empty) -> theta (+ fix-up) -> x += theta d
+//   -> [reprojection every reproject_every iterates]
+// All launches are queued on the context's stream without host syncs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mhar_b200.h"
+#include "chord_kernel.cuh"
+#include "host_linalg.h"
+#include "step_kernels.cuh"
+
+using namespace mhar_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+const char* code_name(int st) {
+  switch (st) {
+    case 1: return "INVALID_ARGUMENT";
+    case 2: return "DIMENSION_MISMATCH";
+    case 3: return "SINGULAR_MATRIX";
+    case 4: return "RANK_DEFICIENT_EQ";
+    case 7: return "UNBOUNDED_POLYTOPE";
+    case 8: return "DIRECTION_DEGENERATE";
+    case 9: return "RETRY_EXHAUSTED";
+    case 12: return "NUMERICAL_FAILURE";
+    default: return "ERROR";
+  }
+}
+
+#define CK(call)                                                                       \
+  do {                                                                                 \
+    cudaError_t e_ = (call);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(MHAR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+struct mhar_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  mhar_options opt{};
+  int64_t n = 0, m = 0, me = 0, z = 0;
+  int64_t n_pad = 0, KT = 0, m_pad = 0, m_tiles = 0, z_pad = 0, ct64 = 0, ct128 = 0;
+  int64_t p_rows_pad = 0;
+
+  // device buffers
+  double *A = nullptr, *b = nullptr, *X = nullptr, *D = nullptr, *H = nullptr;
+  double *Xtmp = nullptr;
+  double *Ppk = nullptr, *Pcm = nullptr, *AE = nullptr, *bE = nullptr, *G = nullptr;
+  double *S = nullptr, *R = nullptr;
+  double *theta = nullptr, *lower = nullptr, *upper = nullptr, *viol = nullptr;
+  double *eqres = nullptr, *eqg = nullptr, *eqviol = nullptr, *rows = nullptr;
+  double *redraw_scratch = nullptr, *x0 = nullptr, *injected_u = nullptr;
+  long long *hi_key = nullptr, *lo_key = nullptr, *viol_key = nullptr;
+  unsigned *sides = nullptr, *flags = nullptr, *collapsed = nullptr;
+  int *redraw_list = nullptr, *redraw_count = nullptr, *attempts = nullptr;
+  int *first_reject = nullptr, *first_bad = nullptr;
+  unsigned long long *err = nullptr, *redraw_total = nullptr;
+  uint64_t *col_state = nullptr, *theta_state = nullptr;
+  int redraw_grid = 1;
+
+  // host bookkeeping
+  int64_t iterations = 0;
+  bool slack_valid = false;
+  int64_t since_refresh = 0;
+  int64_t launches = 0, chord_launches = 0, refreshes = 0;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+  std::vector<double> pending_flops;
+  double chord_flops = 0.0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> event_pool;
+  double chord_ms = 0.0;
+  int64_t chord_timed = 0;
+  std::vector<void*> allocs;
+};
+
+namespace {
+
+template <typename T>
+int dalloc(mhar_ctx* c, T** p, size_t count) {
+  void* q = nullptr;
+  const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+  cudaError_t e = cudaMalloc(&q, bytes);
+  if (e != cudaSuccess)
+    return fail(MHAR_ERR_CUDA, "cudaMalloc(" + std::to_string(bytes) + " B): " +
+                                   cudaGetErrorString(e));
+  c->allocs.push_back(q);
+  *p = static_cast<T*>(q);
+  return 0;
+}
+
+inline int blocks_for(int64_t work, int threads, int cap) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (int)b;
+}
+
+int launch_check(mhar_ctx* c, const char* what) {
+  ++c->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(MHAR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return 0;
+}
+
+#define LAUNCH_OK(c, what)                 \
+  do {                                     \
+    int s_ = launch_check((c), (what));    \
+    if (s_) return s_;                     \
+  } while (0)
+
+void harvest_timing(mhar_ctx* c) {
+  for (size_t i = 0; i < c->pending.size(); ++i) {
+    auto& ev = c->pending[i];
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, ev.first, ev.second) == cudaSuccess) {
+      c->chord_ms += ms;
+      c->chord_flops += c->pending_flops[i];
+      ++c->chord_timed;
+    }
+    c->event_pool.push_back(ev);
+  }
+  c->pending.clear();
+  c->pending_flops.clear();
+}
+
+std::pair<cudaEvent_t, cudaEvent_t> take_events(mhar_ctx* c) {
+  if (!c->event_pool.empty()) {
+    auto e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  std::pair<cudaEvent_t, cudaEvent_t> e;
+  cudaEventCreate(&e.first);
+  cudaEventCreate(&e.second);
+  return e;
+}
+
+ChordParams chord_params(mhar_ctx* c, const double* X) {
+  ChordParams p;
+  p.A = c->A;
+  p.X = X;
+  p.D = c->D;
+  p.b = c->b;
+  p.S = c->S;
+  p.R = c->R;
+  p.theta_prev = c->theta;
+  p.hi_key = c->hi_key;
+  p.lo_key = c->lo_key;
+  p.viol_key = c->viol_key;
+  p.sides = c->sides;
+  p.err = c->err;
+  p.m_tiles = c->m_tiles;
+  p.KT = c->KT;
+  p.ct128 = c->ct128;
+  p.z = c->z;
+  p.eps_dir = c->opt.eps_dir;
+  p.group_m = 16;
+  return p;
+}
+
+int launch_chord(mhar_ctx* c, int mode, const double* X) {
+  ChordParams p = chord_params(c, X);
+  p.col_tiles = (mode == FUSED || mode == FUSED_STORE) ? c->ct64 : c->ct128;
+  const int64_t units = p.m_tiles * p.col_tiles;
+  const int grid = (int)std::min<int64_t>(units, c->num_sms);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (c->timing) {
+    ev = take_events(c);
+    cudaEventRecord(ev.first, c->stream);
+  }
+  switch (mode) {
+    case FUSED:
+      chord_kernel<FUSED><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
+      break;
+    case FUSED_STORE:
+      chord_kernel<FUSED_STORE><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
+      break;
+    case INCREMENTAL:
+      chord_kernel<INCREMENTAL><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
+      break;
+    default:
+      chord_kernel<CHECK><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
+      break;
+  }
+  LAUNCH_OK(c, "chord_kernel");
+  ++c->chord_launches;
+  if (c->timing) {
+    cudaEventRecord(ev.second, c->stream);
+    c->pending.push_back(ev);
+    // algorithmic flops of this launch: 2 m n per product column
+    const double cols = (mode == FUSED || mode == FUSED_STORE) ? 2.0 * c->z : (double)c->z;
+    c->pending_flops.push_back(2.0 * (double)c->m * (double)c->n * cols);
+  }
+  return 0;
+}
+
+int launch_finalize(mhar_ctx* c, bool queue_redraws, bool advance_streams) {
+  FinalizeParams fp;
+  fp.hi_key = c->hi_key;
+  fp.lo_key = c->lo_key;
+  fp.viol_key = c->viol_key;
+  fp.sides = c->sides;
+  fp.collapsed = c->me > 0 ? c->collapsed : nullptr;
+  fp.lower = c->lower;
+  fp.upper = c->upper;
+  fp.viol = c->viol;
+  fp.flags = c->flags;
+  fp.redraw_list = queue_redraws ? c->redraw_list : nullptr;
+  fp.redraw_count = c->redraw_count;
+  fp.err = c->err;
+  fp.col_state = (advance_streams && c->opt.rng == MHAR_RNG_REFERENCE) ? c->col_state : nullptr;
+  fp.draws_per_walk = 2 * ((c->n + 1) / 2);
+  fp.z = c->z;
+  finalize_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(fp);
+  LAUNCH_OK(c, "finalize_kernel");
+  return 0;
+}
+
+int launch_normals(mhar_ctx* c, double* out) {
+  RngParams rp;
+  rp.seed = c->opt.seed;
+  rp.iterate = (uint64_t)c->iterations;
+  rp.chain_offset = c->opt.chain_offset;
+  rp.n = c->n;
+  rp.z = c->z;
+  rp.KT = c->KT;
+  rp.mode = c->opt.rng;
+  rp.col_state = c->col_state;
+  const int64_t work = ((c->n + 1) / 2) * c->z;
+  normals_kernel<<<blocks_for(work, 256, c->num_sms * 16), 256, 0, c->stream>>>(rp, out, c->err);
+  LAUNCH_OK(c, "normals_kernel");
+  return 0;
+}
+
+// D = P H and collapse flags (sampler.cpp:244-250).
+int launch_projection(mhar_ctx* c) {
+  dim3 grid((unsigned)(c->p_rows_pad / BM), (unsigned)c->ct64);
+  project_kernel<<<grid, 256, 0, c->stream>>>(c->Ppk, c->H, c->D, c->n, c->KT, c->err);
+  LAUNCH_OK(c, "project_kernel");
+  collapse_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
+      c->D, c->n, c->z, c->KT, c->collapsed, c->err);
+  LAUNCH_OK(c, "collapse_kernel");
+  return 0;
+}
+
+int launch_redraw(mhar_ctx* c) {
+  RedrawParams rp;
+  rp.A = c->A;
+  rp.b = c->b;
+  rp.X = c->X;
+  rp.D = c->D;
+  rp.P = c->me > 0 ? c->Pcm : nullptr;
+  rp.R = (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) ? c->R : nullptr;
+  rp.ct128 = c->ct128;
+  rp.scratch = c->redraw_scratch;
+  rp.lower = c->lower;
+  rp.upper = c->upper;
+  rp.flags = c->flags;
+  rp.redraw_list = c->redraw_list;
+  rp.redraw_count = c->redraw_count;
+  rp.attempts = c->attempts;
+  rp.redraw_total = c->redraw_total;
+  rp.err = c->err;
+  rp.seed = c->opt.seed;
+  rp.iterate = (uint64_t)c->iterations;
+  rp.chain_offset = c->opt.chain_offset;
+  rp.col_state = c->col_state;
+  rp.mode = c->opt.rng;
+  rp.n = c->n;
+  rp.m = c->m;
+  rp.KT = c->KT;
+  rp.eps_dir = c->opt.eps_dir;
+  redraw_kernel<<<c->redraw_grid, 256, 0, c->stream>>>(rp);
+  LAUNCH_OK(c, "redraw_kernel");
+  return 0;
+}
+
+ThetaParams theta_params(mhar_ctx* c, const double* injected_u) {
+  ThetaParams tp;
+  tp.lower = c->lower;
+  tp.upper = c->upper;
+  tp.flags = c->flags;
+  tp.theta = c->theta;
+  tp.err = c->err;
+  tp.seed = c->opt.seed;
+  tp.iterate = (uint64_t)c->iterations;
+  tp.chain_offset = c->opt.chain_offset;
+  tp.z = c->z;
+  tp.mode = c->opt.rng;
+  tp.theta_state = c->theta_state;
+  tp.first_reject = c->first_reject;
+  tp.injected_u = injected_u;
+  return tp;
+}
+
+int launch_theta_and_move(mhar_ctx* c, const double* injected_u) {
+  ThetaParams tp = theta_params(c, injected_u);
+  theta_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(tp);
+  LAUNCH_OK(c, "theta_kernel");
+  if (!injected_u && c->opt.rng == MHAR_RNG_REFERENCE) {
+    theta_fixup_kernel<<<1, 1, 0, c->stream>>>(tp);
+    LAUNCH_OK(c, "theta_fixup_kernel");
+  }
+  const int64_t total2 = c->z_pad * c->KT * BK / 2;
+  axpy_kernel<<<blocks_for(total2, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->X, c->D, c->theta, total2, c->KT, c->err);
+  LAUNCH_OK(c, "axpy_kernel");
+  return 0;
+}
+
+// reproject_points (projection.cpp:53-60) on the packed state.
+int launch_reproject(mhar_ctx* c) {
+  const int64_t mz = c->me * c->z;
+  eq_residual_kernel<<<blocks_for(mz, 256, 1 << 30), 256, 0, c->stream>>>(
+      c->AE, c->bE, c->X, c->me, c->n, c->z, c->KT, c->eqres);
+  LAUNCH_OK(c, "eq_residual_kernel");
+  eq_gram_kernel<<<blocks_for(mz, 256, 1 << 30), 256, 0, c->stream>>>(c->G, c->eqres, c->me,
+                                                                       c->z, c->eqg);
+  LAUNCH_OK(c, "eq_gram_kernel");
+  eq_correct_kernel<<<blocks_for(c->n * c->z, 256, 1 << 30), 256, 0, c->stream>>>(
+      c->AE, c->eqg, c->X, c->me, c->n, c->z, c->KT);
+  LAUNCH_OK(c, "eq_correct_kernel");
+  c->slack_valid = false;
+  return 0;
+}
+
+// One iterate of every walk.  injected_h (device, packed) / injected_u
+// (device) replace the RNG for the test hook.
+int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
+  CK(cudaMemsetAsync(c->redraw_count, 0, sizeof(int), c->stream));
+  if (!injected) {
+    int s = launch_normals(c, c->me > 0 ? c->H : c->D);
+    if (s) return s;
+  }
+  if (c->me > 0) {
+    int s = launch_projection(c);
+    if (s) return s;
+  }
+  int mode = FUSED;
+  if (!injected && c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
+    const int64_t every = c->opt.refresh_every > 0 ? c->opt.refresh_every : 128;
+    if (!c->slack_valid || c->since_refresh >= every) {
+      mode = FUSED_STORE;
+      c->slack_valid = true;
+      c->since_refresh = 0;
+      ++c->refreshes;
+    } else {
+      mode = INCREMENTAL;
+    }
+    ++c->since_refresh;
+  } else if (injected) {
+    c->slack_valid = false;
+  }
+  int s = launch_chord(c, mode, c->X);
+  if (s) return s;
+  s = launch_finalize(c, !injected, !injected);
+  if (s) return s;
+  if (!injected) {
+    s = launch_redraw(c);
+    if (s) return s;
+  }
+  s = launch_theta_and_move(c, injected ? c->injected_u : nullptr);
+  if (s) return s;
+  ++c->iterations;
+  if (!injected && c->me > 0 && reproject_every > 0 && c->iterations % reproject_every == 0) {
+    s = launch_reproject(c);
+    if (s) return s;
+  }
+  return 0;
+}
+
+// Decodes the device error word into a status (and message).
+int read_error(mhar_ctx* c, int64_t* walk) {
+  unsigned long long w = kNoError;
+  CK(cudaMemcpyAsync(&w, c->err, sizeof(w), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->timing) harvest_timing(c);
+  if (w == kNoError) return 0;
+  const int status = (int)(w & 0xFF);
+  const int64_t k = (int64_t)((w >> 8) & ((1ULL << 48) - 1));
+  if (walk) *walk = k;
+  std::string what;
+  switch (status) {
+    case ST_UNBOUNDED:
+      what = "chord is unbounded on one side; the polytope is not bounded";
+      break;
+    case ST_RETRY_EXHAUSTED:
+      what = "no usable direction after 16 redraws";
+      break;
+    case ST_NUMERICAL:
+      what = "walk left the polytope at a collection";
+      break;
+    default:
+      what = "device error";
+  }
+  return fail(status, std::string(code_name(status)) + ": walk " +
+                          std::to_string(k + c->opt.chain_offset) + ": " + what);
+}
+
+int clear_error(mhar_ctx* c) {
+  CK(cudaMemsetAsync(c->err, 0xFF, sizeof(unsigned long long), c->stream));
+  return 0;
+}
+
+int upload_state_host(mhar_ctx* c, const double* x_host, double* dst) {
+  double* tmp = c->rows;  // n x z staging
+  CK(cudaMemcpyAsync(tmp, x_host, sizeof(double) * c->n * c->z, cudaMemcpyHostToDevice,
+                     c->stream));
+  const int64_t total = c->z_pad * c->KT * BK;
+  pack_b_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      tmp, c->n, c->z, c->z_pad, c->KT, dst);
+  LAUNCH_OK(c, "pack_b_kernel");
+  return 0;
+}
+
+int reset_streams(mhar_ctx* c) {
+  if (c->opt.rng != MHAR_RNG_REFERENCE) return 0;
+  std::vector<uint64_t> st(c->z);
+  for (int64_t k = 0; k < c->z; ++k) st[k] = stream_init(c->opt.seed, (uint64_t)(c->opt.chain_offset + k));
+  const uint64_t th = stream_init(c->opt.seed, ~0ULL);  // WalkRng::kThetaStreamId
+  CK(cudaMemcpyAsync(c->col_state, st.data(), sizeof(uint64_t) * c->z, cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(c->theta_state, &th, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+void mhar_default_options(mhar_options* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->z = 1;
+  o->eps_dir = 1e-11;
+  o->eps_feas = 1e-9;
+  o->rng = MHAR_RNG_PHILOX;
+  o->slack_mode = MHAR_SLACK_INCREMENTAL;
+  o->refresh_every = 128;
+  o->device = 0;
+}
+
+const char* mhar_last_error(void) { return g_last_error.c_str(); }
+const char* mhar_version(void) { return "mhar_b200 0.1 (sm_100a, fp64 DMMA)"; }
+
+int mhar_device_count(int* count) {
+  CK(cudaGetDeviceCount(count));
+  return 0;
+}
+
+int mhar_compute_projection(const double* a_eq, int64_t m_eq, int64_t n, double* p, double* g) {
+  if (!a_eq || !p || !g || n < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "compute_projection: null argument");
+  std::string msg;
+  const int st = mhar_host::compute_projection(a_eq, m_eq, n, p, g, &msg);
+  if (st) return fail(st, std::string(code_name(st)) + ": " + msg);
+  return 0;
+}
+
+int mhar_ctx_create(const mhar_polytope* p, const double* projector, const double* gram_inverse,
+                    const mhar_options* opt, mhar_ctx** out) {
+  if (!p || !opt || !out) return fail(MHAR_ERR_INVALID_ARGUMENT, "ctx_create: null argument");
+  *out = nullptr;
+  if (p->n < 1 || p->m_in < 1 || p->m_eq < 0 || !p->a_in || !p->b_in)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "ctx_create: polytope needs n >= 1 and m_in >= 1");
+  if (p->m_eq > 0 && (!p->a_eq || !p->b_eq))
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "ctx_create: a_eq/b_eq missing");
+  if (opt->z < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: z must be >= 1");
+  if (!(opt->eps_dir > 0.0)) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: eps_dir must be > 0");
+  if (!(opt->eps_feas > 0.0)) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: eps_feas must be > 0");
+  if (opt->rng != MHAR_RNG_PHILOX && opt->rng != MHAR_RNG_REFERENCE)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "options: unknown rng");
+
+  mhar_ctx* c = new mhar_ctx();
+  c->opt = *opt;
+  c->device = opt->device;
+  c->n = p->n;
+  c->m = p->m_in;
+  c->me = p->m_eq;
+  c->z = opt->z;
+  auto bail = [&](int st) {
+    mhar_ctx_destroy(c);
+    return st;
+  };
+  cudaError_t e = cudaSetDevice(c->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(MHAR_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return fail(MHAR_ERR_CUDA, "cudaStreamCreate failed");
+  }
+
+  c->n_pad = round_up(c->n, BK);
+  c->KT = c->n_pad / BK;
+  c->m_pad = round_up(c->m, BM);
+  c->m_tiles = c->m_pad / BM;
+  c->z_pad = round_up(c->z, 128);
+  c->ct64 = c->z_pad / 64;
+  c->ct128 = c->z_pad / 128;
+  c->p_rows_pad = round_up(c->n, BM);
+
+  const size_t nzp = (size_t)c->z_pad * c->n_pad;
+  int st = 0;
+  if ((st = dalloc(c, &c->A, (size_t)c->m_pad * c->n_pad)) ||
+      (st = dalloc(c, &c->b, c->m_pad)) || (st = dalloc(c, &c->X, nzp)) ||
+      (st = dalloc(c, &c->D, nzp)) || (st = dalloc(c, &c->theta, c->z_pad)) ||
+      (st = dalloc(c, &c->lower, c->z_pad)) || (st = dalloc(c, &c->upper, c->z_pad)) ||
+      (st = dalloc(c, &c->viol, c->z_pad)) || (st = dalloc(c, &c->eqviol, c->z_pad)) ||
+      (st = dalloc(c, &c->rows, std::max<size_t>((size_t)c->n * c->z, (size_t)c->m * 1))) ||
+      (st = dalloc(c, &c->hi_key, c->z_pad)) || (st = dalloc(c, &c->lo_key, c->z_pad)) ||
+      (st = dalloc(c, &c->viol_key, c->z_pad)) || (st = dalloc(c, &c->sides, c->z_pad)) ||
+      (st = dalloc(c, &c->flags, c->z_pad)) || (st = dalloc(c, &c->collapsed, c->z_pad)) ||
+      (st = dalloc(c, &c->redraw_list, c->z_pad)) || (st = dalloc(c, &c->redraw_count, 1)) ||
+      (st = dalloc(c, &c->attempts, c->z_pad)) || (st = dalloc(c, &c->first_reject, 1)) ||
+      (st = dalloc(c, &c->first_bad, 1)) || (st = dalloc(c, &c->err, 1)) ||
+      (st = dalloc(c, &c->redraw_total, 1)) || (st = dalloc(c, &c->col_state, c->z_pad)) ||
+      (st = dalloc(c, &c->theta_state, 1)) || (st = dalloc(c, &c->x0, c->n)) ||
+      (st = dalloc(c, &c->injected_u, c->z_pad)))
+    return bail(st);
+  c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
+  if ((st = dalloc(c, &c->redraw_scratch, (size_t)c->redraw_grid * 3 * c->n))) return bail(st);
+  if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
+    const size_t cache = (size_t)c->m_pad * c->z_pad;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    if (2 * cache * sizeof(double) + (1ull << 30) > free_b) {
+      c->opt.slack_mode = MHAR_SLACK_RECOMPUTE;  // not enough HBM for the slack cache
+    } else if ((st = dalloc(c, &c->S, cache)) || (st = dalloc(c, &c->R, cache))) {
+      return bail(st);
+    }
+  }
+
+  // polytope upload: A_I column-major -> packed tiles, b padded with +inf
+  {
+    double* tmp = nullptr;
+    e = cudaMalloc(&tmp, sizeof(double) * (size_t)c->m * c->n);
+    if (e != cudaSuccess) return bail(fail(MHAR_ERR_CUDA, "cudaMalloc(A staging) failed"));
+    cudaMemcpy(tmp, p->a_in, sizeof(double) * (size_t)c->m * c->n, cudaMemcpyHostToDevice);
+    const int64_t total = c->m_pad * c->KT * BK;
+    pack_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
+        tmp, c->m, c->n, c->m, c->m_pad, c->KT, c->A);
+    ++c->launches;
+    cudaStreamSynchronize(c->stream);
+    cudaFree(tmp);
+    std::vector<double> bp(c->m_pad, __builtin_huge_val());
+    std::memcpy(bp.data(), p->b_in, sizeof(double) * c->m);
+    cudaMemcpy(c->b, bp.data(), sizeof(double) * c->m_pad, cudaMemcpyHostToDevice);
+  }
+  if (c->me > 0) {
+    std::vector<double> P((size_t)c->n * c->n), G((size_t)c->me * c->me);
+    if (projector && gram_inverse) {
+      std::memcpy(P.data(), projector, sizeof(double) * P.size());
+      std::memcpy(G.data(), gram_inverse, sizeof(double) * G.size());
+    } else {
+      std::string msg;
+      const int ps = mhar_host::compute_projection(p->a_eq, c->me, c->n, P.data(), G.data(), &msg);
+      if (ps) return bail(fail(ps, std::string(code_name(ps)) + ": " + msg));
+    }
+    if ((st = dalloc(c, &c->H, nzp)) || (st = dalloc(c, &c->Ppk, (size_t)c->p_rows_pad * c->n_pad)) ||
+        (st = dalloc(c, &c->Pcm, (size_t)c->n * c->n)) ||
+        (st = dalloc(c, &c->AE, (size_t)c->me * c->n)) || (st = dalloc(c, &c->bE, c->me)) ||
+        (st = dalloc(c, &c->G, (size_t)c->me * c->me)) ||
+        (st = dalloc(c, &c->eqres, (size_t)c->me * c->z)) ||
+        (st = dalloc(c, &c->eqg, (size_t)c->me * c->z)))
+      return bail(st);
+    cudaMemcpy(c->Pcm, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice);
+    cudaMemcpy(c->AE, p->a_eq, sizeof(double) * c->me * c->n, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->bE, p->b_eq, sizeof(double) * c->me, cudaMemcpyHostToDevice);
+    cudaMemcpy(c->G, G.data(), sizeof(double) * G.size(), cudaMemcpyHostToDevice);
+    const int64_t total = c->p_rows_pad * c->KT * BK;
+    pack_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
+        c->Pcm, c->n, c->n, c->n, c->p_rows_pad, c->KT, c->Ppk);
+    ++c->launches;
+    cudaMemsetAsync(c->H, 0, sizeof(double) * nzp, c->stream);
+  }
+  cudaMemsetAsync(c->X, 0, sizeof(double) * nzp, c->stream);
+  cudaMemsetAsync(c->D, 0, sizeof(double) * nzp, c->stream);
+  cudaMemsetAsync(c->theta, 0, sizeof(double) * c->z_pad, c->stream);
+  cudaMemsetAsync(c->collapsed, 0, sizeof(unsigned) * c->z_pad, c->stream);
+  cudaMemsetAsync(c->redraw_total, 0, sizeof(unsigned long long), c->stream);
+  cudaMemsetAsync(c->err, 0xFF, sizeof(unsigned long long), c->stream);
+  int big = 0x7FFFFFFF;
+  cudaMemcpyAsync(c->first_reject, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  fill_keys_kernel<<<blocks_for(c->z_pad, 256, 1 << 20), 256, 0, c->stream>>>(
+      c->hi_key, c->lo_key, c->viol_key, c->sides, c->z_pad);
+  ++c->launches;
+  cudaFuncSetAttribute(chord_kernel<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
+  cudaFuncSetAttribute(chord_kernel<FUSED_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
+  cudaFuncSetAttribute(chord_kernel<INCREMENTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
+  cudaFuncSetAttribute(chord_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
+  if ((st = reset_streams(c))) return bail(st);
+  e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) return bail(fail(MHAR_ERR_CUDA, std::string("ctx_create: ") + cudaGetErrorString(e)));
+  *out = c;
+  return 0;
+}
+
+int mhar_ctx_destroy(mhar_ctx* c) {
+  if (!c) return 0;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& ev : c->pending) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
+  for (auto& ev : c->event_pool) {
+    cudaEventDestroy(ev.first);
+    cudaEventDestroy(ev.second);
+  }
+  for (void* q : c->allocs) cudaFree(q);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return 0;
+}
+
+int mhar_set_state(mhar_ctx* c, const double* x) {
+  if (!c || !x) return fail(MHAR_ERR_INVALID_ARGUMENT, "set_state: null argument");
+  CK(cudaSetDevice(c->device));
+  int s = upload_state_host(c, x, c->X);
+  if (s) return s;
+  c->slack_valid = false;
+  s = clear_error(c);
+  if (s) return s;
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int mhar_get_state(mhar_ctx* c, double* x) {
+  if (!c || !x) return fail(MHAR_ERR_INVALID_ARGUMENT, "get_state: null argument");
+  CK(cudaSetDevice(c->device));
+  unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->X, c->n, c->z, c->KT, c->rows);
+  LAUNCH_OK(c, "unpack_b_kernel");
+  CK(cudaMemcpyAsync(x, c->rows, sizeof(double) * c->n * c->z, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int mhar_get_state_rows_device(mhar_ctx* c, double* dev_rows) {
+  if (!c || !dev_rows) return fail(MHAR_ERR_INVALID_ARGUMENT, "get_state_rows_device: null");
+  CK(cudaSetDevice(c->device));
+  unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->X, c->n, c->z, c->KT, dev_rows);
+  LAUNCH_OK(c, "unpack_b_kernel");
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int mhar_step(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
+  if (!c || iters < 0) return fail(MHAR_ERR_INVALID_ARGUMENT, "step: bad argument");
+  CK(cudaSetDevice(c->device));
+  for (int64_t i = 0; i < iters; ++i) {
+    int s = enqueue_iterate(c, reproject_every, false);
+    if (s) return s;
+  }
+  return 0;
+}
+
+int mhar_sync(mhar_ctx* c) {
+  if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "sync: null context");
+  CK(cudaSetDevice(c->device));
+  return read_error(c, nullptr);
+}
+
+int mhar_step_timed(mhar_ctx* c, int64_t iters, int64_t reproject_every, double* device_ms) {
+  if (!c || iters < 0) return fail(MHAR_ERR_INVALID_ARGUMENT, "step_timed: bad argument");
+  CK(cudaSetDevice(c->device));
+  cudaEvent_t t0, t1;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
+  CK(cudaEventRecord(t0, c->stream));
+  int s = 0;
+  for (int64_t i = 0; i < iters && !s; ++i) s = enqueue_iterate(c, reproject_every, false);
+  CK(cudaEventRecord(t1, c->stream));
+  CK(cudaEventSynchronize(t1));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  if (device_ms) *device_ms = ms;
+  if (s) return s;
+  return read_error(c, nullptr);
+}
+
+int mhar_step_injected(mhar_ctx* c, const double* h, const double* u, double* lower,
+                       double* upper, double* theta, uint8_t* flags) {
+  if (!c || !h || !u) return fail(MHAR_ERR_INVALID_ARGUMENT, "step_injected: null argument");
+  CK(cudaSetDevice(c->device));
+  int s = read_error(c, nullptr);
+  if (s) return s;
+  s = upload_state_host(c, h, c->me > 0 ? c->H : c->D);
+  if (s) return s;
+  CK(cudaMemsetAsync(c->injected_u, 0, sizeof(double) * c->z_pad, c->stream));
+  CK(cudaMemcpyAsync(c->injected_u, u, sizeof(double) * c->z, cudaMemcpyHostToDevice, c->stream));
+  const int64_t saved = c->iterations;
+  s = enqueue_iterate(c, 0, true);
+  if (s) return s;
+  c->iterations = saved;  // the hook does not advance the RNG counters
+  int64_t walk = -1;
+  s = read_error(c, &walk);
+  std::vector<double> tmp(c->z);
+  if (lower) CK(cudaMemcpy(lower, c->lower, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+  if (upper) CK(cudaMemcpy(upper, c->upper, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+  if (theta) CK(cudaMemcpy(theta, c->theta, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+  if (flags) {
+    std::vector<unsigned> f(c->z);
+    CK(cudaMemcpy(f.data(), c->flags, sizeof(unsigned) * c->z, cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < c->z; ++k) flags[k] = (uint8_t)f[k];
+  }
+  return s;
+}
+
+int mhar_lambda_intervals(mhar_ctx* c, const double* x, const double* d, double* lower,
+                          double* upper, uint8_t* flags) {
+  if (!c || !x || !d) return fail(MHAR_ERR_INVALID_ARGUMENT, "lambda_intervals: null argument");
+  CK(cudaSetDevice(c->device));
+  int s = read_error(c, nullptr);
+  if (s) return s;
+  if (!c->Xtmp) {
+    if ((s = dalloc(c, &c->Xtmp, (size_t)c->z_pad * c->n_pad))) return s;
+  }
+  if ((s = upload_state_host(c, x, c->Xtmp))) return s;
+  if ((s = upload_state_host(c, d, c->D))) return s;
+  c->slack_valid = false;  // D was overwritten
+  if ((s = launch_chord(c, FUSED, c->Xtmp))) return s;
+  if ((s = launch_finalize(c, false, false))) return s;
+  int64_t walk = -1;
+  const int st = read_error(c, &walk);
+  if (lower) CK(cudaMemcpy(lower, c->lower, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+  if (upper) CK(cudaMemcpy(upper, c->upper, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+  if (flags) {
+    std::vector<unsigned> f(c->z);
+    CK(cudaMemcpy(f.data(), c->flags, sizeof(unsigned) * c->z, cudaMemcpyDeviceToHost));
+    for (int64_t k = 0; k < c->z; ++k) flags[k] = (uint8_t)f[k];
+  }
+  if (st) {
+    const std::string msg = g_last_error;
+    clear_error(c);
+    cudaStreamSynchronize(c->stream);
+    g_last_error = msg;
+  }
+  return st;
+}
+
+// Enqueues the containment pass of the current state: viol (max A x - b)
+// and eqviol (max |A_E x - b_E|) per walk.
+static int enqueue_check(mhar_ctx* c) {
+  int s = launch_chord(c, CHECK, c->X);
+  if (s) return s;
+  viol_extract_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(c->viol_key,
+                                                                              c->viol, c->z);
+  LAUNCH_OK(c, "viol_extract_kernel");
+  if (c->me > 0) {
+    const int64_t mz = c->me * c->z;
+    eq_residual_kernel<<<blocks_for(mz, 256, 1 << 30), 256, 0, c->stream>>>(
+        c->AE, c->bE, c->X, c->me, c->n, c->z, c->KT, c->eqres);
+    LAUNCH_OK(c, "eq_residual_kernel");
+    eq_maxabs_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(c->eqres, c->me,
+                                                                            c->z, c->eqviol);
+    LAUNCH_OK(c, "eq_maxabs_kernel");
+  }
+  return 0;
+}
+
+int mhar_check_state(mhar_ctx* c, double eps, int64_t* first_bad, double* max_viol,
+                     double* max_eq) {
+  if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "check_state: null context");
+  CK(cudaSetDevice(c->device));
+  int s = read_error(c, nullptr);
+  if (s) return s;
+  if ((s = enqueue_check(c))) return s;
+  int big = 0x7FFFFFFF;
+  CK(cudaMemcpyAsync(c->first_bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+  contains_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(
+      c->viol, c->me > 0 ? c->eqviol : nullptr, c->z, eps, c->err, 0, c->first_bad);
+  LAUNCH_OK(c, "contains_kernel");
+  int fb = big;
+  CK(cudaMemcpyAsync(&fb, c->first_bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (first_bad) *first_bad = (fb == big) ? -1 : fb;
+  if (max_viol) CK(cudaMemcpy(max_viol, c->viol, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+  if (max_eq) {
+    if (c->me > 0) {
+      CK(cudaMemcpy(max_eq, c->eqviol, sizeof(double) * c->z, cudaMemcpyDeviceToHost));
+    } else {
+      for (int64_t k = 0; k < c->z; ++k) max_eq[k] = 0.0;
+    }
+  }
+  return read_error(c, nullptr);
+}
+
+int mhar_run(mhar_ctx* c, const mhar_run_config* cfg, const double* x0, double* samples,
+             mhar_run_stats* stats) {
+  if (!c || !cfg || !x0) return fail(MHAR_ERR_INVALID_ARGUMENT, "run: null argument");
+  if (cfg->phi < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: phi must be >= 1");
+  if (cfg->windows < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: windows must be >= 1");
+  if (cfg->burn_in < 0 || cfg->reproject_every < 0)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "config: negative burn_in/reproject_every");
+  CK(cudaSetDevice(c->device));
+  int s = 0;
+  // fresh walk: x0 replicated, streams re-seeded, counters from zero (run(),
+  // sampler.cpp:298-302)
+  CK(cudaMemcpyAsync(c->x0, x0, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  const int64_t total = c->z_pad * c->KT * BK;
+  broadcast_state_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->x0, c->n, c->z, c->z_pad, c->KT, c->X);
+  LAUNCH_OK(c, "broadcast_state_kernel");
+  if ((s = clear_error(c))) return s;
+  CK(cudaMemsetAsync(c->redraw_total, 0, sizeof(unsigned long long), c->stream));
+  c->slack_valid = false;
+  c->iterations = 0;
+  if ((s = reset_streams(c))) return s;
+
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventRecord(t0, c->stream);
+  int big = 0x7FFFFFFF;
+  for (int64_t i = 0; i < cfg->burn_in; ++i)
+    if ((s = enqueue_iterate(c, cfg->reproject_every, false))) return s;
+  int64_t walk = -1;
+  for (int64_t w = 0; w < cfg->windows; ++w) {
+    for (int64_t i = 0; i < cfg->phi; ++i)
+      if ((s = enqueue_iterate(c, cfg->reproject_every, false))) return s;
+    if ((s = enqueue_check(c))) return s;
+    CK(cudaMemcpyAsync(c->first_bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    contains_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(
+        c->viol, c->me > 0 ? c->eqviol : nullptr, c->z, c->opt.eps_feas, c->err, 1, c->first_bad);
+    LAUNCH_OK(c, "contains_kernel");
+    if (samples) {
+      unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+          c->X, c->n, c->z, c->KT, c->rows);
+      LAUNCH_OK(c, "unpack_b_kernel");
+      CK(cudaMemcpyAsync(samples + (size_t)w * c->z * c->n, c->rows,
+                         sizeof(double) * c->z * c->n, cudaMemcpyDeviceToHost, c->stream));
+    }
+  }
+  cudaEventRecord(t1, c->stream);
+  s = read_error(c, &walk);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  unsigned long long red = 0;
+  cudaMemcpy(&red, c->redraw_total, sizeof(red), cudaMemcpyDeviceToHost);
+  if (stats) {
+    stats->iterate_count = c->z * cfg->phi * cfg->windows;
+    stats->windows = cfg->windows;
+    stats->redraw_count = (int64_t)red;
+    stats->err_walk = s ? walk + c->opt.chain_offset : -1;
+    stats->seconds = ms * 1e-3;
+  }
+  return s;
+}
+
+int mhar_get_stats(mhar_ctx* c, mhar_ctx_stats* out) {
+  if (!c || !out) return fail(MHAR_ERR_INVALID_ARGUMENT, "get_stats: null argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  harvest_timing(c);
+  unsigned long long red = 0;
+  CK(cudaMemcpy(&red, c->redraw_total, sizeof(red), cudaMemcpyDeviceToHost));
+  out->iterations = c->iterations;
+  out->redraw_count = (int64_t)red;
+  out->kernel_launches = c->launches;
+  out->chord_launches = c->chord_launches;
+  out->chord_ms = c->chord_ms;
+  out->chord_timed = c->chord_timed;
+  out->chord_flops = c->chord_flops;
+  out->refreshes = c->refreshes;
+  out->z = c->z;
+  out->z_padded = c->z_pad;
+  out->m_padded = c->m_pad;
+  out->n_padded = c->n_pad;
+  return 0;
+}
+
+int mhar_set_timing(mhar_ctx* c, int enabled) {
+  if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "set_timing: null context");
+  c->timing = enabled != 0;
+  return 0;
+}
+
+int mhar_reset_stats(mhar_ctx* c) {
+  if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "reset_stats: null context");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  harvest_timing(c);
+  c->launches = 0;
+  c->chord_launches = 0;
+  c->chord_ms = 0.0;
+  c->chord_timed = 0;
+  c->chord_flops = 0.0;
+  c->refreshes = 0;
+  return 0;
+}
+
+double mhar_flops_per_iterate(mhar_ctx* c) {
+  if (!c) return 0.0;
+  double f = 4.0 * (double)c->m * (double)c->n * (double)c->z;
+  if (c->me > 0) f += 2.0 * (double)c->n * (double)c->n * (double)c->z;
+  return f;
+}
+
+}  // extern "C"
