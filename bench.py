@@ -206,16 +206,20 @@ def run_engine(args, world, rank, local):
     ms = max_over_ranks(ms, world)
     value = z * world * args.steps / (ms * 1e-3)
 
-    # e2e: reference-facing C-ABI call with host buffers each step
-    # (set_state from host, one iterate, get_state to host)
-    Xh = eng.get_state()
+    # e2e: the reference-facing call with HOST buffers every step, as the
+    # reference's own loop `step(p, op, cfg, rng, state)` does: the walk state
+    # goes host -> device (pinned), one iterate, device -> host.
+    import torch
+    pinned = torch.empty((z, p.dim()), dtype=torch.float64, pin_memory=True).numpy()
+    Xh = pinned.T  # (n, z) column-major view of pinned memory
+    eng.get_state(out=Xh)
     barrier(world)
     t_e2e = []
     for i in range(args.e2e_steps):
         t0 = time.perf_counter()
         eng.set_state(Xh)
         eng.step(1, reproject)
-        Xh = eng.get_state()
+        eng.get_state(out=Xh)
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(t_e2e), world)
     e2e_value = z * world * args.e2e_steps / e2e_s

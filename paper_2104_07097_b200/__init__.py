@@ -400,8 +400,10 @@ class Engine:
                             f"set_state: x is {x.shape}, expected {(self.n, self.z)}")
         _check(lib().mhar_set_state(self._h, _d(x)))
 
-    def get_state(self) -> np.ndarray:
-        x = np.empty((self.n, self.z), order="F")
+    def get_state(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        x = np.empty((self.n, self.z), order="F") if out is None else out
+        if x.shape != (self.n, self.z) or not x.flags.f_contiguous or x.dtype != np.float64:
+            raise MharError(ErrorCode.dimension_mismatch, "get_state: out must be n x z F-order")
         _check(lib().mhar_get_state(self._h, _d(x)))
         return x
 

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -63,7 +64,7 @@ struct mhar_ctx {
   int num_sms = 148;
   mhar_options opt{};
   int64_t n = 0, m = 0, me = 0, z = 0;
-  int64_t n_pad = 0, KT = 0, m_pad = 0, m_tiles = 0, z_pad = 0, ct64 = 0, ct128 = 0;
+  int64_t n_pad = 0, KT = 0, m_pad = 0, m_tiles = 0, z_pad = 0, ct64 = 0;
   int64_t p_rows_pad = 0;
 
   // device buffers
@@ -81,6 +82,7 @@ struct mhar_ctx {
   unsigned long long *err = nullptr, *redraw_total = nullptr;
   uint64_t *col_state = nullptr, *theta_state = nullptr;
   int redraw_grid = 1;
+  int group_m = 4;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
 
   // host bookkeeping
   int64_t iterations = 0;
@@ -175,18 +177,18 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   p.err = c->err;
   p.m_tiles = c->m_tiles;
   p.KT = c->KT;
-  p.ct128 = c->ct128;
+  p.col_tiles = c->ct64;
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
-  p.group_m = 16;
+  p.group_m = c->group_m;
   return p;
 }
 
 int launch_chord(mhar_ctx* c, int mode, const double* X) {
   ChordParams p = chord_params(c, X);
-  p.col_tiles = (mode == FUSED || mode == FUSED_STORE) ? c->ct64 : c->ct128;
+  const bool fused = (mode == FUSED || mode == FUSED_STORE);
   const int64_t units = p.m_tiles * p.col_tiles;
-  const int grid = (int)std::min<int64_t>(units, c->num_sms);
+  const int grid = (int)std::min<int64_t>(units, (fused ? 1 : 2) * (int64_t)c->num_sms);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (c->timing) {
     ev = take_events(c);
@@ -200,10 +202,10 @@ int launch_chord(mhar_ctx* c, int mode, const double* X) {
       chord_kernel<FUSED_STORE><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
       break;
     case INCREMENTAL:
-      chord_kernel<INCREMENTAL><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
+      chord2_kernel<INCREMENTAL><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
       break;
     default:
-      chord_kernel<CHECK><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
+      chord2_kernel<CHECK><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
       break;
   }
   LAUNCH_OK(c, "chord_kernel");
@@ -275,7 +277,7 @@ int launch_redraw(mhar_ctx* c) {
   rp.D = c->D;
   rp.P = c->me > 0 ? c->Pcm : nullptr;
   rp.R = (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) ? c->R : nullptr;
-  rp.ct128 = c->ct128;
+  rp.ct64 = c->ct64;
   rp.scratch = c->redraw_scratch;
   rp.lower = c->lower;
   rp.upper = c->upper;
@@ -521,9 +523,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   c->KT = c->n_pad / BK;
   c->m_pad = round_up(c->m, BM);
   c->m_tiles = c->m_pad / BM;
-  c->z_pad = round_up(c->z, 128);
+  c->z_pad = round_up(c->z, 64);
   c->ct64 = c->z_pad / 64;
-  c->ct128 = c->z_pad / 128;
   c->p_rows_pad = round_up(c->n, BM);
 
   const size_t nzp = (size_t)c->z_pad * c->n_pad;
@@ -545,6 +546,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       (st = dalloc(c, &c->injected_u, c->z_pad)))
     return bail(st);
   c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
+  if (const char* g = std::getenv("MHAR_GROUP_M")) c->group_m = std::max(1, std::atoi(g));
   if ((st = dalloc(c, &c->redraw_scratch, (size_t)c->redraw_grid * 3 * c->n))) return bail(st);
   if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
     const size_t cache = (size_t)c->m_pad * c->z_pad;
@@ -613,8 +615,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   ++c->launches;
   cudaFuncSetAttribute(chord_kernel<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
   cudaFuncSetAttribute(chord_kernel<FUSED_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
-  cudaFuncSetAttribute(chord_kernel<INCREMENTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
-  cudaFuncSetAttribute(chord_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
+  cudaFuncSetAttribute(chord2_kernel<INCREMENTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
+  cudaFuncSetAttribute(chord2_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   if ((st = reset_streams(c))) return bail(st);
   e = cudaStreamSynchronize(c->stream);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -641,15 +643,30 @@ int mhar_ctx_destroy(mhar_ctx* c) {
   return 0;
 }
 
+// The upload lands in a staging buffer first; if it is bit-identical to the
+// resident state (the common loop `step(p, op, cfg, rng, state)` hands back
+// the state the previous call returned), the slack cache stays valid.
 int mhar_set_state(mhar_ctx* c, const double* x) {
   if (!c || !x) return fail(MHAR_ERR_INVALID_ARGUMENT, "set_state: null argument");
   CK(cudaSetDevice(c->device));
-  int s = upload_state_host(c, x, c->X);
-  if (s) return s;
-  c->slack_valid = false;
-  s = clear_error(c);
-  if (s) return s;
+  int s = 0;
+  if (!c->Xtmp) {
+    if ((s = dalloc(c, &c->Xtmp, (size_t)c->z_pad * c->n_pad))) return s;
+  }
+  if ((s = upload_state_host(c, x, c->Xtmp))) return s;
+  CK(cudaMemsetAsync(c->first_bad, 0, sizeof(int), c->stream));
+  const int64_t total = c->z_pad * c->KT * BK;
+  differs_kernel<<<blocks_for(total, 256, c->num_sms * 8), 256, 0, c->stream>>>(c->Xtmp, c->X,
+                                                                               total, c->first_bad);
+  LAUNCH_OK(c, "differs_kernel");
+  int differs = 1;
+  CK(cudaMemcpyAsync(&differs, c->first_bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  if ((s = clear_error(c))) return s;
   CK(cudaStreamSynchronize(c->stream));
+  if (differs) {
+    std::swap(c->X, c->Xtmp);
+    c->slack_valid = false;
+  }
   return 0;
 }
 

@@ -1,4 +1,4 @@
-// chord_kernel.cuh -- the fused fp64 tensor-core chord kernel.
+// chord_kernel.cuh -- the fused fp64 tensor-core chord kernels.
 //
 // Restates, for all walks at once, compute_lambda_intervals
 // (/root/reference/proj/src/sampler.cpp:150-208) with its per-walk
@@ -8,21 +8,26 @@
 //   upper_k = min{ slack_i / rate_i : rate_i >  eps_dir }
 //   lower_k = max{ slack_i / rate_i : rate_i < -eps_dir }
 //
-// as ONE persistent kernel: a DMMA.8x8x4 product over pre-permuted operand
-// tiles streamed HBM -> smem by the TMA bulk-copy engine through an mbarrier
-// ring, whose epilogue forms the ratios in registers and reduces them
-// (registers -> warp shuffles -> one order-preserving int64 atomic per walk
-// per warp).  The m_I x z products never reach HBM in the FUSED mode.
+// as persistent kernels: a DMMA.8x8x4 product over pre-permuted operand tiles
+// streamed HBM -> smem by the TMA bulk-copy engine through an mbarrier ring,
+// whose epilogue forms the ratios in registers and reduces them (registers ->
+// warp shuffles -> one order-preserving int64 atomic per walk per warp).
 //
 // Modes (template):
 //   FUSED        B = [X | D] per 64-walk tile: both products, bounds, and
 //                max_i (A x - b) (contains(), polytope.cpp:177-190) for free.
+//                The m_I x z products never reach HBM.
 //   FUSED_STORE  FUSED + writes slack and rate into the incremental cache.
-//   INCREMENTAL  B = D per 128-walk tile: only A_I D is multiplied; the slack
-//                of the moved walks comes from the cache,
-//                slack_t = slack_{t-1} - theta_{t-1} rate_{t-1}, which holds
-//                because x_t = x_{t-1} + theta_{t-1} d_{t-1} (half the flops).
+//   INCREMENTAL  B = D: only A_I D is multiplied; the slack of the moved walks
+//                comes from the cache, slack_t = slack_{t-1} - theta_{t-1}
+//                rate_{t-1}, which holds because x_t = x_{t-1} + theta_{t-1}
+//                d_{t-1} (half the flops of FUSED).
 //   CHECK        B = X: max_i (A x - b) only (collection-time containment).
+//
+// FUSED* run one 256-thread CTA per SM on a 128-row x (64 x + 64 d) tile
+// (warp tile 64 x 32, 128 accumulator doubles per thread).  INCREMENTAL and
+// CHECK run TWO 256-thread CTAs per SM on 128-row x 64-walk tiles (warp tile
+// 32 x 32), so one CTA's epilogue overlaps the other's tensor-core work.
 #pragma once
 
 #include "common.cuh"
@@ -31,11 +36,17 @@ namespace mhar_dev {
 
 enum ChordMode { FUSED = 0, FUSED_STORE = 1, INCREMENTAL = 2, CHECK = 3 };
 
-constexpr int CHORD_THREADS = 256;  // 8 MMA warps: 2 (rows) x 4 (walk columns)
-constexpr int CHORD_STAGES = 5;     // 5 x 32 KB ring
-constexpr int CHORD_LAG = 2;        // refill the slot consumed two stages ago
+constexpr int CHORD_THREADS = 256;
+// FUSED* kernel (1 CTA / SM)
+constexpr int CHORD_STAGES = 6;  // 6 x 32 KB ring
+constexpr int CHORD_LAG = 2;     // refill the slot consumed two stages ago
 constexpr int STAGE_DOUBLES = A_PIECE + 2 * B_PIECE;
 constexpr size_t CHORD_SMEM = (size_t)CHORD_STAGES * STAGE_DOUBLES * sizeof(double) + 1024;
+// INCREMENTAL / CHECK kernel (2 CTAs / SM)
+constexpr int CHORD2_STAGES = 4;  // 4 x 24 KB ring per CTA
+constexpr int CHORD2_LAG = 1;
+constexpr int STAGE2_DOUBLES = A_PIECE + B_PIECE;
+constexpr size_t CHORD2_SMEM = (size_t)CHORD2_STAGES * STAGE2_DOUBLES * sizeof(double) + 256;
 
 struct ChordParams {
   const double* A;  // packed A_I (a_index)
@@ -52,23 +63,90 @@ struct ChordParams {
   const unsigned long long* err;
   int64_t m_tiles;    // m_pad / 128
   int64_t KT;         // n_pad / 16
-  int64_t col_tiles;  // FUSED*: 64-walk tiles; INCREMENTAL/CHECK: 128-walk tiles
-  int64_t ct128;      // 128-walk tiles (slack cache geometry)
+  int64_t col_tiles;  // 64-walk tiles
   int64_t z;          // live walks
   double eps_dir;
   int group_m;        // rasterisation band height (m tiles)
 };
 
+// Unit u -> (row tile, walk tile): bands of group_m row tiles, walk tiles
+// inner, so the CTAs in flight share few A tiles and the walk operand stays
+// L2-resident.
 __device__ inline void unit_coords(int64_t u, const ChordParams& p, int64_t* mt, int64_t* ct) {
   const int64_t band_units = (int64_t)p.group_m * p.col_tiles;
   const int64_t band = u / band_units;
-  const int64_t in_band = u % band_units;
+  const int64_t in_band = u - band * band_units;
   const int64_t start = band * p.group_m;
   const int64_t h = (p.m_tiles - start < p.group_m) ? p.m_tiles - start : p.group_m;
   *mt = start + in_band % h;
   *ct = in_band / h;
 }
 
+// One row of the chord scan for walk bounds (hi, lo) with the exact
+// candidate filter: a row can only move a bound if its ratio beats it, and
+// the sign of fma(-bound, rate, slack) -- the sign of the exact value --
+// decides that, so the division runs only for candidates and the result is
+// bit-identical to dividing every row.
+__device__ __forceinline__ void scan_row(double sl, double ad, double eps, double& hi, double& lo,
+                                         unsigned& sd) {
+  if (ad > eps) {
+    sd |= 1u;
+    if (!(fma(-hi, ad, sl) > 0.0)) {
+      const double q = sl / ad;
+      hi = q < hi ? q : hi;
+    }
+  } else if (ad < -eps) {
+    sd |= 2u;
+    if (!(fma(-lo, ad, sl) >= 0.0)) {
+      const double q = sl / ad;
+      lo = q > lo ? q : lo;
+    }
+  }
+}
+
+// Warp reduction over the 8 row lanes sharing (lane & 3), then one atomic per
+// walk from lanes 0..3.  c0 = the walk of (lane & 3) == 0, e = 0.
+template <int NCH, bool BOUNDS>
+__device__ __forceinline__ void reduce_and_publish(double (&hi)[NCH][2], double (&lo)[NCH][2],
+                                                   double (&viol)[NCH][2], unsigned (&sd)[NCH][2],
+                                                   const int64_t (&c0)[NCH], int lane,
+                                                   const ChordParams& p) {
+#pragma unroll
+  for (int j = 0; j < NCH; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+#pragma unroll
+      for (int off = 4; off < 32; off <<= 1) {
+        if (BOUNDS) {
+          hi[j][e] = fmin(hi[j][e], __shfl_xor_sync(0xFFFFFFFFu, hi[j][e], off));
+          lo[j][e] = fmax(lo[j][e], __shfl_xor_sync(0xFFFFFFFFu, lo[j][e], off));
+          sd[j][e] |= __shfl_xor_sync(0xFFFFFFFFu, sd[j][e], off);
+        }
+        viol[j][e] = fmax(viol[j][e], __shfl_xor_sync(0xFFFFFFFFu, viol[j][e], off));
+      }
+    }
+  if (lane < 4) {
+#pragma unroll
+    for (int j = 0; j < NCH; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int64_t c = c0[j] + 2 * lane + e;
+        if (c >= p.z) continue;
+        const long long vk = dkey(viol[j][e]);
+        if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
+        if (BOUNDS) {
+          const long long hk = dkey(hi[j][e]), lk = dkey(lo[j][e]);
+          if (hk < *(volatile long long*)(p.hi_key + c)) atomicMin(p.hi_key + c, hk);
+          if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
+          if (sd[j][e] & ~*(volatile unsigned*)(p.sides + c)) atomicOr(p.sides + c, sd[j][e]);
+        }
+      }
+  }
+}
+
+// ===========================================================================
+// FUSED / FUSED_STORE: one CTA per SM, tile 128 rows x 64 walks x {x, d}.
+// ===========================================================================
 template <int MODE>
 __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordParams p) {
   if (*p.err != kNoError) return;  // sticky device error: stop all work
@@ -78,10 +156,11 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
   uint64_t* empty = full + CHORD_STAGES;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;
+  const int wm = warp >> 2, wn = warp & 3;  // warp tile: 64 rows x (16 walks x {x, d})
   const int64_t n_units = p.m_tiles * p.col_tiles;
-  const int64_t my_units = (blockIdx.x < n_units) ? (n_units - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int64_t total_loads = my_units * p.KT;
+  const int my_units =
+      (blockIdx.x < n_units) ? (int)((n_units - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int KT = (int)p.KT;
 
   if (tid == 0) {
     for (int s = 0; s < CHORD_STAGES; ++s) {
@@ -92,76 +171,52 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
   }
   __syncthreads();
 
-  // Producer (thread 0): issue the bulk copies for global load index q.
-  auto issue = [&](int64_t q) {
-    const int s = (int)(q % CHORD_STAGES);
-    const int64_t ui = q / p.KT, kt = q % p.KT;
-    const int64_t u = blockIdx.x + ui * gridDim.x;
-    int64_t mt, ct;
-    unit_coords(u, p, &mt, &ct);
-    double* st = ring + (size_t)s * STAGE_DOUBLES;
-    mbar_arrive_expect_tx(&full[s], STAGE_DOUBLES * 8);
-    bulk_g2s(st, p.A + (mt * p.KT + kt) * A_PIECE, A_PIECE * 8, &full[s]);
-    const double* b0;
-    const double* b1;
-    if (MODE == FUSED || MODE == FUSED_STORE) {
-      b0 = p.X + (ct * p.KT + kt) * B_PIECE;
-      b1 = p.D + (ct * p.KT + kt) * B_PIECE;
-    } else {
-      const double* src = (MODE == INCREMENTAL) ? p.D : p.X;
-      b0 = src + ((2 * ct) * p.KT + kt) * B_PIECE;
-      b1 = src + ((2 * ct + 1) * p.KT + kt) * B_PIECE;
+  // producer state (thread 0): the consumers' (unit, k-tile) sequence,
+  // CHORD_STAGES - CHORD_LAG loads ahead.
+  int l_ui = 0, l_kt = 0, l_stage = 0, l_round = 0;
+  int64_t l_mt = 0, l_ct = 0;
+  uint64_t keep_policy = 0;
+  auto producer_issue = [&]() {
+    if (l_ui >= my_units) return;
+    if (l_round > 0) mbar_wait(&empty[l_stage], (uint32_t)((l_round - 1) & 1));
+    double* st = ring + (size_t)l_stage * STAGE_DOUBLES;
+    mbar_arrive_expect_tx(&full[l_stage], STAGE_DOUBLES * 8);
+    bulk_g2s(st, p.A + (l_mt * p.KT + l_kt) * A_PIECE, A_PIECE * 8, &full[l_stage]);
+    bulk_g2s_hint(st + A_PIECE, p.X + (l_ct * p.KT + l_kt) * B_PIECE, B_PIECE * 8,
+                  &full[l_stage], keep_policy);
+    bulk_g2s_hint(st + A_PIECE + B_PIECE, p.D + (l_ct * p.KT + l_kt) * B_PIECE, B_PIECE * 8,
+                  &full[l_stage], keep_policy);
+    if (++l_stage == CHORD_STAGES) {
+      l_stage = 0;
+      ++l_round;
     }
-    bulk_g2s(st + A_PIECE, b0, B_PIECE * 8, &full[s]);
-    bulk_g2s(st + A_PIECE + B_PIECE, b1, B_PIECE * 8, &full[s]);
+    if (++l_kt == KT) {
+      l_kt = 0;
+      if (++l_ui < my_units) unit_coords(blockIdx.x + (int64_t)l_ui * gridDim.x, p, &l_mt, &l_ct);
+    }
   };
-
   if (tid == 0) {
-    const int64_t pre = total_loads < (CHORD_STAGES - CHORD_LAG) ? total_loads
-                                                                  : (CHORD_STAGES - CHORD_LAG);
-    for (int64_t q = 0; q < pre; ++q) issue(q);
+    keep_policy = policy_evict_last();
+    if (my_units > 0) unit_coords(blockIdx.x, p, &l_mt, &l_ct);
+    for (int q = 0; q < CHORD_STAGES - CHORD_LAG; ++q) producer_issue();
   }
 
-  // B fragment source (piece, col_group) for this warp's 4 column groups.
-  int bpiece[4], bcg[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    if (MODE == FUSED || MODE == FUSED_STORE) {
-      bpiece[j] = j >> 1;          // j = 0,1: x columns; j = 2,3: d columns
-      bcg[j] = wn * 2 + (j & 1);   // 16 walks per warp
-    } else {
-      bpiece[j] = wn >> 1;         // 32 walks per warp
-      bcg[j] = (wn & 1) * 4 + j;
-    }
-  }
-
-  int64_t q = 0;
-  for (int64_t ui = 0; ui < my_units; ++ui) {
-    const int64_t u = blockIdx.x + ui * gridDim.x;
+  int c_stage = 0, c_phase = 0;
+  for (int ui = 0; ui < my_units; ++ui) {
     int64_t mt, ct;
-    unit_coords(u, p, &mt, &ct);
+    unit_coords(blockIdx.x + (int64_t)ui * gridDim.x, p, &mt, &ct);
 
-    double acc[8][4][2];
+    double acc[8][4][2];  // j = 0,1: A x columns; j = 2,3: A d columns (same walks)
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int64_t kt = 0; kt < p.KT; ++kt, ++q) {
-      if (tid == 0) {
-        const int64_t qn = q + (CHORD_STAGES - CHORD_LAG);
-        if (qn < total_loads) {
-          if (qn >= CHORD_STAGES) {
-            const int64_t prev = qn - CHORD_STAGES;  // previous occupant of the slot
-            mbar_wait(&empty[qn % CHORD_STAGES], (uint32_t)((prev / CHORD_STAGES) & 1));
-          }
-          issue(qn);
-        }
-      }
-      const int s = (int)(q % CHORD_STAGES);
-      mbar_wait(&full[s], (uint32_t)((q / CHORD_STAGES) & 1));
-      const double2* sa = reinterpret_cast<const double2*>(ring + (size_t)s * STAGE_DOUBLES);
-      const double2* sb = reinterpret_cast<const double2*>(ring + (size_t)s * STAGE_DOUBLES + A_PIECE);
+    for (int kt = 0; kt < KT; ++kt) {
+      if (tid == 0) producer_issue();
+      mbar_wait(&full[c_stage], (uint32_t)c_phase);
+      const double2* sa = reinterpret_cast<const double2*>(ring + (size_t)c_stage * STAGE_DOUBLES);
+      const double2* sb = sa + A_PIECE / 2;
 #pragma unroll
       for (int k8 = 0; k8 < 2; ++k8) {
         double2 af[8], bf[4];
@@ -169,7 +224,7 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
         for (int i = 0; i < 8; ++i) af[i] = sa[(k8 * 16 + wm * 8 + i) * 32 + lane];
 #pragma unroll
         for (int j = 0; j < 4; ++j)
-          bf[j] = sb[bpiece[j] * (B_PIECE / 2) + (k8 * 8 + bcg[j]) * 32 + lane];
+          bf[j] = sb[(j >> 1) * (B_PIECE / 2) + (k8 * 8 + wn * 2 + (j & 1)) * 32 + lane];
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -180,31 +235,28 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
           for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      if (lane == 0) mbar_arrive(&empty[c_stage]);
+      if (++c_stage == CHORD_STAGES) {
+        c_stage = 0;
+        c_phase ^= 1;
+      }
     }
 
-    // ---------------- epilogue: chord bounds for this tile ----------------
+    // ---------------- epilogue ----------------
     const int64_t row0 = mt * BM + wm * 64 + (lane >> 2);
-    constexpr int NCH = (MODE == FUSED || MODE == FUSED_STORE) ? 2 : 4;  // walk groups
-    double hi[NCH][2], lo[NCH][2], viol[NCH][2];
-    unsigned sd[NCH][2];
+    double hi[2][2], lo[2][2], viol[2][2];
+    unsigned sd[2][2];
+    int64_t c0[2];
 #pragma unroll
-    for (int j = 0; j < NCH; ++j)
+    for (int j = 0; j < 2; ++j) {
+      c0[j] = ct * 64 + wn * 16 + j * 8;
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
-        hi[j][e] = __longlong_as_double(0x7FF0000000000000LL);   // +inf
-        lo[j][e] = __longlong_as_double((long long)0xFFF0000000000000ULL);  // -inf
-        viol[j][e] = lo[j][e];
+        const int64_t c = c0[j] + 2 * (lane & 3) + e;
+        hi[j][e] = keyd(*(volatile long long*)(p.hi_key + c));
+        lo[j][e] = keyd(*(volatile long long*)(p.lo_key + c));
+        viol[j][e] = __longlong_as_double((long long)0xFFF0000000000000ULL);  // -inf
         sd[j][e] = 0u;
-      }
-    double thp[NCH][2];
-    if (MODE == INCREMENTAL) {
-#pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        const int64_t c = ct * 128 + wn * 32 + j * 8 + 2 * (lane & 3);
-        const double2 t = *reinterpret_cast<const double2*>(p.theta_prev + c);
-        thp[j][0] = t.x;
-        thp[j][1] = t.y;
       }
     }
 #pragma unroll
@@ -212,84 +264,174 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
       const int64_t r = row0 + i * 8;
       const double br = __ldg(p.b + r);
 #pragma unroll
-      for (int j = 0; j < NCH; ++j) {
-        double ax[2], ad[2], sl[2];
-        if (MODE == FUSED || MODE == FUSED_STORE) {
-          ax[0] = acc[i][j][0]; ax[1] = acc[i][j][1];
-          ad[0] = acc[i][j + 2][0]; ad[1] = acc[i][j + 2][1];
-          sl[0] = br - ax[0]; sl[1] = br - ax[1];  // (-ax).colwise() + b, sampler.cpp:175
-        } else if (MODE == INCREMENTAL) {
-          ad[0] = acc[i][j][0]; ad[1] = acc[i][j][1];
-          const int64_t base =
-              (((((mt * p.ct128 + ct) * 8 + warp) * 8 + i) * 4 + j) * 32 + lane) * 2;
-          const double2 so = __ldcs(reinterpret_cast<const double2*>(p.S + base));
-          const double2 ro = __ldcs(reinterpret_cast<const double2*>(p.R + base));
-          sl[0] = fma(-thp[j][0], ro.x, so.x);
-          sl[1] = fma(-thp[j][1], ro.y, so.y);
-          __stcs(reinterpret_cast<double2*>(p.S + base), make_double2(sl[0], sl[1]));
-          __stcs(reinterpret_cast<double2*>(p.R + base), make_double2(ad[0], ad[1]));
-          ax[0] = -sl[0]; ax[1] = -sl[1];
-        } else {  // CHECK
-          ax[0] = acc[i][j][0]; ax[1] = acc[i][j][1];
-        }
+      for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const double v = (MODE == INCREMENTAL) ? ax[e] : ax[e] - br;
-          viol[j][e] = fmax(viol[j][e], v);
-          if (MODE != CHECK) {
-            if (ad[e] > p.eps_dir) {
-              const double qv = sl[e] / ad[e];
-              sd[j][e] |= 1u;
-              hi[j][e] = qv < hi[j][e] ? qv : hi[j][e];
-            } else if (ad[e] < -p.eps_dir) {
-              const double qv = sl[e] / ad[e];
-              sd[j][e] |= 2u;
-              lo[j][e] = qv > lo[j][e] ? qv : lo[j][e];
-            }
+          const double ax = acc[i][j][e], ad = acc[i][j + 2][e];
+          const double sl = br - ax;  // (-ax).colwise() + b, sampler.cpp:175
+          viol[j][e] = fmax(viol[j][e], ax - br);
+          scan_row(sl, ad, p.eps_dir, hi[j][e], lo[j][e], sd[j][e]);
+          if (MODE == FUSED_STORE) {
+            const int64_t si = s_index(r, c0[j] + 2 * (lane & 3) + e, p.col_tiles);
+            p.S[si] = sl;
+            p.R[si] = ad;
           }
         }
-        if (MODE == FUSED_STORE) {
-          const int64_t c = ct * 64 + wn * 16 + j * 8 + 2 * (lane & 3);
+    }
+    reduce_and_publish<2, true>(hi, lo, viol, sd, c0, lane, p);
+  }
+}
+
+// ===========================================================================
+// INCREMENTAL / CHECK: two CTAs per SM, tile 128 rows x 64 walks.
+// ===========================================================================
+template <int MODE>
+__global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordParams p) {
+  if (*p.err != kNoError) return;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* ring = reinterpret_cast<double*>(smem_raw);
+  uint64_t* full =
+      reinterpret_cast<uint64_t*>(smem_raw + (size_t)CHORD2_STAGES * STAGE2_DOUBLES * 8);
+  uint64_t* empty = full + CHORD2_STAGES;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;  // warp tile: 32 rows x 32 walks
+  const int64_t n_units = p.m_tiles * p.col_tiles;
+  const int my_units =
+      (blockIdx.x < n_units) ? (int)((n_units - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int KT = (int)p.KT;
+  const double* __restrict__ Bsrc = (MODE == INCREMENTAL) ? p.D : p.X;
+
+  if (tid == 0) {
+    for (int s = 0; s < CHORD2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CHORD_THREADS / 32);
+    }
+    fence_barrier_init();
+  }
+  __syncthreads();
+
+  int l_ui = 0, l_kt = 0, l_stage = 0, l_round = 0;
+  int64_t l_mt = 0, l_ct = 0;
+  uint64_t keep_policy = 0;
+  auto producer_issue = [&]() {
+    if (l_ui >= my_units) return;
+    if (l_round > 0) mbar_wait(&empty[l_stage], (uint32_t)((l_round - 1) & 1));
+    double* st = ring + (size_t)l_stage * STAGE2_DOUBLES;
+    mbar_arrive_expect_tx(&full[l_stage], STAGE2_DOUBLES * 8);
+    bulk_g2s(st, p.A + (l_mt * p.KT + l_kt) * A_PIECE, A_PIECE * 8, &full[l_stage]);
+    bulk_g2s_hint(st + A_PIECE, Bsrc + (l_ct * p.KT + l_kt) * B_PIECE, B_PIECE * 8,
+                  &full[l_stage], keep_policy);
+    if (++l_stage == CHORD2_STAGES) {
+      l_stage = 0;
+      ++l_round;
+    }
+    if (++l_kt == KT) {
+      l_kt = 0;
+      if (++l_ui < my_units) unit_coords(blockIdx.x + (int64_t)l_ui * gridDim.x, p, &l_mt, &l_ct);
+    }
+  };
+  if (tid == 0) {
+    keep_policy = policy_evict_last();
+    if (my_units > 0) unit_coords(blockIdx.x, p, &l_mt, &l_ct);
+    for (int q = 0; q < CHORD2_STAGES - CHORD2_LAG; ++q) producer_issue();
+  }
+
+  int c_stage = 0, c_phase = 0;
+  for (int ui = 0; ui < my_units; ++ui) {
+    int64_t mt, ct;
+    unit_coords(blockIdx.x + (int64_t)ui * gridDim.x, p, &mt, &ct);
+    const int64_t cache_base = ((mt * p.col_tiles + ct) * 8 + warp) * S_WARP_BLOCK;
+
+    double acc[4][4][2];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int64_t si = s_index(r, c + e, p.ct128);
-            p.S[si] = sl[e];
-            p.R[si] = ad[e];
-          }
-        }
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    for (int kt = 0; kt < KT; ++kt) {
+      if (tid == 0) producer_issue();
+      if (MODE == INCREMENTAL && kt == (KT > 8 ? KT - 8 : 0) && lane == 0) {
+        // stage this warp's slack/rate block (2 x 8 KB) into L2 ahead of the epilogue
+        bulk_prefetch_l2(p.S + cache_base, S_WARP_BLOCK * 8);
+        bulk_prefetch_l2(p.R + cache_base, S_WARP_BLOCK * 8);
+      }
+      mbar_wait(&full[c_stage], (uint32_t)c_phase);
+      const double2* sa =
+          reinterpret_cast<const double2*>(ring + (size_t)c_stage * STAGE2_DOUBLES);
+      const double2* sb = sa + A_PIECE / 2;
+#pragma unroll
+      for (int k8 = 0; k8 < 2; ++k8) {
+        double2 af[4], bf[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) af[i] = sa[(k8 * 16 + wm * 4 + i) * 32 + lane];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bf[j] = sb[(k8 * 8 + wn * 4 + j) * 32 + lane];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].x, bf[j].x);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i].y, bf[j].y);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[c_stage]);
+      if (++c_stage == CHORD2_STAGES) {
+        c_stage = 0;
+        c_phase ^= 1;
       }
     }
-    // reduce over the 8 row lanes sharing (lane & 3)
+
+    // ---------------- epilogue: one walk group (8 walks) at a time --------
+    const int64_t row0 = mt * BM + wm * 32 + (lane >> 2);
+    constexpr bool kBounds = (MODE == INCREMENTAL);
+    double br[4];
+    if (!kBounds) {
 #pragma unroll
-    for (int j = 0; j < NCH; ++j)
+      for (int i = 0; i < 4; ++i) br[i] = __ldg(p.b + row0 + i * 8);
+    }
 #pragma unroll
-      for (int e = 0; e < 2; ++e) {
-#pragma unroll
-        for (int off = 4; off < 32; off <<= 1) {
-          hi[j][e] = fmin(hi[j][e], __shfl_xor_sync(0xFFFFFFFFu, hi[j][e], off));
-          lo[j][e] = fmax(lo[j][e], __shfl_xor_sync(0xFFFFFFFFu, lo[j][e], off));
-          viol[j][e] = fmax(viol[j][e], __shfl_xor_sync(0xFFFFFFFFu, viol[j][e], off));
-          sd[j][e] |= __shfl_xor_sync(0xFFFFFFFFu, sd[j][e], off);
-        }
-      }
-    if (lane < 4) {
-#pragma unroll
-      for (int j = 0; j < NCH; ++j)
+    for (int j = 0; j < 4; ++j) {
+      double hi[1][2], lo[1][2], viol[1][2];
+      unsigned sd[1][2] = {{0u, 0u}};
+      const int64_t c0[1] = {ct * 64 + wn * 32 + j * 8};
+      const int64_t c = c0[0] + 2 * (lane & 3);
+      viol[0][0] = viol[0][1] = __longlong_as_double((long long)0xFFF0000000000000ULL);
+      if (kBounds) {
+        const double2 th = *reinterpret_cast<const double2*>(p.theta_prev + c);
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int64_t c = (MODE == FUSED || MODE == FUSED_STORE)
-                                ? ct * 64 + wn * 16 + j * 8 + 2 * lane + e
-                                : ct * 128 + wn * 32 + j * 8 + 2 * lane + e;
-          if (c >= p.z) continue;
-          const long long vk = dkey(viol[j][e]);
-          if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
-          if (MODE != CHECK) {
-            const long long hk = dkey(hi[j][e]), lk = dkey(lo[j][e]);
-            if (hk < *(volatile long long*)(p.hi_key + c)) atomicMin(p.hi_key + c, hk);
-            if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
-            if (sd[j][e] & ~*(volatile unsigned*)(p.sides + c)) atomicOr(p.sides + c, sd[j][e]);
-          }
+          hi[0][e] = keyd(*(volatile long long*)(p.hi_key + c + e));
+          lo[0][e] = keyd(*(volatile long long*)(p.lo_key + c + e));
         }
+        double2 so[4], ro[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t base = cache_base + ((i * 4 + j) * 32 + lane) * 2;
+          so[i] = __ldcs(reinterpret_cast<const double2*>(p.S + base));
+          ro[i] = __ldcs(reinterpret_cast<const double2*>(p.R + base));
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int64_t base = cache_base + ((i * 4 + j) * 32 + lane) * 2;
+          const double s0 = fma(-th.x, ro[i].x, so[i].x);
+          const double s1 = fma(-th.y, ro[i].y, so[i].y);
+          __stcs(reinterpret_cast<double2*>(p.S + base), make_double2(s0, s1));
+          __stcs(reinterpret_cast<double2*>(p.R + base), make_double2(acc[i][j][0], acc[i][j][1]));
+          viol[0][0] = fmax(viol[0][0], -s0);
+          viol[0][1] = fmax(viol[0][1], -s1);
+          scan_row(s0, acc[i][j][0], p.eps_dir, hi[0][0], lo[0][0], sd[0][0]);
+          scan_row(s1, acc[i][j][1], p.eps_dir, hi[0][1], lo[0][1], sd[0][1]);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) viol[0][e] = fmax(viol[0][e], acc[i][j][e] - br[i]);
+      }
+      reduce_and_publish<1, kBounds>(hi, lo, viol, sd, c0, lane, p);
     }
   }
 }

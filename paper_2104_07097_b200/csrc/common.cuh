@@ -57,14 +57,17 @@ __host__ __device__ inline void b_coords(int64_t i, int64_t KT, int64_t* c, int6
 }
 
 // Slack / rate cache of the incremental mode, stored in the accumulator
-// order of the 128-walk chord tile so each warp reads/writes 512 contiguous
-// bytes per fragment: [m_tile][walk_tile128][warp(8)][i(8)][j(4)][lane][2].
-__host__ __device__ inline int64_t s_index(int64_t r, int64_t c, int64_t CT128) {
-  const int64_t mt = r / BM, rr = r % BM, wm = rr / 64, i = (rr % 64) / 8, rq = rr % 8;
-  const int64_t ct = c / 128, cc = c % 128, wn = cc / 32, j = (cc % 32) / 8, cq = (cc % 8) / 2,
+// order of the incremental chord tile (128 rows x 64 walks, 8 warps as
+// 4 row-groups x 2 walk-groups, warp tile 32 x 32) so each warp reads and
+// writes 512 contiguous bytes per fragment:
+// [m_tile][walk_tile64][warp(8)][i(4)][j(4)][lane(32)][2].
+constexpr int64_t S_WARP_BLOCK = 4 * 4 * 32 * 2;  // doubles per warp per tile
+__host__ __device__ inline int64_t s_index(int64_t r, int64_t c, int64_t CT64) {
+  const int64_t mt = r / BM, rr = r % BM, wm = rr / 32, i = (rr % 32) / 8, rq = rr % 8;
+  const int64_t ct = c / BC, cc = c % BC, wn = cc / 32, j = (cc % 32) / 8, cq = (cc % 8) / 2,
                 e = cc % 2;
-  const int64_t warp = wm * 4 + wn, lane = rq * 4 + cq;
-  return (((((mt * CT128 + ct) * 8 + warp) * 8 + i) * 4 + j) * 32 + lane) * 2 + e;
+  const int64_t warp = wm * 2 + wn, lane = rq * 4 + cq;
+  return (((((mt * CT64 + ct) * 8 + warp) * 4 + i) * 4 + j) * 32 + lane) * 2 + e;
 }
 
 // ---------------------------------------------------------------------------
@@ -201,6 +204,24 @@ __device__ inline void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint
           "r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// Same copy with an L2 eviction-priority policy (createpolicy).
+__device__ inline void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                     uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ inline uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// Bulk prefetch of [src, src + bytes) into L2 (no smem destination).
+__device__ inline void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 // D = A(8x4, row) * B(4x8, col) + D, fp64 tensor core (SASS DMMA.8x8x4).
 __device__ inline void dmma884(double& d0, double& d1, double a, double b) {

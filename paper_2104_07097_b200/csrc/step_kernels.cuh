@@ -66,6 +66,16 @@ __global__ void unpack_b_kernel(const double* __restrict__ src, int64_t n, int64
   }
 }
 
+// *flag = 1 if a and b differ anywhere (bitwise).
+__global__ void differs_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                               int64_t total, int* flag) {
+  int d = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d |= __double_as_longlong(a[i]) != __double_as_longlong(b[i]);
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
 // x0 replicated into every walk column (run(), sampler.cpp:300).
 __global__ void broadcast_state_kernel(const double* __restrict__ x0, int64_t n, int64_t z,
                                        int64_t z_pad, int64_t KT, double* __restrict__ X) {
@@ -281,7 +291,7 @@ struct RedrawParams {
   double* D;              // packed (updated on success)
   const double* P;        // n x n column-major, or null
   double* R;              // incremental rate cache (s_index) or null
-  int64_t ct128;
+  int64_t ct64;
   double* scratch;        // 3 n doubles per CTA
   double* lower;
   double* upper;
@@ -391,7 +401,7 @@ __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
           ad = fma(a, ds[k], ad);
         }
         const double sl = rp.b[r] - ax;
-        if (rp.R) rp.R[s_index(r, c, rp.ct128)] = ad;
+        if (rp.R) rp.R[s_index(r, c, rp.ct64)] = ad;
         if (ad > rp.eps_dir) {
           pos = 1.0;
           thi = fmin(thi, sl / ad);
