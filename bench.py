@@ -152,15 +152,23 @@ def run_reference(args, world, rank):
     if rank != 0:
         return
     from paper_2104_07097_b200 import workloads
+    import oracle
     w = workloads.config(args.config, z=args.z)
     threads = os.cpu_count() or 1
-    steps = []
+    oracle.lib().orc_set_threads(threads)
+    p = w.polytope
+    X = np.zeros((p.dim(), args.cpu_walks), order="F")
+    X[:] = w.x0[:, None]
+    rng = oracle.WalkRng(args.seed, args.cpu_walks)
+    P = oracle.compute_projection(p.a_eq)[1] if p.num_equalities() else None
     for _ in range(args.warmup):
-        cpu_sample(w, args.cpu_walks, 1, threads)
+        assert oracle.step(p.a_in, p.b_in, P, 1e-11, rng, X)[0] == 0
+    total = 0.0
     for _ in range(args.steps):
-        v, _ = cpu_sample(w, args.cpu_walks, 1, threads)
-        steps.append(v)
-    value = statistics.median(steps)
+        t0 = time.perf_counter()
+        assert oracle.step(p.a_in, p.b_in, P, 1e-11, rng, X)[0] == 0
+        total += time.perf_counter() - t0
+    value = args.cpu_walks * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "chain-steps/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
@@ -225,6 +233,17 @@ def run_engine(args, world, rank, local):
     e2e_value = z * world * args.e2e_steps / e2e_s
     bytes_state = p.dim() * z * 8
 
+    # one collection window (outside the timed region): containment of every
+    # walk, rows gathered device-to-device to rank 0 and diagnostics reduced
+    # -- the only collectives of a multi-GPU run (NCCL over NVLink).
+    from paper_2104_07097_b200.distributed import gather_rows, reduce_diagnostics
+    bad, viol, eqv = eng.check_state(eng.eps_feas)
+    rows = torch.empty((z, p.dim()), dtype=torch.float64, device=f"cuda:{local}")
+    eng.state_rows_to_device(rows.data_ptr())
+    diag = reduce_diagnostics(st["redraw_count"], float(viol.max()), float(eqv.max()), rows,
+                              device=rows.device)
+    gathered = gather_rows(rows, [z] * world)
+
     fpi = eng.flops_per_iterate()
     chord_avg_ms = st["chord_ms"] / max(st["chord_timed"], 1)
     achieved = st["chord_flops"] / max(st["chord_ms"] * 1e-3, 1e-30) / 1e12
@@ -261,6 +280,11 @@ def run_engine(args, world, rank, local):
                 "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
         "gpu_launches": st["kernel_launches"],
         "clocks": clk.summary(),
+        "checks": {"walks_gathered_on_rank0": int(gathered.shape[0]),
+                   "max_violation": diag.max_violation, "max_eq_residual": diag.max_eq_residual,
+                   "all_inside_eps_feas": bool(diag.max_violation <= 1e-9 and
+                                               diag.max_eq_residual <= 1e-9),
+                   "redraws": diag.redraws},
     }
     if cpu:
         line["cpu_baseline"] = cpu

@@ -1,0 +1,232 @@
+// Host shim: the reference's C++ sampler API over the engine's C ABI.
+#include "mhar/sampler.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "../../../include/mhar_b200.h"
+
+namespace mhar {
+
+// ----------------------------------------------------------------- errors --
+const char* error_code_name(ErrorCode code) {
+  static const char* names[] = {"INVALID_ARGUMENT",  "DIMENSION_MISMATCH", "SINGULAR_MATRIX",
+                                "RANK_DEFICIENT_EQ", "EMPTY_POLYTOPE",     "NO_INTERIOR",
+                                "UNBOUNDED_POLYTOPE", "DIRECTION_DEGENERATE", "RETRY_EXHAUSTED",
+                                "CYCLE_SUSPECTED",   "DEGENERATE_TEST",    "NUMERICAL_FAILURE",
+                                "IO_FAILURE"};
+  const int i = static_cast<int>(code);
+  return (i >= 0 && i < 13) ? names[i] : "UNKNOWN";
+}
+
+Error::Error(ErrorCode code, const std::string& message)
+    : std::runtime_error(std::string(error_code_name(code)) + ": " + message), code_(code) {}
+
+void raise(ErrorCode code, const std::string& message) { throw Error(code, message); }
+
+namespace {
+// C-ABI status -> mhar::Error (the engine's message already names the code).
+void check(int status) {
+  if (status == MHAR_OK) return;
+  const std::string msg = mhar_last_error();
+  if (status == MHAR_ERR_CUDA) throw std::runtime_error("CUDA: " + msg);
+  throw Error(static_cast<ErrorCode>(status - 1), msg);
+}
+}  // namespace
+
+// --------------------------------------------------------------- polytope --
+Polytope::Polytope(Matrix a_in_, Vector b_in_) : a_in(std::move(a_in_)), b_in(std::move(b_in_)) {
+  a_eq = Matrix(0, a_in.cols());
+}
+Polytope::Polytope(Matrix a_in_, Vector b_in_, Matrix a_eq_, Vector b_eq_)
+    : a_in(std::move(a_in_)), b_in(std::move(b_in_)), a_eq(std::move(a_eq_)),
+      b_eq(std::move(b_eq_)) {}
+
+bool contains(const Polytope& p, const double* x, double eps) {
+  for (Index i = 0; i < p.a_in.rows(); ++i) {
+    double s = 0.0;
+    for (Index j = 0; j < p.a_in.cols(); ++j) s += p.a_in(i, j) * x[j];
+    if (s - p.b_in(i) > eps) return false;
+  }
+  for (Index i = 0; i < p.a_eq.rows(); ++i) {
+    double s = 0.0;
+    for (Index j = 0; j < p.a_eq.cols(); ++j) s += p.a_eq(i, j) * x[j];
+    if (std::fabs(s - p.b_eq(i)) > eps) return false;
+  }
+  return true;
+}
+
+Polytope make_hypercube(int n) {
+  if (n < 1) raise(ErrorCode::invalid_argument, "make_hypercube: n must be >= 1");
+  Matrix a(2 * n, n);
+  for (int i = 0; i < n; ++i) {
+    a(i, i) = 1.0;
+    a(n + i, i) = -1.0;
+  }
+  return Polytope(std::move(a), Vector::Ones(2 * n));
+}
+
+Polytope make_simplex(int n) {
+  if (n < 2) raise(ErrorCode::invalid_argument, "make_simplex: n must be >= 2");
+  Matrix a(n, n);
+  for (int i = 0; i < n; ++i) a(i, i) = -1.0;
+  return Polytope(std::move(a), Vector::Zero(n), Matrix::Constant(1, n, 1.0), Vector::Ones(1));
+}
+
+// ------------------------------------------------------------- projection --
+ProjectionOperator compute_projection(const Matrix& a_eq) {
+  if (a_eq.rows() == 0) raise(ErrorCode::invalid_argument, "compute_projection: empty");
+  ProjectionOperator op;
+  op.source_eq = a_eq;
+  op.p = Matrix(a_eq.cols(), a_eq.cols());
+  op.gram_inverse = Matrix(a_eq.rows(), a_eq.rows());
+  check(mhar_compute_projection(a_eq.data(), a_eq.rows(), a_eq.cols(), op.p.data(),
+                                op.gram_inverse.data()));
+  return op;
+}
+
+// ---------------------------------------------------------------- engine --
+class Engine {
+ public:
+  Engine(const Polytope& p, const ProjectionOperator* projector, int z, uint64_t seed,
+         double eps_dir, double eps_feas, int rng_mode) {
+    mhar_polytope poly{p.dim(), p.num_inequalities(), p.num_equalities(), p.a_in.data(),
+                       p.b_in.data(), p.num_equalities() ? p.a_eq.data() : nullptr,
+                       p.num_equalities() ? p.b_eq.data() : nullptr};
+    mhar_options opt;
+    mhar_default_options(&opt);
+    opt.z = z;
+    opt.seed = seed;
+    opt.eps_dir = eps_dir;
+    opt.eps_feas = eps_feas;
+    opt.rng = rng_mode;
+    check(mhar_ctx_create(&poly, projector ? projector->p.data() : nullptr,
+                          projector ? projector->gram_inverse.data() : nullptr, &opt, &ctx_));
+    eps_dir_ = eps_dir;
+  }
+  ~Engine() { mhar_ctx_destroy(ctx_); }
+  mhar_ctx* ctx() { return ctx_; }
+  double eps_dir() const { return eps_dir_; }
+  long long redraws() {
+    mhar_ctx_stats s;
+    check(mhar_get_stats(ctx_, &s));
+    return s.redraw_count;
+  }
+
+ private:
+  mhar_ctx* ctx_ = nullptr;
+  double eps_dir_ = 0.0;
+};
+
+// ---------------------------------------------------------------- sampler --
+SamplerConfig resolve(const SamplerConfig& cfg, const Polytope& p) {
+  SamplerConfig r = cfg;
+  const int n = p.dim();
+  const long long walk_dim = n - p.num_equalities();
+  if (r.z == 0) r.z = std::max(p.num_inequalities(), n) + 1;
+  if (r.phi == 0) r.phi = walk_dim * walk_dim * walk_dim;
+  if (r.burn_in < 0) r.burn_in = r.phi;
+  if (r.reproject_every < 0) r.reproject_every = r.phi;
+  if (r.z < 1) raise(ErrorCode::invalid_argument, "config: z must be >= 1");
+  if (r.phi < 1) raise(ErrorCode::invalid_argument, "config: phi must be >= 1");
+  if (r.t_target < 1) raise(ErrorCode::invalid_argument, "config: t_target must be >= 1");
+  if (!(r.eps_dir > 0.0)) raise(ErrorCode::invalid_argument, "config: eps_dir must be > 0");
+  if (!(r.eps_feas > 0.0)) raise(ErrorCode::invalid_argument, "config: eps_feas must be > 0");
+  return r;
+}
+
+LambdaIntervals compute_lambda_intervals(const Polytope& p, const Matrix& x, const Matrix& d,
+                                         double eps_dir) {
+  const Index n = p.dim(), z = x.cols();
+  if (x.rows() != n || d.rows() != n || d.cols() != z) {
+    raise(ErrorCode::dimension_mismatch, "compute_lambda_intervals: x is " +
+                                             std::to_string(x.rows()) + "x" +
+                                             std::to_string(x.cols()) + ", d is " +
+                                             std::to_string(d.rows()) + "x" +
+                                             std::to_string(d.cols()) + ", polytope dim " +
+                                             std::to_string(n));
+  }
+  Engine eng(p, nullptr, static_cast<int>(z), 0, eps_dir, 1e-9, MHAR_RNG_PHILOX);
+  LambdaIntervals out;
+  out.lower = Vector(z);
+  out.upper = Vector(z);
+  std::vector<uint8_t> flags(static_cast<size_t>(z));
+  check(mhar_lambda_intervals(eng.ctx(), x.data(), d.data(), out.lower.data(), out.upper.data(),
+                              flags.data()));
+  out.degenerate.resize(static_cast<size_t>(z));
+  for (Index k = 0; k < z; ++k)
+    out.degenerate[static_cast<size_t>(k)] = flags[static_cast<size_t>(k)] & MHAR_FLAG_DEGENERATE;
+  return out;
+}
+
+double chord_point(double u, double lower, double upper) { return lower + u * (upper - lower); }
+
+WalkRng::WalkRng(uint64_t seed, int z) : seed_(seed), z_(z) {
+  if (z < 1) raise(ErrorCode::invalid_argument, "WalkRng: z must be >= 1, got " + std::to_string(z));
+}
+WalkRng::~WalkRng() = default;
+
+void step(const Polytope& p, const ProjectionOperator* projector, const SamplerConfig& cfg,
+          WalkRng& rng, WalkState& state) {
+  if (state.x.cols() != rng.width() || state.x.rows() != p.dim())
+    raise(ErrorCode::dimension_mismatch, "step: state does not match the rng width / polytope");
+  // The walks' streams live with the device context: created on the first
+  // step for this polytope, reused while the caller keeps stepping it.
+  if (!rng.engine_ || rng.bound_ != &p || rng.engine_->eps_dir() != cfg.eps_dir) {
+    rng.engine_ = std::make_unique<Engine>(p, projector, rng.width(), rng.seed(), cfg.eps_dir,
+                                           cfg.eps_feas, MHAR_RNG_REFERENCE);
+    rng.bound_ = &p;
+  }
+  mhar_ctx* ctx = rng.engine_->ctx();
+  const long long before = rng.engine_->redraws();
+  check(mhar_set_state(ctx, state.x.data()));
+  int st = mhar_step(ctx, 1, 0);
+  if (st == MHAR_OK) st = mhar_sync(ctx);
+  state.redraws += rng.engine_->redraws() - before;
+  check(st);
+  check(mhar_get_state(ctx, state.x.data()));
+  ++state.j;
+}
+
+SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0, const ClockFn& clock) {
+  const SamplerConfig rc = resolve(cfg, p);
+  if (x0.size() != p.dim()) raise(ErrorCode::dimension_mismatch, "run: x0 has the wrong size");
+  auto now = [&clock]() {
+    if (clock) return clock();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  };
+  const double t0 = now();
+  std::unique_ptr<ProjectionOperator> projector;
+  if (p.num_equalities() > 0)
+    projector = std::make_unique<ProjectionOperator>(compute_projection(p.a_eq));
+  const long long windows = (rc.t_target + rc.z - 1) / rc.z;
+  Engine eng(p, projector.get(), rc.z, rc.seed, rc.eps_dir, rc.eps_feas, MHAR_RNG_REFERENCE);
+  SampleSet out;
+  out.config = rc;
+  out.start = x0;
+  out.windows = windows;
+  out.samples = Matrix(windows * rc.z, p.dim());
+  // the engine writes row-major (windows*z) x n; transpose into the
+  // column-major Matrix (one collected point per row, like the reference)
+  std::vector<double> rows(static_cast<size_t>(windows * rc.z * p.dim()));
+  mhar_run_config rcfg{rc.phi, windows, rc.burn_in, projector ? rc.reproject_every : 0};
+  mhar_run_stats stats;
+  check(mhar_run(eng.ctx(), &rcfg, x0.data(), rows.data(), &stats));
+  const Index n = p.dim();
+  for (Index r = 0; r < windows * rc.z; ++r)
+    for (Index j = 0; j < n; ++j) out.samples(r, j) = rows[static_cast<size_t>(r * n + j)];
+  out.seconds = now() - t0;
+  out.iterate_count = stats.iterate_count;
+  out.redraw_count = stats.redraw_count;
+  return out;
+}
+
+SampleSet run(const Polytope&, const SamplerConfig&, const ClockFn&) {
+  raise(ErrorCode::invalid_argument,
+        "run: pass a warm start x0 (Chebyshev centering is not part of the engine)");
+}
+
+}  // namespace mhar

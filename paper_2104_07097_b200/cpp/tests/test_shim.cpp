@@ -1,0 +1,217 @@
+// C++ tests of the drop-in host API, restating the reference's own doctest
+// cases (/root/reference/proj/tests/test_sampler.cpp, test_projection.cpp)
+// against the B200 engine.  The z = 1 equivalence compares with the CPU
+// oracle (oracle/mhar_oracle.h, test infrastructure) on the same streams.
+// Run by tests/test_cpp_shim.py on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "../../../oracle/mhar_oracle.h"
+#include "mhar/sampler.hpp"
+
+using mhar::Matrix;
+using mhar::Vector;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                          \
+  do {                                                                       \
+    if (!(cond)) {                                                           \
+      std::printf("  FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+      ++g_fail;                                                              \
+    }                                                                        \
+  } while (0)
+
+template <typename F>
+static void expect_error(mhar::ErrorCode code, F f) {
+  try {
+    f();
+    std::printf("  FAILED: expected %s\n", mhar::error_code_name(code));
+    ++g_fail;
+  } catch (const mhar::Error& e) {
+    CHECK(e.code() == code);
+  }
+}
+
+static void run_case(const char* name, const std::function<void()>& body) {
+  const int before = g_fail;
+  try {
+    body();
+  } catch (const std::exception& e) {
+    std::printf("  FAILED: unexpected exception %s\n", e.what());
+    ++g_fail;
+  }
+  std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", name);
+  if (g_fail == before) ++g_pass;
+}
+
+int main() {
+  run_case("config defaults derive from the polytope shape", [] {
+    const auto cube = mhar::make_hypercube(5);
+    const auto rc = mhar::resolve(mhar::SamplerConfig{}, cube);
+    CHECK(rc.z == 11 && rc.phi == 125 && rc.burn_in == 125 && rc.reproject_every == 125);
+    const auto rs = mhar::resolve(mhar::SamplerConfig{}, mhar::make_simplex(4));
+    CHECK(rs.z == 5 && rs.phi == 27);
+    mhar::SamplerConfig bad;
+    bad.z = -2;
+    expect_error(mhar::ErrorCode::invalid_argument, [&] { mhar::resolve(bad, cube); });
+  });
+
+  run_case("chord bounds on the box match hand geometry", [] {
+    const auto cube = mhar::make_hypercube(2);
+    Matrix x(2, 2), d(2, 2);
+    x(0, 1) = 0.5;
+    d(0, 0) = 1.0;
+    d(0, 1) = 1.0;
+    const auto iv = mhar::compute_lambda_intervals(cube, x, d, 1e-11);
+    CHECK(iv.lower(0) == -1.0 && iv.upper(0) == 1.0);
+    CHECK(iv.lower(1) == -1.5 && iv.upper(1) == 0.5);
+    CHECK(iv.degenerate[0] == 0 && iv.degenerate[1] == 0);
+  });
+
+  run_case("all-parallel directions are flagged", [] {
+    const auto cube = mhar::make_hypercube(2);
+    Matrix x(2, 1), d(2, 1);
+    d(0, 0) = 1.0;
+    const auto iv = mhar::compute_lambda_intervals(cube, x, d, 1e9);
+    CHECK(iv.degenerate[0] == 1);
+  });
+
+  run_case("one-sided chords report an unbounded body", [] {
+    Matrix a(2, 2);
+    a(0, 0) = a(1, 1) = -1.0;
+    const mhar::Polytope quadrant(a, Vector::Zero(2));
+    Matrix x(2, 1, 1.0), d(2, 1);
+    d(0, 0) = 0.3;
+    d(1, 0) = 1.0;
+    expect_error(mhar::ErrorCode::unbounded_polytope,
+                 [&] { mhar::compute_lambda_intervals(quadrant, x, d, 1e-11); });
+  });
+
+  run_case("single steps keep every walk inside the body", [] {
+    const auto cube = mhar::make_hypercube(4);
+    const auto cfg = mhar::resolve(mhar::SamplerConfig{}, cube);
+    mhar::WalkRng rng(cfg.seed, 6);
+    mhar::WalkState state;
+    state.x = Matrix::Zero(4, 6);
+    for (int it = 0; it < 50; ++it) {
+      mhar::step(cube, nullptr, cfg, rng, state);
+      for (int k = 0; k < 6; ++k) CHECK(mhar::contains(cube, state.x.col(k), 1e-12));
+    }
+    CHECK(state.j == 50);
+  });
+
+  run_case("projected steps never leave the equality slice", [] {
+    const auto simplex = mhar::make_simplex(5);
+    const auto cfg = mhar::resolve(mhar::SamplerConfig{}, simplex);
+    const auto op = mhar::compute_projection(simplex.a_eq);
+    mhar::WalkRng rng(cfg.seed, 4);
+    mhar::WalkState state;
+    state.x = Vector::Constant(5, 0.2).replicate(4);
+    for (int it = 0; it < 200; ++it) mhar::step(simplex, &op, cfg, rng, state);
+    for (int k = 0; k < 4; ++k) {
+      double s = 0;
+      for (int i = 0; i < 5; ++i) s += state.x(i, k);
+      CHECK(std::fabs(s - 1.0) <= 1e-9);
+      CHECK(mhar::contains(simplex, state.x.col(k), 1e-9));
+    }
+  });
+
+  run_case("hopeless direction retries give up with the retry error", [] {
+    const auto cube = mhar::make_hypercube(2);
+    auto cfg = mhar::resolve(mhar::SamplerConfig{}, cube);
+    cfg.eps_dir = 1e9;
+    mhar::WalkRng rng(55, 1);
+    mhar::WalkState state;
+    state.x = Matrix::Zero(2, 1);
+    expect_error(mhar::ErrorCode::retry_exhausted,
+                 [&] { mhar::step(cube, nullptr, cfg, rng, state); });
+    CHECK(state.redraws == mhar::kMaxDirectionRetries);
+  });
+
+  run_case("full runs count batches, windows, and iterates", [] {
+    const auto cube = mhar::make_hypercube(3);
+    mhar::SamplerConfig cfg;
+    cfg.z = 2;
+    cfg.phi = 3;
+    cfg.t_target = 4;
+    cfg.burn_in = 0;
+    cfg.seed = 7;
+    const auto out = mhar::run(cube, cfg, Vector::Zero(3));
+    CHECK(out.samples.rows() == 4 && out.samples.cols() == 3);
+    CHECK(out.windows == 2 && out.iterate_count == 12);
+    for (int r = 0; r < 4; ++r) {
+      double x[3] = {out.samples(r, 0), out.samples(r, 1), out.samples(r, 2)};
+      CHECK(mhar::contains(cube, x, cfg.eps_feas));
+    }
+    expect_error(mhar::ErrorCode::invalid_argument, [&] { mhar::run(cube, cfg); });
+  });
+
+  run_case("runs are bit-reproducible per seed and move between seeds", [] {
+    const auto cube = mhar::make_hypercube(4);
+    mhar::SamplerConfig cfg;
+    cfg.z = 3;
+    cfg.phi = 10;
+    cfg.t_target = 30;
+    cfg.seed = 99;
+    const auto a = mhar::run(cube, cfg, Vector::Zero(4));
+    const auto b = mhar::run(cube, cfg, Vector::Zero(4));
+    CHECK(a.samples == b.samples);
+    cfg.seed = 100;
+    const auto c = mhar::run(cube, cfg, Vector::Zero(4));
+    CHECK(!(a.samples == c.samples));
+  });
+
+  run_case("box moments settle near the uniform law", [] {
+    const auto cube = mhar::make_hypercube(5);
+    mhar::SamplerConfig cfg;
+    cfg.z = 100;
+    cfg.phi = 125;
+    cfg.t_target = 10000;
+    cfg.seed = 11;
+    const auto out = mhar::run(cube, cfg, Vector::Zero(5));
+    CHECK(out.samples.rows() == 10000);
+    for (int c = 0; c < 5; ++c) {
+      double m = 0, v = 0;
+      for (int r = 0; r < 10000; ++r) m += out.samples(r, c);
+      m /= 10000;
+      for (int r = 0; r < 10000; ++r) v += (out.samples(r, c) - m) * (out.samples(r, c) - m);
+      v /= 9999;
+      CHECK(std::fabs(m) <= 0.05 && std::fabs(v - 1.0 / 3.0) <= 0.05);
+    }
+  });
+
+  run_case("simplex projector is exact and z=1 walks retrace the oracle", [] {
+    const auto simplex = mhar::make_simplex(4);
+    const auto op = mhar::compute_projection(simplex.a_eq);
+    Matrix expected(4, 4, -0.25);
+    for (int i = 0; i < 4; ++i) expected(i, i) = 0.75;
+    CHECK(op.p == expected);
+    for (int body = 0; body < 2; ++body) {
+      const auto p = body == 0 ? mhar::make_hypercube(5) : simplex;
+      const auto cfg = mhar::resolve(mhar::SamplerConfig{}, p);
+      const uint64_t seed = 4242;
+      mhar::WalkRng rng(seed, 1);
+      mhar::WalkState state;
+      const int n = p.dim();
+      state.x = Vector::Constant(n, body == 0 ? 0.0 : 0.25).replicate(1);
+      std::vector<double> xr(state.x.data(), state.x.data() + n);
+      uint64_t col = orc_stream_init(seed, 0), th = orc_stream_init(seed, ~0ULL);
+      int64_t red = 0, err = -1;
+      double worst = 0.0;
+      for (int it = 0; it < 1000; ++it) {
+        mhar::step(p, body == 0 ? nullptr : &op, cfg, rng, state);
+        CHECK(orc_step(p.a_in.data(), p.b_in.data(), p.num_inequalities(), n,
+                       body == 0 ? nullptr : op.p.data(), cfg.eps_dir, &col, &th, xr.data(), 1,
+                       &red, &err) == 0);
+        for (int j = 0; j < n; ++j) worst = std::fmax(worst, std::fabs(state.x(j, 0) - xr[j]));
+      }
+      CHECK(worst <= 1e-12);
+    }
+  });
+
+  std::printf("%d passed, %d failed checks\n", g_pass, g_fail);
+  return g_fail == 0 ? 0 : 1;
+}

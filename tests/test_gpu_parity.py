@@ -334,3 +334,34 @@ def test_config3_full_width_stays_inside():
     ax = w.polytope.a_in @ X[:, :16]
     assert (ax - w.polytope.b_in[:, None]).max() <= 1e-9
     assert np.abs(X).max() > 0.05  # the walks moved
+
+
+def test_sharding_invariance_global_walk_ids():
+    # Philox is keyed on the global walk id: one engine over 192 walks and
+    # three shards of 64 (chain_offset 0, 64, 128) produce the same walks --
+    # the multi-GPU sample set does not depend on the GPU count.
+    p = workloads.random_polytope(40, 900, seed=4)
+    z, steps = 192, 12
+    with mh.Engine(p, z, seed=21) as eng:
+        eng.set_state(np.zeros((40, z)))
+        eng.step(steps)
+        whole = eng.get_state()
+    parts = []
+    for off in (0, 64, 128):
+        with mh.Engine(p, 64, seed=21, chain_offset=off) as eng:
+            eng.set_state(np.zeros((40, 64)))
+            eng.step(steps)
+            parts.append(eng.get_state())
+    assert np.array_equal(whole, np.hstack(parts))
+
+
+def test_state_rows_to_device_and_gather_layout():
+    import torch
+    p = mh.make_hypercube(6)
+    with mh.Engine(p, 70, seed=3) as eng:
+        eng.set_state(np.zeros((6, 70)))
+        eng.step(5)
+        X = eng.get_state()
+        rows = torch.empty((70, 6), dtype=torch.float64, device="cuda:0")
+        eng.state_rows_to_device(rows.data_ptr())
+    assert np.array_equal(rows.cpu().numpy(), X.T)
