@@ -185,6 +185,49 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# The paper's published MHAR throughputs (fp64,
+# best padding z* per body/dimension): (figure, n, z*, samples/s).
+PAPER_TABLE = [
+    ("hypercube", 3, 10000, 25357073.87), ("hypercube", 5, 10000, 13206089.93),
+    ("hypercube", 15, 10000, 25344794.68), ("hypercube", 25, 5000, 10839474.35),
+    ("hypercube", 50, 2500, 5151516.81), ("hypercube", 100, 4000, 4363525.70),
+    ("hypercube", 250, 3000, 1219419.53), ("hypercube", 500, 4000, 621554.24),
+    ("hypercube", 1000, 4000, 248513.69), ("hypercube", 2500, 1500, 50808.74),
+    ("hypercube", 5000, 1000, 16161.69),
+    ("simplex", 3, 10000, 19795014.21), ("simplex", 5, 10000, 22878783.33),
+    ("simplex", 15, 10000, 24269548.32), ("simplex", 25, 10000, 24338761.06),
+    ("simplex", 50, 10000, 13425900.57), ("simplex", 100, 3000, 7255837.08),
+    ("simplex", 250, 4000, 2656449.22), ("simplex", 500, 1500, 944784.52),
+    ("simplex", 1000, 500, 329315.49), ("simplex", 2500, 500, 77312.01),
+    ("simplex", 5000, 1000, 22437.63),
+]
+
+
+def run_paper(args):
+    """The paper's own benchmark (Avg. samples/s = z phi T / Time,
+    PAPER.md:694-698) on its bodies and padding z*, through run() on one
+    B200: phi is sized so each run takes ~0.5 s (the paper used 30,000)."""
+    import paper_2104_07097_b200 as mh
+    out = []
+    for fig, n, z, paper in PAPER_TABLE:
+        if fig == "hypercube":
+            p, x0 = mh.make_hypercube(n), np.zeros(n)
+        else:
+            p, x0 = mh.make_simplex(n), np.full(n, 1.0 / n)
+        proj = mh.compute_projection(p.a_eq) if p.num_equalities() else None
+        with mh.Engine(p, z, seed=args.seed, projector=proj) as eng:
+            _, st = eng.run(x0, 20, 1, 0, 20 if proj else 0)  # warm-up + cost probe
+            per_iter = st.seconds / 20
+            phi = int(min(30000, max(50, 0.5 / max(per_iter, 1e-9))))
+            _, st = eng.run(x0, phi, 1, 0, phi if proj else 0)
+        value = z * phi / st.seconds
+        rec = {"figure": fig, "n": n, "z": z, "phi": phi, "seconds": st.seconds,
+               "chain_steps_per_s": value, "paper_p100": paper, "ratio_vs_paper": value / paper}
+        out.append(rec)
+        print(json.dumps(rec), flush=True)
+    return out
+
+
 def run_engine(args, world, rank, local):
     import paper_2104_07097_b200 as mh
     from paper_2104_07097_b200 import workloads
@@ -307,10 +350,14 @@ def main():
     ap.add_argument("--cpu-walks", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--paper", action="store_true",
+                    help="run the paper's hypercube/simplex table (PAPER.md:845-887) instead")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
-    if args.impl == "reference":
+    if args.paper:
+        run_paper(args)
+    elif args.impl == "reference":
         run_reference(args, world, rank)
     else:
         run_engine(args, world, rank, local)
