@@ -94,6 +94,8 @@ typedef struct {
   int slack_mode;        /* MHAR_SLACK_* */
   int64_t refresh_every; /* incremental mode: fused refresh cadence (0 = default 64) */
   int device;            /* CUDA ordinal */
+  int small_path;        /* 1 (default): bodies whose A_I, P, A_E fit in shared memory run
+                            all iterates of a batch in one walk-resident launch (Philox only) */
 } mhar_options;
 
 /* Fills o with the reference defaults (sampler.hpp:16-25): eps_dir 1e-11,

@@ -94,7 +94,8 @@ class _Polytope(C.Structure):
 class _Options(C.Structure):
     _fields_ = [("z", C.c_int64), ("chain_offset", C.c_int64), ("seed", C.c_uint64),
                 ("eps_dir", C.c_double), ("eps_feas", C.c_double), ("rng", C.c_int),
-                ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int)]
+                ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int),
+                ("small_path", C.c_int)]
 
 
 class _RunConfig(C.Structure):
@@ -334,13 +335,14 @@ class Engine:
     independent of the GPU count) or "reference" (the reference's SplitMix
     streams: column stream k and the shared theta stream, rng.hpp:42-55).
     slack: "incremental" (default) or "recompute" (one fused A_I[X|D] pass
-    per iterate).
+    per iterate).  small_path: allow the walk-resident kernel for bodies that
+    fit in shared memory (Philox only).
     """
 
     def __init__(self, p: Polytope, z: int, seed: int = 0, projector: Optional[ProjectionOperator] = None,
                  eps_dir: float = 1e-11, eps_feas: float = 1e-9, rng: str = "philox",
                  slack: str = "incremental", refresh_every: int = 128, device: int = 0,
-                 chain_offset: int = 0):
+                 chain_offset: int = 0, small_path: bool = True):
         L = lib()
         self.p = p
         self.n = p.dim()
@@ -366,6 +368,7 @@ class Engine:
         opt.slack_mode = {"recompute": SLACK_RECOMPUTE, "incremental": SLACK_INCREMENTAL}[slack]
         opt.refresh_every = int(refresh_every)
         opt.device = int(device)
+        opt.small_path = 1 if small_path else 0
         P = G = None
         if projector is not None:
             P = _f(projector.p)

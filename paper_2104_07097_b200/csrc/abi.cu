@@ -21,6 +21,7 @@
 #include "chord_kernel.cuh"
 #include "host_linalg.h"
 #include "step_kernels.cuh"
+#include "small_kernel.cuh"
 
 using namespace mhar_dev;
 
@@ -83,6 +84,11 @@ struct mhar_ctx {
   uint64_t *col_state = nullptr, *theta_state = nullptr;
   int redraw_grid = 1;
   int group_m = 4;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
+  // walk-resident small-body path (small_kernel.cuh); Acm != null enables it
+  double* Acm = nullptr;
+  unsigned long long* walk_err = nullptr;
+  size_t small_smem = 0;
+  int small_ns = 1, small_grid = 0;
 
   // host bookkeeping
   int64_t iterations = 0;
@@ -395,6 +401,49 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
   return 0;
 }
 
+// `iters` iterates of every walk: one walk-resident launch for small bodies,
+// else the per-iterate kernel chain.
+int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
+  if (iters <= 0) return 0;
+  if (!c->Acm) {
+    for (int64_t i = 0; i < iters; ++i) {
+      int s = enqueue_iterate(c, reproject_every, false);
+      if (s) return s;
+    }
+    return 0;
+  }
+  SmallParams sp;
+  sp.A = c->Acm;
+  sp.b = c->b;
+  sp.P = c->me > 0 ? c->Pcm : nullptr;
+  sp.AE = c->AE;
+  sp.bE = c->bE;
+  sp.G = c->G;
+  sp.X = c->X;
+  sp.n = c->n;
+  sp.m = c->m;
+  sp.me = c->me;
+  sp.z = c->z;
+  sp.KT = c->KT;
+  sp.seed = c->opt.seed;
+  sp.chain_offset = c->opt.chain_offset;
+  sp.it0 = c->iterations;
+  sp.iters = iters;
+  sp.reproject_every = c->me > 0 ? reproject_every : 0;
+  sp.eps_dir = c->opt.eps_dir;
+  sp.redraw_total = c->redraw_total;
+  sp.err = c->err;
+  sp.walk_err = c->walk_err;
+  sp.ns = c->small_ns;
+  small_kernel<<<c->small_grid, 32 * SMALL_WARPS, c->small_smem, c->stream>>>(sp);
+  LAUNCH_OK(c, "small_kernel");
+  small_error_kernel<<<1, 256, 0, c->stream>>>(c->walk_err, c->z, c->err);
+  LAUNCH_OK(c, "small_error_kernel");
+  c->iterations += iters;
+  c->slack_valid = false;
+  return 0;
+}
+
 // Decodes the device error word into a status (and message).
 int read_error(mhar_ctx* c, int64_t* walk) {
   unsigned long long w = kNoError;
@@ -465,6 +514,7 @@ void mhar_default_options(mhar_options* o) {
   o->slack_mode = MHAR_SLACK_INCREMENTAL;
   o->refresh_every = 128;
   o->device = 0;
+  o->small_path = 1;
 }
 
 const char* mhar_last_error(void) { return g_last_error.c_str(); }
@@ -570,7 +620,17 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         tmp, c->m, c->n, c->m, c->m_pad, c->KT, c->A);
     ++c->launches;
     cudaStreamSynchronize(c->stream);
-    cudaFree(tmp);
+    // small bodies: keep the column-major copy for the walk-resident kernel
+    c->small_ns = (int)(c->n | 1);
+    const size_t small_bytes =
+        sizeof(double) * small_smem_doubles(c->n, c->m, c->me, c->me > 0, c->small_ns);
+    if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_bytes <= 200 * 1024) {
+      c->Acm = tmp;
+      c->allocs.push_back(tmp);
+      c->small_smem = small_bytes;
+    } else {
+      cudaFree(tmp);
+    }
     std::vector<double> bp(c->m_pad, __builtin_huge_val());
     std::memcpy(bp.data(), p->b_in, sizeof(double) * c->m);
     cudaMemcpy(c->b, bp.data(), sizeof(double) * c->m_pad, cudaMemcpyHostToDevice);
@@ -617,6 +677,17 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   cudaFuncSetAttribute(chord_kernel<FUSED_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
   cudaFuncSetAttribute(chord2_kernel<INCREMENTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   cudaFuncSetAttribute(chord2_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
+  if (c->Acm) {
+    if ((st = dalloc(c, &c->walk_err, c->z))) return bail(st);
+    cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)c->small_smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_kernel, 32 * SMALL_WARPS,
+                                                  c->small_smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t need = (c->z + SMALL_WARPS - 1) / SMALL_WARPS;
+    c->small_grid = (int)std::min<int64_t>(need, (int64_t)per_sm * c->num_sms);
+  }
   if ((st = reset_streams(c))) return bail(st);
   e = cudaStreamSynchronize(c->stream);
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -694,11 +765,7 @@ int mhar_get_state_rows_device(mhar_ctx* c, double* dev_rows) {
 int mhar_step(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   if (!c || iters < 0) return fail(MHAR_ERR_INVALID_ARGUMENT, "step: bad argument");
   CK(cudaSetDevice(c->device));
-  for (int64_t i = 0; i < iters; ++i) {
-    int s = enqueue_iterate(c, reproject_every, false);
-    if (s) return s;
-  }
-  return 0;
+  return advance(c, iters, reproject_every);
 }
 
 int mhar_sync(mhar_ctx* c) {
@@ -715,7 +782,7 @@ int mhar_step_timed(mhar_ctx* c, int64_t iters, int64_t reproject_every, double*
   CK(cudaEventCreate(&t1));
   CK(cudaEventRecord(t0, c->stream));
   int s = 0;
-  for (int64_t i = 0; i < iters && !s; ++i) s = enqueue_iterate(c, reproject_every, false);
+  s = advance(c, iters, reproject_every);
   CK(cudaEventRecord(t1, c->stream));
   CK(cudaEventSynchronize(t1));
   float ms = 0.f;
@@ -861,12 +928,10 @@ int mhar_run(mhar_ctx* c, const mhar_run_config* cfg, const double* x0, double* 
   cudaEventCreate(&t1);
   cudaEventRecord(t0, c->stream);
   int big = 0x7FFFFFFF;
-  for (int64_t i = 0; i < cfg->burn_in; ++i)
-    if ((s = enqueue_iterate(c, cfg->reproject_every, false))) return s;
+  if ((s = advance(c, cfg->burn_in, cfg->reproject_every))) return s;
   int64_t walk = -1;
   for (int64_t w = 0; w < cfg->windows; ++w) {
-    for (int64_t i = 0; i < cfg->phi; ++i)
-      if ((s = enqueue_iterate(c, cfg->reproject_every, false))) return s;
+    if ((s = advance(c, cfg->phi, cfg->reproject_every))) return s;
     if ((s = enqueue_check(c))) return s;
     CK(cudaMemcpyAsync(c->first_bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
     contains_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(
