@@ -55,13 +55,17 @@ def test_small_path_retry_exhausted_and_redraw_count():
 
 
 def test_small_path_unbounded_names_walk():
+    # both paths raise for the same (earliest iterate, lowest) walk
     quadrant = mh.Polytope(-np.eye(2), np.zeros(2))
-    with mh.Engine(quadrant, 5, seed=2) as eng:
-        eng.set_state(np.ones((2, 5)))
-        with pytest.raises(mh.MharError) as e:
-            eng.step(3)
-        assert e.value.code == mh.ErrorCode.unbounded_polytope
-        assert "walk 0" in str(e.value)
+    msgs = []
+    for small in (True, False):
+        with mh.Engine(quadrant, 5, seed=2, small_path=small) as eng:
+            eng.set_state(np.ones((2, 5)))
+            with pytest.raises(mh.MharError) as e:
+                eng.step(3)
+            assert e.value.code == mh.ErrorCode.unbounded_polytope
+            msgs.append(str(e.value))
+    assert msgs[0] == msgs[1]
 
 
 def test_small_path_redraws_match_kernel_chain():
