@@ -238,7 +238,8 @@ def run_engine(args, world, rank, local):
     projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
     reproject = args.reproject if p.num_equalities() else 0
     eng = mh.Engine(p, z, seed=args.seed, projector=projector, slack=args.slack,
-                    refresh_every=args.refresh, device=local, chain_offset=rank * z)
+                    refresh_every=args.refresh, device=local, chain_offset=rank * z,
+                    precision=args.precision)
     X0 = np.zeros((p.dim(), z), order="F")
     X0[:] = w.x0[:, None]
     eng.set_state(X0)
@@ -350,6 +351,8 @@ def main():
     ap.add_argument("--cpu-walks", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
+                    help="32: the fp32 variant (tcgen05 3xTF32 rates, fp64 state)")
     ap.add_argument("--paper", action="store_true",
                     help="run the paper's hypercube/simplex table (PAPER.md:845-887) instead")
     args = ap.parse_args()

@@ -96,6 +96,10 @@ typedef struct {
   int device;            /* CUDA ordinal */
   int small_path;        /* 1 (default): bodies whose A_I, P, A_E fit in shared memory run
                             all iterates of a batch in one walk-resident launch (Philox only) */
+  int precision;         /* 64 (default): fp64 DMMA.  32: the fp32 variant -- A_I rounded to
+                            fp32, rates A_I d on tcgen05 tensor cores (3xTF32, fp32 accuracy),
+                            fp64 slack/state, chords of {A_I x <= b_I - fp32_margin} */
+  double fp32_margin;    /* precision 32: slack margin mu (0 = default 1e-6) */
 } mhar_options;
 
 /* Fills o with the reference defaults (sampler.hpp:16-25): eps_dir 1e-11,

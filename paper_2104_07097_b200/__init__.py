@@ -95,7 +95,7 @@ class _Options(C.Structure):
     _fields_ = [("z", C.c_int64), ("chain_offset", C.c_int64), ("seed", C.c_uint64),
                 ("eps_dir", C.c_double), ("eps_feas", C.c_double), ("rng", C.c_int),
                 ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int),
-                ("small_path", C.c_int)]
+                ("small_path", C.c_int), ("precision", C.c_int), ("fp32_margin", C.c_double)]
 
 
 class _RunConfig(C.Structure):
@@ -342,7 +342,8 @@ class Engine:
     def __init__(self, p: Polytope, z: int, seed: int = 0, projector: Optional[ProjectionOperator] = None,
                  eps_dir: float = 1e-11, eps_feas: float = 1e-9, rng: str = "philox",
                  slack: str = "incremental", refresh_every: int = 128, device: int = 0,
-                 chain_offset: int = 0, small_path: bool = True):
+                 chain_offset: int = 0, small_path: bool = True, precision: int = 64,
+                 fp32_margin: float = 0.0):
         L = lib()
         self.p = p
         self.n = p.dim()
@@ -369,6 +370,9 @@ class Engine:
         opt.refresh_every = int(refresh_every)
         opt.device = int(device)
         opt.small_path = 1 if small_path else 0
+        opt.precision = int(precision)
+        opt.fp32_margin = float(fp32_margin)
+        self.precision = int(precision)
         P = G = None
         if projector is not None:
             P = _f(projector.p)

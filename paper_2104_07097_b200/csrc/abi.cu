@@ -22,6 +22,7 @@
 #include "host_linalg.h"
 #include "step_kernels.cuh"
 #include "small_kernel.cuh"
+#include "chord_tc32.cuh"
 
 using namespace mhar_dev;
 
@@ -86,6 +87,9 @@ struct mhar_ctx {
   int group_m = 4;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
   // walk-resident small-body path (small_kernel.cuh); Acm != null enables it
   double* Acm = nullptr;
+  // fp32 variant (chord_tc32.cuh)
+  float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr, *Dlo = nullptr;
+  int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
   unsigned long long* walk_err = nullptr;
   size_t small_smem = 0;
   int small_ns = 1, small_grid = 0;
@@ -187,6 +191,7 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
   p.group_m = c->group_m;
+  p.tc_walk_tiles = c->tc_walk_tiles;
   return p;
 }
 
@@ -222,6 +227,47 @@ int launch_chord(mhar_ctx* c, int mode, const double* X) {
     // algorithmic flops of this launch: 2 m n per product column
     const double cols = (mode == FUSED || mode == FUSED_STORE) ? 2.0 * c->z : (double)c->z;
     c->pending_flops.push_back(2.0 * (double)c->m * (double)c->n * cols);
+  }
+  return 0;
+}
+
+// fp32 variant: incremental chord with tcgen05 3xTF32 rates.
+int launch_tc32(mhar_ctx* c) {
+  TcParams p;
+  p.Ahi = c->Ahi;
+  p.Alo = c->Alo;
+  p.Dhi = c->Dhi;
+  p.Dlo = c->Dlo;
+  p.S = c->S;
+  p.R = c->R;
+  p.theta_prev = c->theta;
+  p.hi_key = c->hi_key;
+  p.lo_key = c->lo_key;
+  p.viol_key = c->viol_key;
+  p.sides = c->sides;
+  p.err = c->err;
+  p.row_tiles = c->tc_row_tiles;
+  p.walk_tiles = c->tc_walk_tiles;
+  p.KT = c->KT;
+  p.m = c->m;
+  p.z = c->z;
+  p.eps_dir = c->opt.eps_dir;
+  p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 1e-6;
+  p.group_n = 2;
+  const int64_t units = p.row_tiles * p.walk_tiles;
+  const int grid = (int)std::min<int64_t>(units, c->num_sms);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (c->timing) {
+    ev = take_events(c);
+    cudaEventRecord(ev.first, c->stream);
+  }
+  chord_tc32_kernel<<<grid, TC_THREADS, TC_SMEM, c->stream>>>(p);
+  LAUNCH_OK(c, "chord_tc32_kernel");
+  ++c->chord_launches;
+  if (c->timing) {
+    cudaEventRecord(ev.second, c->stream);
+    c->pending.push_back(ev);
+    c->pending_flops.push_back(2.0 * (double)c->m * (double)c->n * (double)c->z);
   }
   return 0;
 }
@@ -284,6 +330,7 @@ int launch_redraw(mhar_ctx* c) {
   rp.P = c->me > 0 ? c->Pcm : nullptr;
   rp.R = (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) ? c->R : nullptr;
   rp.ct64 = c->ct64;
+  rp.tc_walk_tiles = c->tc_walk_tiles;
   rp.scratch = c->redraw_scratch;
   rp.lower = c->lower;
   rp.upper = c->upper;
@@ -383,7 +430,28 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
   } else if (injected) {
     c->slack_valid = false;
   }
-  int s = launch_chord(c, mode, c->X);
+  int s = 0;
+  if (c->Ahi) {
+    // fp32 variant: the tensor cores see D_hi + D_lo; D becomes that direction
+    const int64_t total = c->z_pad * c->KT * BK;
+    tc_split_d_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->D, c->n, c->z_pad, c->KT, c->Dhi, c->Dlo, c->err);
+    LAUNCH_OK(c, "tc_split_d_kernel");
+  }
+  if (c->Ahi && injected) {
+    // test hook of the fp32 path: exact fp64 slack of X into the cache, the
+    // chord of that pass discarded, then the tensor-core rates with theta = 0
+    if ((s = launch_chord(c, FUSED_STORE, c->X))) return s;
+    fill_keys_kernel<<<blocks_for(c->z_pad, 256, 1 << 20), 256, 0, c->stream>>>(
+        c->hi_key, c->lo_key, c->viol_key, c->sides, c->z_pad);
+    LAUNCH_OK(c, "fill_keys_kernel");
+    CK(cudaMemsetAsync(c->theta, 0, sizeof(double) * c->z_pad, c->stream));
+    s = launch_tc32(c);
+  } else if (c->Ahi && mode == INCREMENTAL) {
+    s = launch_tc32(c);
+  } else {
+    s = launch_chord(c, mode, c->X);
+  }
   if (s) return s;
   s = launch_finalize(c, !injected, !injected);
   if (s) return s;
@@ -546,9 +614,17 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   if (!(opt->eps_feas > 0.0)) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: eps_feas must be > 0");
   if (opt->rng != MHAR_RNG_PHILOX && opt->rng != MHAR_RNG_REFERENCE)
     return fail(MHAR_ERR_INVALID_ARGUMENT, "options: unknown rng");
+  if (opt->precision != 0 && opt->precision != 32 && opt->precision != 64)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "options: precision must be 64 or 32");
 
   mhar_ctx* c = new mhar_ctx();
   c->opt = *opt;
+  const bool fp32 = opt->precision == 32;
+  if (fp32) {
+    // the fp32 variant is the incremental tensor-core path (fp64 refreshes)
+    c->opt.slack_mode = MHAR_SLACK_INCREMENTAL;
+    c->opt.small_path = 0;
+  }
   c->device = opt->device;
   c->n = p->n;
   c->m = p->m_in;
@@ -571,10 +647,14 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
 
   c->n_pad = round_up(c->n, BK);
   c->KT = c->n_pad / BK;
-  c->m_pad = round_up(c->m, BM);
+  c->m_pad = round_up(c->m, fp32 ? TC_N : BM);
   c->m_tiles = c->m_pad / BM;
-  c->z_pad = round_up(c->z, 64);
+  c->z_pad = round_up(c->z, fp32 ? TC_M : 64);
   c->ct64 = c->z_pad / 64;
+  if (fp32) {
+    c->tc_row_tiles = c->m_pad / TC_N;
+    c->tc_walk_tiles = c->z_pad / TC_M;
+  }
   c->p_rows_pad = round_up(c->n, BM);
 
   const size_t nzp = (size_t)c->z_pad * c->n_pad;
@@ -603,6 +683,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     if (2 * cache * sizeof(double) + (1ull << 30) > free_b) {
+      if (fp32) return bail(fail(MHAR_ERR_CUDA, "precision 32: not enough HBM for the slack cache"));
       c->opt.slack_mode = MHAR_SLACK_RECOMPUTE;  // not enough HBM for the slack cache
     } else if ((st = dalloc(c, &c->S, cache)) || (st = dalloc(c, &c->R, cache))) {
       return bail(st);
@@ -620,6 +701,23 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         tmp, c->m, c->n, c->m, c->m_pad, c->KT, c->A);
     ++c->launches;
     cudaStreamSynchronize(c->stream);
+    if (fp32) {
+      // A_I rounded to fp32 and split for 3xTF32; the fp64 copy becomes A_hi + A_lo
+      const size_t an = (size_t)c->m_pad * c->n_pad, dn = (size_t)c->z_pad * c->n_pad;
+      if ((st = dalloc(c, &c->Ahi, an)) || (st = dalloc(c, &c->Alo, an)) ||
+          (st = dalloc(c, &c->Dhi, dn)) || (st = dalloc(c, &c->Dlo, dn))) {
+        cudaFree(tmp);
+        return bail(st);
+      }
+      tc_split_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
+          tmp, c->m, c->n, c->m_pad, c->KT, c->Ahi, c->Alo, c->A, c->KT);
+      ++c->launches;
+      cudaMemsetAsync(c->Dhi, 0, dn * sizeof(float), c->stream);
+      cudaMemsetAsync(c->Dlo, 0, dn * sizeof(float), c->stream);
+      cudaStreamSynchronize(c->stream);
+      cudaFuncSetAttribute(chord_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TC_SMEM);
+    }
     // small bodies: keep the column-major copy for the walk-resident kernel
     c->small_ns = (int)(c->n | 1);
     const size_t small_bytes =

@@ -67,7 +67,15 @@ struct ChordParams {
   int64_t z;          // live walks
   double eps_dir;
   int group_m;        // rasterisation band height (m tiles)
+  int64_t tc_walk_tiles;  // > 0: the slack cache uses the fp32-variant layout (tc_s_index)
 };
+
+// Slack-cache index for FUSED_STORE: the layout of whichever kernel consumes it.
+__device__ inline int64_t cache_index(int64_t r, int64_t c, const ChordParams& p) {
+  if (p.tc_walk_tiles > 0)  // tc_s_index (chord_tc32.cuh): [rt(256)][wt(128)][row][walk]
+    return (((r / 256) * p.tc_walk_tiles + c / 128) * 256 + r % 256) * 128 + c % 128;
+  return s_index(r, c, p.col_tiles);
+}
 
 // Unit u -> (row tile, walk tile): bands of group_m row tiles, walk tiles
 // inner, so the CTAs in flight share few A tiles and the walk operand stays
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
           viol[j][e] = fmax(viol[j][e], ax - br);
           scan_row(sl, ad, p.eps_dir, hi[j][e], lo[j][e], sd[j][e]);
           if (MODE == FUSED_STORE) {
-            const int64_t si = s_index(r, c0[j] + 2 * (lane & 3) + e, p.col_tiles);
+            const int64_t si = cache_index(r, c0[j] + 2 * (lane & 3) + e, p);
             p.S[si] = sl;
             p.R[si] = ad;
           }

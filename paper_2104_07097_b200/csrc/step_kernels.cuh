@@ -292,6 +292,7 @@ struct RedrawParams {
   const double* P;        // n x n column-major, or null
   double* R;              // incremental rate cache (s_index) or null
   int64_t ct64;
+  int64_t tc_walk_tiles;  // > 0: fp32-variant cache layout
   double* scratch;        // 3 n doubles per CTA
   double* lower;
   double* upper;
@@ -401,7 +402,10 @@ __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
           ad = fma(a, ds[k], ad);
         }
         const double sl = rp.b[r] - ax;
-        if (rp.R) rp.R[s_index(r, c, rp.ct64)] = ad;
+        if (rp.R)
+          rp.R[rp.tc_walk_tiles > 0
+                   ? (((r / 256) * rp.tc_walk_tiles + c / 128) * 256 + r % 256) * 128 + c % 128
+                   : s_index(r, c, rp.ct64)] = ad;
         if (ad > rp.eps_dir) {
           pos = 1.0;
           thi = fmin(thi, sl / ad);

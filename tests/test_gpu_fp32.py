@@ -1,0 +1,103 @@
+"""The fp32 variant (precision=32): A_I rounded to fp32, rates on tcgen05
+tensor cores in 3xTF32 (csrc/chord_tc32.cuh), fp64 slack/state, chords of
+{A x <= b - mu}.  North-star bar: one iterate within 1e-4 relative of the
+reference step on the same (fp32-rounded) body; every emitted sample exactly
+feasible; moments within Monte-Carlo error."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2104_07097_b200 as mh
+from paper_2104_07097_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+RTOL32 = 1e-4
+
+
+def _tf32(x):
+    u = np.asarray(x, dtype=np.float32).view(np.uint32) & np.uint32(0xFFFFE000)
+    return u.view(np.float32)
+
+
+def split_used(a):
+    """The value the tensor cores see for a: fp32(a) = hi + tf32(fp32(a) - hi)."""
+    a32 = np.asarray(a, dtype=np.float32)
+    hi = _tf32(a32)
+    lo = _tf32((a32 - hi).astype(np.float32))
+    return hi.astype(np.float64) + lo.astype(np.float64)
+
+
+def _interior(p, z, rng, shrink=0.4):
+    X = rng.uniform(-1, 1, (p.dim(), z))
+    s = np.max((p.a_in @ X) / p.b_in[:, None], axis=0)
+    return np.asfortranarray(X * (shrink / s))
+
+
+@pytest.mark.parametrize("n,m,z", [(16, 300, 128), (37, 1000, 200), (500, 20000, 256)])
+def test_fp32_injected_step_parity(orc, n, m, z):
+    p = workloads.random_polytope(n, m, seed=n)
+    rng = np.random.default_rng(m)
+    X = _interior(p, z, rng)
+    H = np.asfortranarray(rng.standard_normal((n, z)))
+    U = rng.uniform(0.05, 0.95, z)
+    with mh.Engine(p, z, precision=32) as eng:
+        eng.set_state(X)
+        lo, hi, th, fl = eng.step_injected(H, U)
+        Xg = eng.get_state()
+    A_used = np.asfortranarray(split_used(p.a_in))
+    D_used = np.asfortranarray(split_used(H))
+    st, Xr, lor, hir, thr, flr, _ = orc.step_injected(A_used, p.b_in, None, 1e-11, X, D_used, U)
+    assert st == 0
+    assert np.array_equal(fl & mh.FLAG_DEGENERATE, flr & mh.FLAG_DEGENERATE)
+    w = hir - lor
+    assert np.all(np.abs(lo - lor) <= RTOL32 * w)
+    assert np.all(np.abs(hi - hir) <= RTOL32 * w)
+    # the margin only ever shrinks the chord
+    assert np.all(hi <= hir + 1e-12 * w) and np.all(lo >= lor - 1e-12 * w)
+    assert np.abs(Xg - Xr).max() <= RTOL32 * np.abs(Xr).max()
+
+
+def test_fp32_walks_stay_exactly_feasible():
+    p = workloads.random_polytope(64, 4000, seed=3)
+    with mh.Engine(p, 256, seed=4, precision=32, refresh_every=64) as eng:
+        eng.set_state(np.zeros((64, 256)))
+        for _ in range(5):
+            eng.step(60)
+            bad, viol, _ = eng.check_state(1e-9)   # fresh fp64 product on A_used
+            assert bad == -1 and viol.max() <= 0.0
+        X = eng.get_state()
+    A_used = split_used(p.a_in)
+    assert (A_used @ X - p.b_in[:, None]).max() <= 1e-9
+    assert np.abs(X).max() > 0.1
+
+
+def test_fp32_run_box_moments():
+    p = mh.make_hypercube(12)
+    with mh.Engine(p, 512, seed=5, precision=32) as eng:
+        S, st = eng.run(np.zeros(12), phi=40, windows=20, burn_in=100)
+    assert S.shape == (20 * 512, 12)
+    assert (S @ p.a_in.T - p.b_in).max() <= 1e-9
+    assert np.abs(S.mean(0)).max() <= 0.03
+    assert np.abs(S.var(0) - 1 / 3).max() <= 0.03
+
+
+def test_fp32_matches_fp64_in_law():
+    # same Philox streams, fp32 vs fp64 chords: trajectories stay close over
+    # a few iterates (rate errors ~1e-6 relative, margin 1e-6)
+    p = workloads.random_polytope(40, 1500, seed=9)
+    out = {}
+    for prec in (64, 32):
+        with mh.Engine(p, 128, seed=12, precision=prec, small_path=False) as eng:
+            eng.set_state(np.zeros((40, 128)))
+            eng.step(4)
+            out[prec] = eng.get_state()
+    assert np.abs(out[32] - out[64]).max() <= 1e-3
+
+
+def test_fp32_config5_full_width_feasible():
+    w = workloads.config(5)
+    with mh.Engine(w.polytope, w.z, seed=5, precision=32) as eng:
+        eng.set_state(np.zeros((2000, w.z)))
+        eng.step(10)
+        bad, viol, _ = eng.check_state(1e-9)
+    assert bad == -1 and viol.max() <= 0.0
