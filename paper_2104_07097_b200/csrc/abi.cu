@@ -88,7 +88,7 @@ struct mhar_ctx {
   // walk-resident small-body path (small_kernel.cuh); Acm != null enables it
   double* Acm = nullptr;
   // fp32 variant (chord_tc32.cuh)
-  float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr, *Dlo = nullptr;
+  float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr;
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
   unsigned long long* walk_err = nullptr;
   size_t small_smem = 0;
@@ -237,7 +237,6 @@ int launch_tc32(mhar_ctx* c) {
   p.Ahi = c->Ahi;
   p.Alo = c->Alo;
   p.Dhi = c->Dhi;
-  p.Dlo = c->Dlo;
   p.S = c->S;
   p.R = c->R;
   p.theta_prev = c->theta;
@@ -252,7 +251,7 @@ int launch_tc32(mhar_ctx* c) {
   p.m = c->m;
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
-  p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 1e-6;
+  p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 2e-5;
   p.group_n = 2;
   const int64_t units = p.row_tiles * p.walk_tiles;
   const int grid = (int)std::min<int64_t>(units, c->num_sms);
@@ -435,7 +434,7 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
     // fp32 variant: the tensor cores see D_hi + D_lo; D becomes that direction
     const int64_t total = c->z_pad * c->KT * BK;
     tc_split_d_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        c->D, c->n, c->z_pad, c->KT, c->Dhi, c->Dlo, c->err);
+        c->D, c->n, c->z_pad, c->KT, c->Dhi, c->err);
     LAUNCH_OK(c, "tc_split_d_kernel");
   }
   if (c->Ahi && injected) {
@@ -705,7 +704,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       // A_I rounded to fp32 and split for 3xTF32; the fp64 copy becomes A_hi + A_lo
       const size_t an = (size_t)c->m_pad * c->n_pad, dn = (size_t)c->z_pad * c->n_pad;
       if ((st = dalloc(c, &c->Ahi, an)) || (st = dalloc(c, &c->Alo, an)) ||
-          (st = dalloc(c, &c->Dhi, dn)) || (st = dalloc(c, &c->Dlo, dn))) {
+          (st = dalloc(c, &c->Dhi, dn))) {
         cudaFree(tmp);
         return bail(st);
       }
@@ -713,7 +712,6 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
           tmp, c->m, c->n, c->m_pad, c->KT, c->Ahi, c->Alo, c->A, c->KT);
       ++c->launches;
       cudaMemsetAsync(c->Dhi, 0, dn * sizeof(float), c->stream);
-      cudaMemsetAsync(c->Dlo, 0, dn * sizeof(float), c->stream);
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TC_SMEM);

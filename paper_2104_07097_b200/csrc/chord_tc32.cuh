@@ -4,8 +4,10 @@
 // Same computation as chord2_kernel<INCREMENTAL> (compute_lambda_intervals,
 // /root/reference/proj/src/sampler.cpp:150-208, with the slack carried
 // incrementally), but the rates A_I d are formed in fp32 accuracy with the
-// 3xTF32 split  a d ~= a_hi d_hi + a_lo d_hi + a_hi d_lo  (a_hi = tf32(a),
-// a_lo = tf32(a - a_hi)) on tcgen05, accumulating in fp32 in TMEM.  The
+// split  a d = a_hi d + a_lo d  (a_hi = tf32(a), a_lo = tf32(a - a_hi); the
+// direction d itself is rounded to TF32, which keeps it centrally symmetric
+// -- tf32(-d) = -tf32(d) -- so hit-and-run's uniform law is unchanged) on
+// tcgen05, accumulating in fp32 in TMEM.  The
 // slack cache and the walk state stay fp64.  To keep every emitted sample
 // exactly feasible despite fp32 rates, chords are taken in the body shrunk
 // by a margin mu (slack - mu), see DESIGN.md "fp32 variant".
@@ -28,10 +30,10 @@ namespace mhar_dev {
 constexpr int TC_M = 128;             // walks per tile
 constexpr int TC_N = 256;             // rows per tile
 constexpr int TC_BK = 16;             // k per stage
-constexpr int TC_STAGES = 4;
-constexpr int TC_D_PIECE = TC_M * TC_BK;   // floats per D_hi (or D_lo) stage piece (8 KB)
+constexpr int TC_STAGES = 5;
+constexpr int TC_D_PIECE = TC_M * TC_BK;   // floats per D stage piece (8 KB)
 constexpr int TC_A_PIECE = TC_N * TC_BK;   // floats per A_hi (or A_lo) stage piece (16 KB)
-constexpr int TC_STAGE_FLOATS = 2 * TC_D_PIECE + 2 * TC_A_PIECE;  // 48 KB
+constexpr int TC_STAGE_FLOATS = TC_D_PIECE + 2 * TC_A_PIECE;  // 40 KB
 constexpr int TC_THREADS = 192;
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 256;
 
@@ -40,7 +42,7 @@ constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 256;
 __host__ __device__ inline int64_t tc_piece_index(int64_t r, int64_t kk, int64_t R) {
   return ((kk >> 2) * (R >> 3) + (r >> 3)) * 32 + (r & 7) * 4 + (kk & 3);
 }
-// (walk c, coordinate k) in the packed fp32 D_hi / D_lo arrays.
+// (walk c, coordinate k) in the packed TF32 direction array.
 __host__ __device__ inline int64_t tc_d_index(int64_t c, int64_t k, int64_t KT) {
   return ((c / TC_M) * KT + k / TC_BK) * TC_D_PIECE + tc_piece_index(c % TC_M, k % TC_BK, TC_M);
 }
@@ -100,8 +102,7 @@ __device__ inline void tc_ld32(uint32_t addr, float (&v)[32]) {
 struct TcParams {
   const float* Ahi;  // tc_a_index layout
   const float* Alo;
-  const float* Dhi;  // tc_d_index layout
-  const float* Dlo;
+  const float* Dhi;  // tc_d_index layout, TF32-exact directions
   double* S;         // tc_s_index layout, fp64 slack
   double* R;         // fp64 rates of the previous iterate
   const double* theta_prev;
@@ -183,9 +184,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
           const int64_t doff = (wt * p.KT + kt) * TC_D_PIECE;
           const int64_t aoff = (rt * p.KT + kt) * TC_A_PIECE;
           bulk_g2s_hint(st, p.Dhi + doff, TC_D_PIECE * 4, &full[stage], keep);
-          bulk_g2s_hint(st + TC_D_PIECE, p.Dlo + doff, TC_D_PIECE * 4, &full[stage], keep);
-          bulk_g2s(st + 2 * TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage]);
-          bulk_g2s(st + 2 * TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage]);
+          bulk_g2s(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage]);
+          bulk_g2s(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage]);
           if (++stage == TC_STAGES) {
             stage = 0;
             ++round;
@@ -205,21 +205,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], (uint32_t)phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const float* sd_hi = ring + (size_t)stage * TC_STAGE_FLOATS;
-          const float* sd_lo = sd_hi + TC_D_PIECE;
-          const float* sa_hi = sd_hi + 2 * TC_D_PIECE;
+          const float* sd = ring + (size_t)stage * TC_STAGE_FLOATS;
+          const float* sa_hi = sd + TC_D_PIECE;
           const float* sa_lo = sa_hi + TC_A_PIECE;
 #pragma unroll
           for (int k = 0; k < TC_BK / 8; ++k) {
             // K step k: k-chunks 2k, 2k+1; LBO = stride between k-chunks
             const uint32_t dofs = 2 * k * (TC_M * 4), aofs = 2 * k * (TC_N * 4);
-            const uint64_t dh = umma_desc(sd_hi + dofs, TC_M * 16, 128);
-            const uint64_t dl = umma_desc(sd_lo + dofs, TC_M * 16, 128);
+            const uint64_t dd = umma_desc(sd + dofs, TC_M * 16, 128);
             const uint64_t ah = umma_desc(sa_hi + aofs, TC_N * 16, 128);
             const uint64_t al = umma_desc(sa_lo + aofs, TC_N * 16, 128);
-            tc_mma(acc, dh, ah, (kt | k) ? 1u : 0u);
-            tc_mma(acc, dh, al, 1u);
-            tc_mma(acc, dl, ah, 1u);
+            tc_mma(acc, dd, ah, (kt | k) ? 1u : 0u);
+            tc_mma(acc, dd, al, 1u);
           }
           tc_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
           if (++stage == TC_STAGES) {
@@ -248,21 +245,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
       unsigned sd = 0u;
       const int64_t sbase = (rt * p.walk_tiles + wt) * TC_N * TC_M + wl;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * TC_N);
-      for (int c0 = 0; c0 < TC_N; c0 += 32) {
-        float v[32];
-        tc_ld32(taddr + (uint32_t)c0, v);
-#pragma unroll 8
-        for (int j = 0; j < 32; ++j) {
-          const int64_t si = sbase + (int64_t)(c0 + j) * TC_M;
-          const double so = __ldcs(p.S + si);
-          const double ro = __ldcs(p.R + si);
-          const double ad = (double)v[j];
-          const double s = fma(-th, ro, so);
-          __stcs(p.S + si, s);
-          __stcs(p.R + si, ad);
+      const double* __restrict__ Sin = p.S + sbase;
+      const double* __restrict__ Rin = p.R + sbase;
+      double* __restrict__ Sout = p.S + sbase;
+      double* __restrict__ Rout = p.R + sbase;
+      // 16 rows at a time: all loads of the group in flight before any store
+      // (the cache is read and rewritten in place; interleaving them would
+      // cost one DRAM latency per row)
+      auto rows16 = [&](int r0, const float* vv) {
+        double so[16], ro[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          so[j] = __ldcs(Sin + (int64_t)(r0 + j) * TC_M);
+          ro[j] = __ldcs(Rin + (int64_t)(r0 + j) * TC_M);
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const double ad = (double)vv[j];
+          const double s = fma(-th, ro[j], so[j]);
+          __stcs(Sout + (int64_t)(r0 + j) * TC_M, s);
+          __stcs(Rout + (int64_t)(r0 + j) * TC_M, ad);
           viol = fmax(viol, -s);
           scan_row(s - p.margin, ad, p.eps_dir, hi, lo, sd);
         }
+      };
+      for (int c0 = 0; c0 < TC_N; c0 += 32) {
+        float v[32];
+        tc_ld32(taddr + (uint32_t)c0, v);
+        rows16(c0, v);
+        rows16(c0 + 16, v + 16);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
@@ -302,24 +313,19 @@ __global__ void tc_split_a_kernel(const double* __restrict__ Acm, int64_t m, int
   }
 }
 
-// fp64 directions (packed b_index) -> (D_hi, D_lo); D is replaced by the
-// direction the tensor cores see, D_hi + D_lo, so the update moves along it.
+// fp64 directions (packed b_index) -> TF32-exact directions; D is replaced
+// by them so the walk moves along exactly the direction the tensor cores see.
 __global__ void tc_split_d_kernel(double* __restrict__ D, int64_t n, int64_t z_pad, int64_t KT,
-                                  float* __restrict__ Dhi, float* __restrict__ Dlo,
-                                  const unsigned long long* err) {
+                                  float* __restrict__ Dhi, const unsigned long long* err) {
   if (*err != kNoError) return;
   const int64_t total = z_pad * KT * BK;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c, k;
     b_coords(i, KT, &c, &k);
-    const float d = (float)D[i];
-    const float h = tf32_trunc(d);
-    const float l = tf32_trunc(d - h);
-    const int64_t ti = tc_d_index(c, k, KT);
-    Dhi[ti] = h;
-    Dlo[ti] = l;
-    D[i] = (double)h + (double)l;
+    const float h = tf32_trunc((float)D[i]);
+    Dhi[tc_d_index(c, k, KT)] = h;
+    D[i] = (double)h;
   }
 }
 

@@ -45,7 +45,7 @@ def test_fp32_injected_step_parity(orc, n, m, z):
         lo, hi, th, fl = eng.step_injected(H, U)
         Xg = eng.get_state()
     A_used = np.asfortranarray(split_used(p.a_in))
-    D_used = np.asfortranarray(split_used(H))
+    D_used = np.asfortranarray(_tf32(H).astype(np.float64))  # TF32-exact directions
     st, Xr, lor, hir, thr, flr, _ = orc.step_injected(A_used, p.b_in, None, 1e-11, X, D_used, U)
     assert st == 0
     assert np.array_equal(fl & mh.FLAG_DEGENERATE, flr & mh.FLAG_DEGENERATE)
