@@ -46,6 +46,17 @@ def fp64_peak():
     return best
 
 
+def tf32_dense_peak():
+    """TF32 tensor-core peak: the driver-measured dense bf16 GEMM rate
+    (MEASURED_PEAKS.json) halved -- TF32 runs at half the bf16 rate on
+    Blackwell; fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["bf16_tflops"] / 2.0
+    except (OSError, KeyError, ValueError):
+        return 1590.0 / 2.0
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -294,6 +305,33 @@ def run_engine(args, world, rank, local):
     peak = fp64_peak()
     eng.close()
 
+    # the north star's fp32 variant on the same workload (A_I rounded to fp32,
+    # rates on tcgen05 tensor cores): same timing protocol, reported beside
+    fp32 = None
+    if args.precision == 64 and not args.no_fp32:
+        e32 = mh.Engine(p, z, seed=args.seed, projector=projector, refresh_every=args.refresh,
+                        device=local, chain_offset=rank * z, precision=32)
+        e32.set_state(X0)
+        e32.step_timed(args.warmup, reproject)
+        e32.reset_stats()
+        e32.set_timing(True)
+        barrier(world)
+        ms32 = max_over_ranks(e32.step_timed(args.steps, reproject), world)
+        s32 = e32.stats()
+        bad32, viol32, _ = e32.check_state(e32.eps_feas)
+        e32.close()
+        tf32_exec = 2.0 * s32["chord_flops"] / max(s32["chord_ms"] * 1e-3, 1e-30) / 1e12
+        tf32_peak = tf32_dense_peak()
+        fp32 = {"value": z * world * args.steps / (ms32 * 1e-3), "unit": "chain-steps/s",
+                "ms_per_step": ms32 / args.steps,
+                "dtype": "A_I rounded to f32; rates f32-accurate on tcgen05 (TF32 hi/lo split); "
+                         "slack and walks f64",
+                "kernel": "chord_tc32_kernel (tcgen05.mma kind::tf32, TMEM, bulk-copy ring)",
+                "roofline": {"bound": "tensor", "achieved": tf32_exec, "peak": tf32_peak,
+                             "unit": "TFLOP/s (TF32 executed)", "frac": tf32_exec / tf32_peak,
+                             "peak_source": "MEASURED_PEAKS.json bf16 dense / 2"},
+                "all_inside_eps_feas": bool(bad32 == -1)}
+
     if rank != 0:
         return
     cpu = None
@@ -332,6 +370,15 @@ def run_engine(args, world, rank, local):
     }
     if cpu:
         line["cpu_baseline"] = cpu
+    if fp32:
+        line["fp32_variant"] = fp32
+    if args.precision == 32:
+        line["dtype"] = "f32 rates (tcgen05 TF32 split), f64 slack/state"
+        line["roofline"].update({"achieved": 2.0 * achieved, "peak": tf32_dense_peak(),
+                                 "unit": "TFLOP/s (TF32 executed)",
+                                 "frac": 2.0 * achieved / tf32_dense_peak(),
+                                 "kernel": "chord_tc32_kernel",
+                                 "peak_source": "MEASURED_PEAKS.json bf16 dense / 2"})
     print(json.dumps(line), flush=True)
 
 
@@ -351,6 +398,7 @@ def main():
     ap.add_argument("--cpu-walks", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-variant measurement")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="32: the fp32 variant (tcgen05 3xTF32 rates, fp64 state)")
     ap.add_argument("--paper", action="store_true",
