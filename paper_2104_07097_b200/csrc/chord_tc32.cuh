@@ -184,8 +184,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
           const int64_t doff = (wt * p.KT + kt) * TC_D_PIECE;
           const int64_t aoff = (rt * p.KT + kt) * TC_A_PIECE;
           bulk_g2s_hint(st, p.Dhi + doff, TC_D_PIECE * 4, &full[stage], keep);
-          bulk_g2s(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage]);
-          bulk_g2s(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage]);
+          bulk_g2s_hint(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage], keep);
+          bulk_g2s_hint(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage],
+                        keep);
           if (++stage == TC_STAGES) {
             stage = 0;
             ++round;
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
     // ---------------- epilogue: thread = walk ----------------
     const int q = warp & 3;              // TMEM lane quarter of this warp
     const int wl = q * 32 + lane;        // walk within the tile
+    const uint64_t stream_policy = policy_evict_first();  // the slack stream must not evict A
     for (int ui = 0; ui < my_units; ++ui) {
       int64_t rt, wt;
       tc_unit(blockIdx.x + (int64_t)ui * gridDim.x, p, &rt, &wt);
@@ -256,15 +258,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
         double so[16], ro[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          so[j] = __ldcs(Sin + (int64_t)(r0 + j) * TC_M);
-          ro[j] = __ldcs(Rin + (int64_t)(r0 + j) * TC_M);
+          so[j] = ld_policy(Sin + (int64_t)(r0 + j) * TC_M, stream_policy);
+          ro[j] = ld_policy(Rin + (int64_t)(r0 + j) * TC_M, stream_policy);
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const double ad = (double)vv[j];
           const double s = fma(-th, ro[j], so[j]);
-          __stcs(Sout + (int64_t)(r0 + j) * TC_M, s);
-          __stcs(Rout + (int64_t)(r0 + j) * TC_M, ad);
+          st_policy(Sout + (int64_t)(r0 + j) * TC_M, s, stream_policy);
+          st_policy(Rout + (int64_t)(r0 + j) * TC_M, ad, stream_policy);
           viol = fmax(viol, -s);
           scan_row(s - p.margin, ad, p.eps_dir, hi, lo, sd);
         }
