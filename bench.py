@@ -239,6 +239,33 @@ def run_paper(args):
     return out
 
 
+def run_sweep(args):
+    """Padding sweep (the reference's sweep_padding, proj/src/bench.cpp:49-61,
+    and the paper's z* experiment): chain-steps/s against
+    the walk count z on one B200, phi and the body fixed.  The paper
+    conjectured that large z causes memory contention on its P100."""
+    import paper_2104_07097_b200 as mh
+    from paper_2104_07097_b200 import workloads
+    w = workloads.config(args.config)
+    p = w.polytope
+    proj = mh.compute_projection(p.a_eq) if p.num_equalities() else None
+    out = []
+    for z in [int(v) for v in args.sweep_z.split(",")]:
+        for prec in ([64, 32] if args.config >= 3 else [64]):
+            with mh.Engine(p, z, seed=args.seed, projector=proj, precision=prec) as eng:
+                X = np.empty((p.dim(), z), order="F")
+                X[:] = w.x0[:, None]
+                eng.set_state(X)
+                eng.step_timed(3, 0)
+                ms = eng.step_timed(args.steps, 0)
+            rec = {"sweep": "padding", "config": args.config, "precision": prec, "z": z,
+                   "chain_steps_per_s": z * args.steps / (ms * 1e-3),
+                   "ms_per_iterate": ms / args.steps}
+            out.append(rec)
+            print(json.dumps(rec), flush=True)
+    return out
+
+
 def run_engine(args, world, rank, local):
     import paper_2104_07097_b200 as mh
     from paper_2104_07097_b200 import workloads
@@ -399,6 +426,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=2)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-variant measurement")
+    ap.add_argument("--sweep-z", default="",
+                    help="comma-separated walk counts: padding sweep instead of the bench line")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="32: the fp32 variant (tcgen05 3xTF32 rates, fp64 state)")
     ap.add_argument("--paper", action="store_true",
@@ -408,6 +437,8 @@ def main():
     world, rank, local = dist_setup(args)
     if args.paper:
         run_paper(args)
+    elif args.sweep_z:
+        run_sweep(args)
     elif args.impl == "reference":
         run_reference(args, world, rank)
     else:

@@ -28,7 +28,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(HERE, "lib", "libmhar_b200.so")
+# MHAR_LIB selects an alternative in-tree build (tuning experiments only).
+_LIB_PATH = os.environ.get("MHAR_LIB") or os.path.join(HERE, "lib", "libmhar_b200.so")
 
 # Constants mirrored from the reference headers.
 kDegenerateWidth = 1e-14      # sampler.hpp:40
