@@ -209,6 +209,28 @@ int mhar_reset_stats(mhar_ctx* ctx);
  * with equalities) and of its dominant chord launch. */
 double mhar_flops_per_iterate(mhar_ctx* ctx);
 
+/* ---- two-sample uniformity test ----------------------
+ * minimum_spanning_tree (stats.hpp:31, stats.cpp:50-91): Prim over N points
+ * (row-major N x n) on GPU `device`; N - 1 edges in insertion order. */
+int mhar_minimum_spanning_tree(const double* points, int64_t N, int64_t n, int device,
+                               int32_t* edge_a, int32_t* edge_b, double* edge_w);
+
+/* MstTestResult (stats.hpp:34-41). */
+typedef struct {
+  int64_t cross_edges;
+  double expected_cross;
+  double variance_cross;
+  double z_value;
+  int64_t shared_end_pairs;
+  int64_t pooled_size;
+} mhar_fr_result;
+
+/* friedman_rafsky (stats.hpp:50, stats.cpp:93-143): a (na x n) and b (nb x n)
+ * row-major; DEGENERATE_TEST when a sample has < 2 points or the null
+ * variance is not positive. */
+int mhar_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t nb, int64_t n,
+                         int device, mhar_fr_result* out);
+
 const char* mhar_last_error(void);
 const char* mhar_version(void);
 int mhar_device_count(int* count);

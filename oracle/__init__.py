@@ -33,6 +33,12 @@ class RunConfig(C.Structure):
                 ("eps_feas", C.c_double)]
 
 
+class FrResult(C.Structure):
+    _fields_ = [("cross_edges", _i64), ("expected_cross", C.c_double),
+                ("variance_cross", C.c_double), ("z_value", C.c_double),
+                ("shared_end_pairs", _i64), ("pooled_size", _i64)]
+
+
 class RunStats(C.Structure):
     _fields_ = [("windows", _i64), ("iterate_count", _i64), ("redraw_count", _i64),
                 ("err_chain", _i64), ("seconds", C.c_double)]
@@ -95,6 +101,11 @@ def lib():
         L.orc_run.restype = C.c_int
         L.orc_run.argtypes = [_dp, _dp, _i64, _dp, _dp, _i64, _i64, C.POINTER(RunConfig), _dp,
                               _dp, C.POINTER(RunStats)]
+        _i32p = C.POINTER(C.c_int32)
+        L.orc_minimum_spanning_tree.restype = C.c_int
+        L.orc_minimum_spanning_tree.argtypes = [_dp, _i64, _i64, _i32p, _i32p, _dp]
+        L.orc_friedman_rafsky.restype = C.c_int
+        L.orc_friedman_rafsky.argtypes = [_dp, _i64, _dp, _i64, _i64, C.POINTER(FrResult)]
         _lib = L
     return _lib
 
@@ -293,3 +304,30 @@ def run(A, b, x0, *, z, phi, t_target, burn_in, reproject_every, seed, eps_dir=1
     st = lib().orc_run(_d(A), _d(b), A.shape[0], _d(AEf), _d(bEf), me, n, C.byref(cfg), _d(x0),
                        _d(samples), C.byref(stats))
     return st, samples, stats
+
+
+# ------------------------------------------------ two-sample tree test ----
+
+def minimum_spanning_tree(points):
+    """stats.cpp:50-91 (row points)."""
+    P = np.ascontiguousarray(points, dtype=np.float64)
+    if P.ndim == 1:
+        P = P[:, None]
+    N, n = P.shape
+    a = np.empty(N - 1, np.int32)
+    b = np.empty(N - 1, np.int32)
+    w = np.empty(N - 1)
+    lib().orc_minimum_spanning_tree(_d(P), N, n, a.ctypes.data_as(C.POINTER(C.c_int32)),
+                                    b.ctypes.data_as(C.POINTER(C.c_int32)), _d(w))
+    return a, b, w
+
+
+def friedman_rafsky(sample_a, sample_b):
+    """stats.cpp:93-143.  Returns (status, FrResult)."""
+    A = np.ascontiguousarray(sample_a, dtype=np.float64)
+    B = np.ascontiguousarray(sample_b, dtype=np.float64)
+    if A.ndim == 1:
+        A, B = A[:, None], B[:, None]
+    r = FrResult()
+    st = lib().orc_friedman_rafsky(_d(A), A.shape[0], _d(B), B.shape[0], A.shape[1], C.byref(r))
+    return st, r

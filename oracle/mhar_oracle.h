@@ -106,6 +106,21 @@ int orc_run(const double* A, const double* b, int64_t m, const double* AE, const
             int64_t me, int64_t n, const orc_run_config* cfg, const double* x0,
             double* samples, orc_run_stats* stats);
 
+/* ---- two-sample tree test: proj/src/stats.cpp:50-143 ----------------------
+ * Prim MST of N points (row-major N x n), vertices entering in index order,
+ * strict-< updates (ties keep the earlier candidate).  Edges in insertion
+ * order: (ea[i], eb[i]) with weight ew[i]. */
+int orc_minimum_spanning_tree(const double* pts, int64_t N, int64_t n, int32_t* ea, int32_t* eb,
+                              double* ew);
+typedef struct {
+  int64_t cross_edges;
+  double expected_cross, variance_cross, z_value;
+  int64_t shared_end_pairs, pooled_size;
+} orc_fr_result;
+/* a: na x n, b: nb x n, row-major; DEGENERATE_TEST (11) / DIMENSION_MISMATCH */
+int orc_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t nb, int64_t n,
+                        orc_fr_result* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -129,7 +129,14 @@ EXPORTED_SYMBOLS = [
     "mhar_step_injected", "mhar_lambda_intervals", "mhar_check_state", "mhar_run",
     "mhar_compute_projection", "mhar_get_stats", "mhar_set_timing", "mhar_reset_stats",
     "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
+    "mhar_minimum_spanning_tree", "mhar_friedman_rafsky",
 ]
+
+
+class _FrResult(C.Structure):
+    _fields_ = [("cross_edges", C.c_int64), ("expected_cross", C.c_double),
+                ("variance_cross", C.c_double), ("z_value", C.c_double),
+                ("shared_end_pairs", C.c_int64), ("pooled_size", C.c_int64)]
 
 _lib = None
 
@@ -171,6 +178,12 @@ def lib():
     L.mhar_last_error.restype = C.c_char_p
     L.mhar_version.restype = C.c_char_p
     L.mhar_device_count.argtypes = [C.POINTER(C.c_int)]
+    _i32p = C.POINTER(C.c_int32)
+    L.mhar_minimum_spanning_tree.argtypes = [_dp, C.c_int64, C.c_int64, C.c_int, _i32p, _i32p, _dp]
+    L.mhar_minimum_spanning_tree.restype = C.c_int
+    L.mhar_friedman_rafsky.argtypes = [_dp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int,
+                                       C.POINTER(_FrResult)]
+    L.mhar_friedman_rafsky.restype = C.c_int
     for name in ("mhar_ctx_create", "mhar_ctx_destroy", "mhar_set_state", "mhar_get_state",
                  "mhar_get_state_rows_device", "mhar_step", "mhar_sync", "mhar_step_timed",
                  "mhar_step_injected",

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -23,6 +24,7 @@
 #include "step_kernels.cuh"
 #include "small_kernel.cuh"
 #include "chord_tc32.cuh"
+#include "stats_kernels.cuh"
 
 using namespace mhar_dev;
 
@@ -1098,6 +1100,94 @@ int mhar_reset_stats(mhar_ctx* c) {
   c->chord_timed = 0;
   c->chord_flops = 0.0;
   c->refreshes = 0;
+  return 0;
+}
+
+int mhar_minimum_spanning_tree(const double* points, int64_t N, int64_t n, int device,
+                               int32_t* edge_a, int32_t* edge_b, double* edge_w) {
+  if (!points || N < 2 || n < 1 || !edge_a || !edge_b || !edge_w)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "minimum_spanning_tree: need at least two points");
+  CK(cudaSetDevice(device));
+  // coordinate-major copy for coalesced distance sweeps
+  std::vector<double> pt((size_t)N * n);
+  for (int64_t v = 0; v < N; ++v)
+    for (int64_t k = 0; k < n; ++k) pt[(size_t)k * N + v] = points[(size_t)v * n + k];
+  double *dP = nullptr, *dbest = nullptr, *dew = nullptr;
+  int *dpar = nullptr, *dea = nullptr, *deb = nullptr;
+  unsigned char* dint = nullptr;
+  cudaStream_t s;
+  CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  auto cleanup = [&]() {
+    cudaFree(dP);
+    cudaFree(dbest);
+    cudaFree(dew);
+    cudaFree(dpar);
+    cudaFree(dea);
+    cudaFree(deb);
+    cudaFree(dint);
+    cudaStreamDestroy(s);
+  };
+  if (cudaMalloc(&dP, sizeof(double) * pt.size()) != cudaSuccess ||
+      cudaMalloc(&dbest, sizeof(double) * N) != cudaSuccess ||
+      cudaMalloc(&dew, sizeof(double) * N) != cudaSuccess ||
+      cudaMalloc(&dpar, sizeof(int) * N) != cudaSuccess ||
+      cudaMalloc(&dea, sizeof(int) * N) != cudaSuccess ||
+      cudaMalloc(&deb, sizeof(int) * N) != cudaSuccess || cudaMalloc(&dint, N) != cudaSuccess) {
+    cleanup();
+    return fail(MHAR_ERR_CUDA, "minimum_spanning_tree: cudaMalloc failed");
+  }
+  cudaMemcpyAsync(dP, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice, s);
+  prim_kernel<<<1, PRIM_THREADS, 0, s>>>(dP, N, n, dbest, dpar, dint, dea, deb, dew);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    cudaMemcpyAsync(edge_a, dea, sizeof(int) * (N - 1), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(edge_b, deb, sizeof(int) * (N - 1), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(edge_w, dew, sizeof(double) * (N - 1), cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+  }
+  cleanup();
+  if (e != cudaSuccess) return fail(MHAR_ERR_CUDA, std::string("prim_kernel: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int mhar_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t nb, int64_t n,
+                         int device, mhar_fr_result* out) {
+  if (!out) return fail(MHAR_ERR_INVALID_ARGUMENT, "friedman_rafsky: null result");
+  if (!a || !b || na < 2 || nb < 2)
+    return fail(MHAR_ERR_DEGENERATE_TEST,
+                "DEGENERATE_TEST: friedman_rafsky: each sample needs at least two points");
+  if (n < 1) return fail(MHAR_ERR_DIMENSION_MISMATCH, "friedman_rafsky: samples have no width");
+  const int64_t N = na + nb;
+  std::vector<double> pooled((size_t)N * n);
+  std::memcpy(pooled.data(), a, sizeof(double) * na * n);
+  std::memcpy(pooled.data() + na * n, b, sizeof(double) * nb * n);
+  std::vector<int32_t> ea(N), eb(N);
+  std::vector<double> ew(N);
+  int st = mhar_minimum_spanning_tree(pooled.data(), N, n, device, ea.data(), eb.data(), ew.data());
+  if (st) return st;
+  // stats.cpp:115-142
+  std::memset(out, 0, sizeof(*out));
+  out->pooled_size = N;
+  std::vector<int64_t> degree(N, 0);
+  for (int64_t i = 0; i < N - 1; ++i) {
+    ++degree[ea[i]];
+    ++degree[eb[i]];
+    if ((ea[i] < na) != (eb[i] < na)) ++out->cross_edges;
+  }
+  int64_t shared = 0;
+  for (int64_t d : degree) shared += d * (d - 1) / 2;
+  out->shared_end_pairs = shared;
+  const double m = (double)na, np = (double)nb, bn = (double)N, two_mn = 2.0 * m * np;
+  out->expected_cross = two_mn / bn + 1.0;
+  const double cc = (double)shared;
+  const double lead = two_mn / (bn * (bn - 1.0));
+  out->variance_cross = lead * ((two_mn - bn) / bn + (cc - bn + 2.0) / ((bn - 2.0) * (bn - 3.0)) *
+                                                         (bn * (bn - 1.0) - 2.0 * two_mn + 2.0));
+  if (!(out->variance_cross > 0.0))
+    return fail(MHAR_ERR_DEGENERATE_TEST, "DEGENERATE_TEST: friedman_rafsky: null variance " +
+                                              std::to_string(out->variance_cross) +
+                                              " is not positive");
+  out->z_value = ((double)out->cross_edges - out->expected_cross) / std::sqrt(out->variance_cross);
   return 0;
 }
 
