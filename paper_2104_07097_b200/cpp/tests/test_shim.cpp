@@ -3,13 +3,20 @@
 // against the B200 engine.  The z = 1 equivalence compares with the CPU
 // oracle (oracle/mhar_oracle.h, test infrastructure) on the same streams.
 // Run by tests/test_cpp_shim.py on a GPU box.
+#include <unistd.h>
+
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <sstream>
 #include <functional>
 #include <string>
 #include <vector>
 
 #include "../../../oracle/mhar_oracle.h"
+#include "mhar/io.hpp"
 #include "mhar/sampler.hpp"
 
 using mhar::Matrix;
@@ -210,6 +217,55 @@ int main() {
       }
       CHECK(worst <= 1e-12);
     }
+  });
+
+  run_case("format_double is the shortest round trip (io.hpp:13)", [] {
+    CHECK(mhar::format_double(0.1) == "0.1");
+    CHECK(mhar::format_double(2.0) == "2");
+    CHECK(mhar::format_double(-1.5e-9) == "-1.5e-09");
+    CHECK(mhar::format_double(1.0 / 3.0) == "0.3333333333333333");
+    uint64_t s = 12345;
+    for (int i = 0; i < 2000; ++i) {
+      s = s * 6364136223846793005ULL + 1442695040888963407ULL;
+      double v;
+      uint64_t bits = (s >> 2) | 0x3000000000000000ULL;  // finite, varied exponents
+      std::memcpy(&v, &bits, 8);
+      if (i & 1) v = -v;
+      const std::string t = mhar::format_double(v);
+      CHECK(std::strtod(t.c_str(), nullptr) == v);
+    }
+  });
+
+  run_case("sample files round-trip and runs are byte-reproducible (acceptance #9)", [] {
+    const auto cube = mhar::make_hypercube(3);
+    mhar::SamplerConfig cfg;
+    cfg.z = 16;
+    cfg.phi = 20;
+    cfg.t_target = 64;
+    cfg.seed = 42;
+    const auto a = mhar::run(cube, cfg, Vector::Zero(3));
+    const auto b = mhar::run(cube, cfg, Vector::Zero(3));
+    const std::string dir = "/tmp/mhar_shim_io_" + std::to_string(::getpid());
+    if (std::system(("mkdir -p " + dir).c_str()) != 0) CHECK(false);
+    mhar::write_sample_csv(dir + "/a.csv", a.samples);
+    mhar::write_sample_csv(dir + "/b.csv", b.samples);
+    auto slurp = [](const std::string& p) {
+      std::ifstream in(p, std::ios::binary);
+      std::ostringstream ss;
+      ss << in.rdbuf();
+      return ss.str();
+    };
+    CHECK(slurp(dir + "/a.csv") == slurp(dir + "/b.csv"));
+    CHECK(slurp(dir + "/a.csv").rfind("x1,x2,x3\n", 0) == 0);
+    CHECK(mhar::read_sample_csv(dir + "/a.csv") == a.samples);
+    mhar::write_sample_bin(dir + "/a.bin", a.samples);
+    CHECK(mhar::read_sample_bin(dir + "/a.bin") == a.samples);
+    const std::string man = mhar::manifest_string(a, "hypercube:3", dir + "/a.csv");
+    CHECK(man.find("\"samples_written\": 64") != std::string::npos);
+    CHECK(man.find("\"windows\": 4") != std::string::npos);
+    CHECK(man.find("\"iterate_count\": 1280") != std::string::npos);
+    CHECK(man.find("\"eps_dir\": 1e-11") != std::string::npos);
+    if (std::system(("rm -rf " + dir).c_str()) != 0) CHECK(false);
   });
 
   std::printf("%d passed, %d failed checks\n", g_pass, g_fail);

@@ -92,6 +92,11 @@ struct mhar_ctx {
   // fp32 variant (chord_tc32.cuh)
   float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr;
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
+  // run(): overlapped collection (second rows buffer, pinned staging, side stream)
+  double* rows2 = nullptr;
+  double* pinned[2] = {nullptr, nullptr};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   unsigned long long* walk_err = nullptr;
   size_t small_smem = 0;
   int small_ns = 1, small_grid = 0;
@@ -806,6 +811,13 @@ int mhar_ctx_destroy(mhar_ctx* c) {
     cudaEventDestroy(ev.first);
     cudaEventDestroy(ev.second);
   }
+  if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+  for (int b = 0; b < 2; ++b) {
+    if (c->pinned[b]) cudaFreeHost(c->pinned[b]);
+    if (c->ev_ready[b]) cudaEventDestroy(c->ev_ready[b]);
+    if (c->ev_copied[b]) cudaEventDestroy(c->ev_copied[b]);
+  }
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (void* q : c->allocs) cudaFree(q);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1021,27 +1033,57 @@ int mhar_run(mhar_ctx* c, const mhar_run_config* cfg, const double* x0, double* 
   c->iterations = 0;
   if ((s = reset_streams(c))) return s;
 
+  // Collection streams out while the next window computes: rows of window w
+  // go to a device buffer (double-buffered), a side stream copies them into
+  // pinned staging, and the host moves window w-2 into `samples` while the
+  // device works on window w.
+  const size_t win = (size_t)c->z * c->n;
+  if (samples && !c->copy_stream) {
+    if ((s = dalloc(c, &c->rows2, win))) return s;
+    CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaHostAlloc(&c->pinned[b], win * sizeof(double), cudaHostAllocDefault));
+      CK(cudaEventCreateWithFlags(&c->ev_ready[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+    }
+  }
+  double* drows[2] = {c->rows, c->rows2};
+  auto drain = [&](int64_t w) {  // window w's rows -> samples (host)
+    const int b = (int)(w & 1);
+    cudaEventSynchronize(c->ev_copied[b]);
+    std::memcpy(samples + (size_t)w * win, c->pinned[b], win * sizeof(double));
+  };
+
   cudaEvent_t t0, t1;
   cudaEventCreate(&t0);
   cudaEventCreate(&t1);
   cudaEventRecord(t0, c->stream);
-  int big = 0x7FFFFFFF;
   if ((s = advance(c, cfg->burn_in, cfg->reproject_every))) return s;
   int64_t walk = -1;
   for (int64_t w = 0; w < cfg->windows; ++w) {
     if ((s = advance(c, cfg->phi, cfg->reproject_every))) return s;
     if ((s = enqueue_check(c))) return s;
-    CK(cudaMemcpyAsync(c->first_bad, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemsetAsync(c->first_bad, 0x7F, sizeof(int), c->stream));
     contains_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(
         c->viol, c->me > 0 ? c->eqviol : nullptr, c->z, c->opt.eps_feas, c->err, 1, c->first_bad);
     LAUNCH_OK(c, "contains_kernel");
     if (samples) {
+      const int b = (int)(w & 1);
+      if (w >= 2) CK(cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
       unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-          c->X, c->n, c->z, c->KT, c->rows);
+          c->X, c->n, c->z, c->KT, drows[b]);
       LAUNCH_OK(c, "unpack_b_kernel");
-      CK(cudaMemcpyAsync(samples + (size_t)w * c->z * c->n, c->rows,
-                         sizeof(double) * c->z * c->n, cudaMemcpyDeviceToHost, c->stream));
+      CK(cudaEventRecord(c->ev_ready[b], c->stream));
+      if (w >= 2) drain(w - 2);  // overlaps the device work just queued
+      CK(cudaStreamWaitEvent(c->copy_stream, c->ev_ready[b], 0));
+      CK(cudaMemcpyAsync(c->pinned[b], drows[b], win * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->copy_stream));
+      CK(cudaEventRecord(c->ev_copied[b], c->copy_stream));
     }
+  }
+  if (samples) {
+    for (int64_t w = std::max<int64_t>(0, cfg->windows - 2); w < cfg->windows; ++w) drain(w);
+    CK(cudaStreamWaitEvent(c->stream, c->ev_copied[(cfg->windows - 1) & 1], 0));
   }
   cudaEventRecord(t1, c->stream);
   s = read_error(c, &walk);
