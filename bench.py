@@ -110,14 +110,21 @@ class ClockSampler:
 
 
 def dist_setup(args):
+    """One process per GPU, NCCL.  MHAR_SHARE_GPU=1 (functional testing of
+    the multi-rank path on a one-GPU box only) maps every rank to device 0
+    and runs the collectives on gloo; such timings are not bench numbers."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        if os.environ.get("MHAR_SHARE_GPU") == "1":
+            local = 0
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
     return world, rank, local
 
 
@@ -127,12 +134,20 @@ def barrier(world):
         dist.barrier()
 
 
+def coll_device():
+    """Device for collective tensors: CUDA under NCCL, CPU under gloo."""
+    import torch.distributed as dist
+    if dist.is_initialized() and dist.get_backend() == "gloo":
+        return "cpu"
+    return "cuda"
+
+
 def max_over_ranks(v: float, world: int) -> float:
     if world == 1:
         return v
     import torch
     import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    t = torch.tensor([v], dtype=torch.float64, device=coll_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -322,6 +337,8 @@ def run_engine(args, world, rank, local):
     bad, viol, eqv = eng.check_state(eng.eps_feas)
     rows = torch.empty((z, p.dim()), dtype=torch.float64, device=f"cuda:{local}")
     eng.state_rows_to_device(rows.data_ptr())
+    if coll_device() == "cpu":
+        rows = rows.cpu()
     diag = reduce_diagnostics(st["redraw_count"], float(viol.max()), float(eqv.max()), rows,
                               device=rows.device)
     gathered = gather_rows(rows, [z] * world)
