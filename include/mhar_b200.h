@@ -147,6 +147,18 @@ int mhar_step_timed(mhar_ctx* ctx, int64_t iters, int64_t reproject_every, doubl
 int mhar_step_injected(mhar_ctx* ctx, const double* h, const double* u, double* lower,
                        double* upper, double* theta, uint8_t* flags);
 
+/* generate_directions (sampler.hpp:46, sampler.cpp:143-148): the next n x z
+ * batch of standard normals from the walks' streams (column k from walk k's
+ * stream, 2*ceil(n/2) draws), advancing them; column-major into h. */
+int mhar_generate_directions(mhar_ctx* ctx, double* h);
+
+/* select_points (sampler.hpp:66-67, sampler.cpp:214-233): for every walk
+ * theta from the theta stream, uniform on the open chord (lower, upper),
+ * out = x + theta d (n x z column-major).  DIRECTION_DEGENERATE if any walk
+ * is flagged in `degenerate` (nonzero), before any draw. */
+int mhar_select_points(mhar_ctx* ctx, const double* x, const double* d, const double* lower,
+                       const double* upper, const uint8_t* degenerate, double* out);
+
 /* compute_lambda_intervals for host X and D (n x z each) against the
  * context's polytope; does not move the state.  degenerate gets
  * MHAR_FLAG_* bits.  UNBOUNDED_POLYTOPE names the first one-sided walk. */

@@ -129,7 +129,8 @@ EXPORTED_SYMBOLS = [
     "mhar_step_injected", "mhar_lambda_intervals", "mhar_check_state", "mhar_run",
     "mhar_compute_projection", "mhar_get_stats", "mhar_set_timing", "mhar_reset_stats",
     "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
-    "mhar_minimum_spanning_tree", "mhar_friedman_rafsky",
+    "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
+    "mhar_select_points",
 ]
 
 
@@ -184,6 +185,10 @@ def lib():
     L.mhar_friedman_rafsky.argtypes = [_dp, C.c_int64, _dp, C.c_int64, C.c_int64, C.c_int,
                                        C.POINTER(_FrResult)]
     L.mhar_friedman_rafsky.restype = C.c_int
+    L.mhar_generate_directions.argtypes = [C.c_void_p, _dp]
+    L.mhar_generate_directions.restype = C.c_int
+    L.mhar_select_points.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _u8p, _dp]
+    L.mhar_select_points.restype = C.c_int
     for name in ("mhar_ctx_create", "mhar_ctx_destroy", "mhar_set_state", "mhar_get_state",
                  "mhar_get_state_rows_device", "mhar_step", "mhar_sync", "mhar_step_timed",
                  "mhar_step_injected",
@@ -456,6 +461,25 @@ class Engine:
         _check(lib().mhar_step_injected(self._h, _d(H), _d(U), _d(lo), _d(hi), _d(th),
                                         fl.ctypes.data_as(_u8p)))
         return lo, hi, th, fl
+
+    def generate_directions(self) -> np.ndarray:
+        """generate_directions (sampler.cpp:143-148): the next n x z batch of
+        standard normals from the walks' streams (advances them)."""
+        h = np.empty((self.n, self.z), order="F")
+        _check(lib().mhar_generate_directions(self._h, _d(h)))
+        return h
+
+    def select_points(self, X, D, intervals: "LambdaIntervals") -> np.ndarray:
+        """select_points (sampler.cpp:214-233): x + theta d, theta uniform on
+        each open chord from the theta stream; DIRECTION_DEGENERATE on flags."""
+        X, D = _f(X), _f(D)
+        lo = np.ascontiguousarray(intervals.lower, dtype=np.float64)
+        hi = np.ascontiguousarray(intervals.upper, dtype=np.float64)
+        dg = np.ascontiguousarray(intervals.degenerate, dtype=np.uint8)
+        out = np.empty((self.n, self.z), order="F")
+        _check(lib().mhar_select_points(self._h, _d(X), _d(D), _d(lo), _d(hi),
+                                        dg.ctypes.data_as(_u8p), _d(out)))
+        return out
 
     def lambda_intervals(self, X, D) -> LambdaIntervals:
         X, D = _f(X), _f(D)

@@ -186,11 +186,22 @@ class WalkRng {
  private:
   friend void step(const Polytope&, const ProjectionOperator*, const SamplerConfig&, WalkRng&,
                    struct WalkState&);
+  friend Matrix generate_directions(WalkRng&, int);
+  friend Matrix select_points(WalkRng&, const Matrix&, const Matrix&, const LambdaIntervals&);
+  Engine& engine_for_streams(int n);  // an engine whose streams these are
   uint64_t seed_;
   int z_;
   std::unique_ptr<Engine> engine_;
   const Polytope* bound_ = nullptr;
 };
+
+/// One standard normal direction per walk column, n x z (sampler.hpp:46).
+Matrix generate_directions(WalkRng& rng, int n);
+
+/// Moves every walk to x + theta d, theta uniform on its open chord via the
+/// theta stream; DIRECTION_DEGENERATE if any walk is flagged (sampler.hpp:66-67).
+Matrix select_points(WalkRng& rng, const Matrix& x, const Matrix& d,
+                     const LambdaIntervals& intervals);
 
 struct WalkState {
   Matrix x;

@@ -168,6 +168,48 @@ WalkRng::WalkRng(uint64_t seed, int z) : seed_(seed), z_(z) {
 }
 WalkRng::~WalkRng() = default;
 
+// The streams live in a device context; without a polytope bound yet, a
+// unit box of the requested dimension carries them (streams do not depend on
+// the body).
+Engine& WalkRng::engine_for_streams(int n) {
+  if (!engine_) {
+    static thread_local std::vector<std::unique_ptr<Polytope>> boxes;
+    boxes.push_back(std::make_unique<Polytope>(make_hypercube(n)));
+    engine_ = std::make_unique<Engine>(*boxes.back(), nullptr, z_, seed_, 1e-11, 1e-9,
+                                       MHAR_RNG_REFERENCE);
+    bound_ = boxes.back().get();
+  }
+  return *engine_;
+}
+
+Matrix generate_directions(WalkRng& rng, int n) {
+  if (n < 1) raise(ErrorCode::invalid_argument, "generate_directions: n must be >= 1");
+  Engine& e = rng.engine_for_streams(n);
+  if (rng.bound_->dim() != n)
+    raise(ErrorCode::dimension_mismatch, "generate_directions: streams are bound to dimension " +
+                                             std::to_string(rng.bound_->dim()));
+  Matrix h(n, rng.width());
+  check(mhar_generate_directions(e.ctx(), h.data()));
+  return h;
+}
+
+Matrix select_points(WalkRng& rng, const Matrix& x, const Matrix& d,
+                     const LambdaIntervals& intervals) {
+  const Index z = x.cols();
+  if (d.cols() != z || intervals.lower.size() != z || intervals.upper.size() != z ||
+      static_cast<Index>(intervals.degenerate.size()) != z || z != rng.width())
+    raise(ErrorCode::dimension_mismatch, "select_points: inputs disagree on walk count");
+  for (Index k = 0; k < z; ++k)
+    if (intervals.degenerate[static_cast<size_t>(k)])
+      raise(ErrorCode::direction_degenerate,
+            "select_points: walk " + std::to_string(k) + " has no usable chord");
+  Engine& e = rng.engine_for_streams(static_cast<int>(x.rows()));
+  Matrix out(x.rows(), z);
+  check(mhar_select_points(e.ctx(), x.data(), d.data(), intervals.lower.data(),
+                           intervals.upper.data(), intervals.degenerate.data(), out.data()));
+  return out;
+}
+
 void step(const Polytope& p, const ProjectionOperator* projector, const SamplerConfig& cfg,
           WalkRng& rng, WalkState& state) {
   if (state.x.cols() != rng.width() || state.x.rows() != p.dim())

@@ -932,6 +932,69 @@ int mhar_step_injected(mhar_ctx* c, const double* h, const double* u, double* lo
   return s;
 }
 
+int mhar_generate_directions(mhar_ctx* c, double* h) {
+  if (!c || !h) return fail(MHAR_ERR_INVALID_ARGUMENT, "generate_directions: null argument");
+  CK(cudaSetDevice(c->device));
+  int s = read_error(c, nullptr);
+  if (s) return s;
+  if ((s = launch_normals(c, c->D))) return s;
+  if (c->opt.rng == MHAR_RNG_REFERENCE) {
+    advance_streams_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(
+        c->col_state, c->z, 2 * ((c->n + 1) / 2));
+    LAUNCH_OK(c, "advance_streams_kernel");
+  }
+  ++c->iterations;       // Philox: the next batch is keyed on the next counter
+  c->slack_valid = false;  // D was overwritten
+  unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->D, c->n, c->z, c->KT, c->rows);
+  LAUNCH_OK(c, "unpack_b_kernel");
+  CK(cudaMemcpyAsync(h, c->rows, sizeof(double) * c->n * c->z, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int mhar_select_points(mhar_ctx* c, const double* x, const double* d, const double* lower,
+                       const double* upper, const uint8_t* degenerate, double* out) {
+  if (!c || !x || !d || !lower || !upper || !degenerate || !out)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "select_points: null argument");
+  for (int64_t k = 0; k < c->z; ++k)
+    if (degenerate[k])
+      return fail(MHAR_ERR_DIRECTION_DEGENERATE, "DIRECTION_DEGENERATE: select_points: walk " +
+                                                     std::to_string(k + c->opt.chain_offset) +
+                                                     " has no usable chord");
+  CK(cudaSetDevice(c->device));
+  int s = read_error(c, nullptr);
+  if (s) return s;
+  if (!c->Xtmp) {
+    if ((s = dalloc(c, &c->Xtmp, (size_t)c->z_pad * c->n_pad))) return s;
+  }
+  if ((s = upload_state_host(c, x, c->Xtmp))) return s;
+  if ((s = upload_state_host(c, d, c->D))) return s;
+  c->slack_valid = false;
+  CK(cudaMemcpyAsync(c->lower, lower, sizeof(double) * c->z, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemcpyAsync(c->upper, upper, sizeof(double) * c->z, cudaMemcpyHostToDevice, c->stream));
+  CK(cudaMemsetAsync(c->flags, 0, sizeof(unsigned) * c->z_pad, c->stream));
+  CK(cudaMemsetAsync(c->theta, 0, sizeof(double) * c->z_pad, c->stream));
+  ThetaParams tp = theta_params(c, nullptr);
+  theta_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(tp);
+  LAUNCH_OK(c, "theta_kernel");
+  if (c->opt.rng == MHAR_RNG_REFERENCE) {
+    theta_fixup_kernel<<<1, 1, 0, c->stream>>>(tp);
+    LAUNCH_OK(c, "theta_fixup_kernel");
+  }
+  const int64_t total2 = c->z_pad * c->KT * BK / 2;
+  axpy_kernel<<<blocks_for(total2, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->Xtmp, c->D, c->theta, total2, c->KT, c->err);
+  LAUNCH_OK(c, "axpy_kernel");
+  ++c->iterations;
+  unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->Xtmp, c->n, c->z, c->KT, c->rows);
+  LAUNCH_OK(c, "unpack_b_kernel");
+  CK(cudaMemcpyAsync(out, c->rows, sizeof(double) * c->n * c->z, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return read_error(c, nullptr);
+}
+
 int mhar_lambda_intervals(mhar_ctx* c, const double* x, const double* d, double* lower,
                           double* upper, uint8_t* flags) {
   if (!c || !x || !d) return fail(MHAR_ERR_INVALID_ARGUMENT, "lambda_intervals: null argument");

@@ -158,7 +158,7 @@ __device__ __forceinline__ void reduce_and_publish(double (&hi)[NCH][2], double 
 template <int MODE>
 __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordParams p) {
   if (*p.err != kNoError) return;  // sticky device error: stop all work
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)CHORD_STAGES * STAGE_DOUBLES * 8);
   uint64_t* empty = full + CHORD_STAGES;
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
 template <int MODE>
 __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordParams p) {
   if (*p.err != kNoError) return;
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
   double* ring = reinterpret_cast<double*>(smem_raw);
   uint64_t* full =
       reinterpret_cast<uint64_t*>(smem_raw + (size_t)CHORD2_STAGES * STAGE2_DOUBLES * 8);

@@ -147,6 +147,13 @@ __global__ void normals_kernel(const RngParams rp, double* __restrict__ H,
   }
 }
 
+// Reference streams: walk c consumed `draws` uniforms (the normals kernel
+// reads the states without advancing them).
+__global__ void advance_streams_kernel(uint64_t* col_state, int64_t z, int64_t draws) {
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < z) col_state[c] += (uint64_t)draws * kGolden;
+}
+
 // ------------------------------------------------ projection D = P H -------
 // Straight DMMA tile product for the (small) n x n projector: one CTA per
 // (128 output coordinates x 64 walks) tile, operands staged through smem.
