@@ -243,6 +243,25 @@ typedef struct {
 int mhar_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t nb, int64_t n,
                          int device, mhar_fr_result* out);
 
+typedef struct mhar_lp_stats {
+  int32_t rounds;        /* constraint-generation rounds (LP solves) */
+  int32_t reserved;
+  int64_t pivots;        /* simplex pivots over all rounds */
+  int64_t working_rows;  /* inequality rows in the final working set */
+} mhar_lp_stats;
+
+/* chebyshev_center (chebyshev.hpp:22-25, chebyshev.cpp:45-66): the centre
+ * and radius of the largest ball inside p, the start point run() uses when no
+ * x0 is given (sampler.cpp:276).  The reference solves the LP of
+ * build_chebyshev_lp (chebyshev.cpp:9-43) with a dense tableau over all rows
+ * (lp.cpp:120-297); here constraint generation keeps a working set of rows in
+ * a GPU-resident tableau and scans all rows for violations on the GPU.
+ * Errors as the reference: EMPTY_POLYTOPE (infeasible), UNBOUNDED_POLYTOPE,
+ * NO_INTERIOR (radius <= 1e-10), NUMERICAL_FAILURE (centre fails
+ * containment at 1e-8), CYCLE_SUSPECTED (pivot budget).  stats may be NULL. */
+int mhar_chebyshev_center(const mhar_polytope* p, int device, double* x_out, double* radius,
+                          mhar_lp_stats* stats);
+
 const char* mhar_last_error(void);
 const char* mhar_version(void);
 int mhar_device_count(int* count);

@@ -130,7 +130,7 @@ EXPORTED_SYMBOLS = [
     "mhar_compute_projection", "mhar_get_stats", "mhar_set_timing", "mhar_reset_stats",
     "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
     "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
-    "mhar_select_points",
+    "mhar_select_points", "mhar_chebyshev_center",
 ]
 
 
@@ -138,6 +138,11 @@ class _FrResult(C.Structure):
     _fields_ = [("cross_edges", C.c_int64), ("expected_cross", C.c_double),
                 ("variance_cross", C.c_double), ("z_value", C.c_double),
                 ("shared_end_pairs", C.c_int64), ("pooled_size", C.c_int64)]
+
+class _LpStats(C.Structure):
+    _fields_ = [("rounds", C.c_int32), ("reserved", C.c_int32), ("pivots", C.c_int64),
+                ("working_rows", C.c_int64)]
+
 
 _lib = None
 
@@ -189,6 +194,9 @@ def lib():
     L.mhar_generate_directions.restype = C.c_int
     L.mhar_select_points.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp, _u8p, _dp]
     L.mhar_select_points.restype = C.c_int
+    L.mhar_chebyshev_center.argtypes = [C.POINTER(_Polytope), C.c_int, _dp, _dp,
+                                        C.POINTER(_LpStats)]
+    L.mhar_chebyshev_center.restype = C.c_int
     for name in ("mhar_ctx_create", "mhar_ctx_destroy", "mhar_set_state", "mhar_get_state",
                  "mhar_get_state_rows_device", "mhar_step", "mhar_sync", "mhar_step_timed",
                  "mhar_step_injected",
@@ -547,15 +555,53 @@ def contains(p: Polytope, x, eps: float) -> bool:
     return True
 
 
+@dataclasses.dataclass
+class ChebyshevCenter:
+    """chebyshev.hpp:8-11 (+ the constraint-generation counters)."""
+    x: np.ndarray
+    radius: float
+    rounds: int = 0
+    pivots: int = 0
+    working_rows: int = 0
+
+
+def chebyshev_center(p: Polytope, device: int = 0) -> ChebyshevCenter:
+    """chebyshev_center (chebyshev.hpp:22-25): centre and radius of the
+    largest inscribed ball, solved on the GPU by constraint generation over a
+    device-resident simplex tableau.  Raises EMPTY_POLYTOPE /
+    UNBOUNDED_POLYTOPE / NO_INTERIOR / NUMERICAL_FAILURE like the reference."""
+    L = lib()
+    a_in = np.asfortranarray(p.a_in, dtype=np.float64)
+    b_in = np.ascontiguousarray(p.b_in, dtype=np.float64)
+    poly = _Polytope()
+    poly.n = p.dim()
+    poly.m_in = p.num_inequalities()
+    poly.m_eq = p.num_equalities()
+    poly.a_in = a_in.ctypes.data_as(_dp)
+    poly.b_in = b_in.ctypes.data_as(_dp)
+    if poly.m_eq > 0:
+        a_eq = np.asfortranarray(p.a_eq, dtype=np.float64)
+        b_eq = np.ascontiguousarray(p.b_eq, dtype=np.float64)
+        poly.a_eq = a_eq.ctypes.data_as(_dp)
+        poly.b_eq = b_eq.ctypes.data_as(_dp)
+    x = np.zeros(p.dim())
+    r = C.c_double(0.0)
+    st = _LpStats()
+    _check(L.mhar_chebyshev_center(C.byref(poly), int(device), _d(x), C.byref(r), C.byref(st)))
+    return ChebyshevCenter(x=x, radius=r.value, rounds=st.rounds, pivots=st.pivots,
+                           working_rows=st.working_rows)
+
+
 def run(p: Polytope, cfg: SamplerConfig, x0=None, rng: str = "philox", slack: str = "incremental",
         device: int = 0) -> SampleSet:
-    """run() (sampler.cpp:274-335) on one B200.  x0 is the warm start that
-    replaces the reference's Chebyshev-center LP (sampler.cpp:276); it is
-    required (the dense-tableau LP does not scale to the target configs)."""
+    """run() (sampler.cpp:274-335) on one B200.  Without x0 the start is the
+    Chebyshev centre (sampler.cpp:276), computed before the clock starts as
+    in the reference; with x0 that warm start replaces it (start_radius 0)."""
     rc = resolve(cfg, p)
+    radius = 0.0
     if x0 is None:
-        raise MharError(ErrorCode.invalid_argument,
-                        "run: a warm start x0 is required (Chebyshev centering is out of scope)")
+        center = chebyshev_center(p, device=device)
+        x0, radius = center.x, center.radius
     projector = compute_projection(p.a_eq) if p.num_equalities() > 0 else None
     windows = (rc.t_target + rc.z - 1) // rc.z
     with Engine(p, rc.z, seed=rc.seed, projector=projector, eps_dir=rc.eps_dir,
@@ -563,5 +609,5 @@ def run(p: Polytope, cfg: SamplerConfig, x0=None, rng: str = "philox", slack: st
         samples, st = eng.run(x0, rc.phi, windows, rc.burn_in,
                               rc.reproject_every if projector is not None else 0)
     return SampleSet(samples=samples, config=rc, start=np.asarray(x0, dtype=np.float64),
-                     start_radius=0.0, seconds=st.seconds, iterate_count=st.iterate_count,
+                     start_radius=radius, seconds=st.seconds, iterate_count=st.iterate_count,
                      windows=st.windows, redraw_count=st.redraw_count)

@@ -228,14 +228,25 @@ struct SampleSet {
 
 using ClockFn = std::function<double()>;
 
-/// run() with a warm start x0 (the reference's run() derives the start from
-/// the Chebyshev-center LP, sampler.cpp:276; the engine takes it from the
-/// caller).  Samples are collected on the device.
+/// chebyshev.hpp:8-25: centre and radius of the largest inscribed ball.
+struct ChebyshevCenter {
+  Vector x;
+  double radius = 0.0;
+};
+inline constexpr double kMinInteriorRadius = 1e-10;
+
+/// Solved on the B200 (constraint generation over a device-resident simplex
+/// tableau); raises EMPTY_POLYTOPE / UNBOUNDED_POLYTOPE / NO_INTERIOR /
+/// NUMERICAL_FAILURE like the reference.
+ChebyshevCenter chebyshev_center(const Polytope& p);
+
+/// run() with a warm start x0 in place of the Chebyshev centre.  Samples are
+/// collected on the device.
 SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0,
               const ClockFn& clock = {});
 
-/// run() without a start point: raises INVALID_ARGUMENT (centering is not
-/// part of the engine; pass x0).
+/// run() (sampler.hpp:93-97): starts every walk at the Chebyshev centre
+/// (sampler.cpp:276), computed before the clock starts.
 SampleSet run(const Polytope& p, const SamplerConfig& cfg, const ClockFn& clock = {});
 
 }  // namespace mhar

@@ -266,9 +266,23 @@ SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0, con
   return out;
 }
 
-SampleSet run(const Polytope&, const SamplerConfig&, const ClockFn&) {
-  raise(ErrorCode::invalid_argument,
-        "run: pass a warm start x0 (Chebyshev centering is not part of the engine)");
+ChebyshevCenter chebyshev_center(const Polytope& p) {
+  mhar_polytope poly{p.dim(), p.num_inequalities(), p.num_equalities(), p.a_in.data(),
+                     p.b_in.data(), p.num_equalities() ? p.a_eq.data() : nullptr,
+                     p.num_equalities() ? p.b_eq.data() : nullptr};
+  ChebyshevCenter c;
+  c.x = Vector(p.dim());
+  check(mhar_chebyshev_center(&poly, 0, c.x.data(), &c.radius, nullptr));
+  return c;
+}
+
+SampleSet run(const Polytope& p, const SamplerConfig& cfg, const ClockFn& clock) {
+  // sampler.cpp:274-276: resolve, then centre, before the clock starts
+  resolve(cfg, p);
+  const ChebyshevCenter center = chebyshev_center(p);
+  SampleSet out = run(p, cfg, center.x, clock);
+  out.start_radius = center.radius;
+  return out;
 }
 
 }  // namespace mhar

@@ -153,7 +153,33 @@ int main() {
       double x[3] = {out.samples(r, 0), out.samples(r, 1), out.samples(r, 2)};
       CHECK(mhar::contains(cube, x, cfg.eps_feas));
     }
-    expect_error(mhar::ErrorCode::invalid_argument, [&] { mhar::run(cube, cfg); });
+    // without x0 the walks start at the Chebyshev centre: the origin, radius 1
+    const auto centred = mhar::run(cube, cfg);
+    CHECK(centred.start_radius == 1.0);
+    CHECK(centred.start(0) == 0.0 && centred.start(1) == 0.0 && centred.start(2) == 0.0);
+    CHECK(centred.samples == out.samples);
+  });
+
+  run_case("chebyshev centres: box exact, simplex barycentre, errors", [] {
+    for (int n : {2, 10, 100}) {
+      const auto c = mhar::chebyshev_center(mhar::make_hypercube(n));
+      CHECK(c.radius == 1.0);
+      for (int i = 0; i < n; ++i) CHECK(c.x(i) == 0.0);
+    }
+    for (int n : {3, 4, 10}) {
+      const auto c = mhar::chebyshev_center(mhar::make_simplex(n));
+      CHECK(std::fabs(c.radius - 1.0 / n) <= 1e-8);
+      for (int i = 0; i < n; ++i) CHECK(std::fabs(c.x(i) - 1.0 / n) <= 1e-8);
+    }
+    Matrix cone(1, 1);
+    cone(0, 0) = -1.0;
+    expect_error(mhar::ErrorCode::unbounded_polytope,
+                 [&] { mhar::chebyshev_center(mhar::Polytope(cone, Vector{0.0})); });
+    Matrix gap(2, 1);
+    gap(0, 0) = 1.0;
+    gap(1, 0) = -1.0;
+    expect_error(mhar::ErrorCode::empty_polytope,
+                 [&] { mhar::chebyshev_center(mhar::Polytope(gap, Vector{0.0, -1.0})); });
   });
 
   run_case("runs are bit-reproducible per seed and move between seeds", [] {

@@ -21,6 +21,7 @@
 #include "../../include/mhar_b200.h"
 #include "chord_kernel.cuh"
 #include "host_linalg.h"
+#include "lp.h"
 #include "step_kernels.cuh"
 #include "small_kernel.cuh"
 #include "chord_tc32.cuh"
@@ -1293,6 +1294,45 @@ int mhar_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t n
                                               std::to_string(out->variance_cross) +
                                               " is not positive");
   out->z_value = ((double)out->cross_edges - out->expected_cross) / std::sqrt(out->variance_cross);
+  return 0;
+}
+
+int mhar_chebyshev_center(const mhar_polytope* p, int device, double* x_out, double* radius,
+                          mhar_lp_stats* stats) {
+  if (!p || !x_out || !radius) return fail(MHAR_ERR_INVALID_ARGUMENT, "chebyshev_center: null argument");
+  if (p->n < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "chebyshev_center: dimension must be positive");
+  if (p->m_in < 0 || p->m_eq < 0 || (p->m_in > 0 && (!p->a_in || !p->b_in)) ||
+      (p->m_eq > 0 && (!p->a_eq || !p->b_eq)))
+    return fail(MHAR_ERR_DIMENSION_MISMATCH, "chebyshev_center: inconsistent polytope arrays");
+  mhar_lp::LpStats ls;
+  std::string msg;
+  const int st = mhar_lp::chebyshev_center(p->a_in, p->b_in, p->m_in, p->a_eq, p->b_eq, p->m_eq,
+                                           p->n, device, x_out, radius, &ls, &msg);
+  if (stats) {
+    stats->rounds = ls.rounds;
+    stats->reserved = 0;
+    stats->pivots = ls.pivots;
+    stats->working_rows = ls.working_rows;
+  }
+  if (st) return fail(st, msg);
+  // chebyshev.cpp:61-63: the centre must pass containment at kLpFeasTol
+  const int64_t n = p->n;
+  std::vector<double> ax(p->m_in, 0.0);
+  for (int64_t k = 0; k < n; ++k) {
+    const double* col = p->a_in + k * p->m_in;
+    for (int64_t i = 0; i < p->m_in; ++i) ax[i] += col[i] * x_out[k];
+  }
+  for (int64_t i = 0; i < p->m_in; ++i)
+    if (ax[i] > p->b_in[i] + 1e-8)
+      return fail(MHAR_ERR_NUMERICAL_FAILURE,
+                  "NUMERICAL_FAILURE: chebyshev_center: computed center fails containment");
+  for (int64_t i = 0; i < p->m_eq; ++i) {
+    double s = 0.0;
+    for (int64_t k = 0; k < n; ++k) s += p->a_eq[i + k * p->m_eq] * x_out[k];
+    if (std::fabs(s - p->b_eq[i]) > 1e-8)
+      return fail(MHAR_ERR_NUMERICAL_FAILURE,
+                  "NUMERICAL_FAILURE: chebyshev_center: computed center fails containment");
+  }
   return 0;
 }
 

@@ -1,0 +1,570 @@
+// lp.cu -- start point without a warm start: the
+// Chebyshev centre of {A_I x <= b_I, A_E x = b_E} (the reference's
+// chebyshev_center, /root/reference/proj/src/chebyshev.cpp:9-66: maximise r
+// subject to a_i x + |a_i| r <= b_i, A_E x = b_E, r >= 0) at scale.
+//
+// The reference solves that LP with a dense tableau over ALL rows
+// (src/lp.cpp:120-297), which cannot exceed ~1e4 rows.  Here the LP is solved
+// by constraint generation: a two-phase primal simplex (Dantzig pricing,
+// Bland's rule after a degenerate stall) on a working set of rows, with the
+// tableau resident on the GPU and every pivot one rank-1 update kernel; after
+// each solve one GEMV over all m_I rows finds the violated constraints, the
+// most violated are added, and the loop stops when none is violated.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "lp.h"
+
+namespace mhar_lp {
+namespace {
+
+constexpr double kPivotTol = 1e-10;
+constexpr double kDriveOutTol = 1e-7;
+constexpr double kDegenerateStep = 1e-12;
+constexpr double kReducedCostTol = 1e-9;
+constexpr double kFeasTol = 1e-8;
+constexpr int kThreads = 1024;
+
+// ---------------------------------------------------------------- kernels --
+// Tableau T: rows x cols row-major; b: rows; cost: cols.
+
+// Single CTA: entering column (Dantzig: largest reduced cost > tol; Bland:
+// first such column), then the leaving row by the minimum-ratio test with
+// ties (within 1e-15) broken by the smallest basic column.
+__global__ void __launch_bounds__(kThreads) select_kernel(const double* __restrict__ T,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ cost,
+                                                          const int* __restrict__ basis, int rows,
+                                                          int cols, int limit_col, int bland,
+                                                          int* out /* entering, leaving */,
+                                                          double* out_ratio) {
+  __shared__ double sv[kThreads / 32];
+  __shared__ int si[kThreads / 32];
+  __shared__ int s_enter;
+  __shared__ double s_min;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // pricing
+  double bv = bland ? 0.0 : kReducedCostTol;
+  int bi = 0x7FFFFFFF;
+  for (int j = tid; j < limit_col; j += kThreads) {
+    const double c = cost[j];
+    if (bland) {
+      if (c > kReducedCostTol && j < bi) bi = j;
+    } else if (c > bv || (c == bv && c > kReducedCostTol && j < bi)) {
+      bv = c;
+      bi = j;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+    const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+    if (bland ? (oi < bi) : (ov > bv || (ov == bv && oi < bi))) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if (lane == 0) {
+    sv[warp] = bv;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kThreads / 32; ++w)
+      if (bland ? (si[w] < bi) : (sv[w] > bv || (sv[w] == bv && si[w] < bi))) {
+        bv = sv[w];
+        bi = si[w];
+      }
+    s_enter = (bi == 0x7FFFFFFF) ? -1 : bi;
+    out[0] = s_enter;
+  }
+  __syncthreads();
+  const int e = s_enter;
+  if (e < 0) return;
+  // ratio test, pass 1: minimum ratio
+  double mr = __longlong_as_double(0x7FF0000000000000LL);
+  for (int i = tid; i < rows; i += kThreads) {
+    const double a = T[(size_t)i * cols + e];
+    if (a > kPivotTol) mr = fmin(mr, b[i] / a);
+  }
+  for (int o = 16; o > 0; o >>= 1) mr = fmin(mr, __shfl_xor_sync(0xFFFFFFFFu, mr, o));
+  if (lane == 0) sv[warp] = mr;
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kThreads / 32; ++w) mr = fmin(mr, sv[w]);
+    s_min = mr;
+  }
+  __syncthreads();
+  // pass 2: among ratios within 1e-15 of the minimum, the smallest basic column
+  const double lim = s_min + 1e-15;
+  int best_basic = 0x7FFFFFFF, best_row = -1;
+  if (s_min < __longlong_as_double(0x7FF0000000000000LL)) {
+    for (int i = tid; i < rows; i += kThreads) {
+      const double a = T[(size_t)i * cols + e];
+      if (a > kPivotTol && b[i] / a <= lim && basis[i] < best_basic) {
+        best_basic = basis[i];
+        best_row = i;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const int ob = __shfl_xor_sync(0xFFFFFFFFu, best_basic, o);
+    const int orow = __shfl_xor_sync(0xFFFFFFFFu, best_row, o);
+    if (ob < best_basic) {
+      best_basic = ob;
+      best_row = orow;
+    }
+  }
+  if (lane == 0) {
+    si[warp] = best_row;
+    sv[warp] = (double)best_basic;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < kThreads / 32; ++w)
+      if (sv[w] < (double)best_basic) {
+        best_basic = (int)sv[w];
+        best_row = si[w];
+      }
+    out[1] = best_row;
+    *out_ratio = s_min;
+  }
+}
+
+// pivot on (row, col): prow = T[row,:]/piv, fcol = T[:,col] captured first
+__global__ void capture_kernel(const double* __restrict__ T, const double* __restrict__ b,
+                               int rows, int cols, int row, int col, double* prow, double* fcol,
+                               double* pb) {
+  const double piv = T[(size_t)row * cols + col];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+    prow[j] = T[(size_t)row * cols + j] / piv;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+    fcol[i] = T[(size_t)i * cols + col];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *pb = b[row] / piv;
+}
+
+__global__ void pivot_kernel(double* __restrict__ T, double* __restrict__ b,
+                             double* __restrict__ cost, int* basis, int rows, int cols, int row,
+                             int col, const double* __restrict__ prow,
+                             const double* __restrict__ fcol, const double* pb) {
+  // blockIdx.y walks tableau rows (rows == the cost row), x-threads columns
+  const double brow = *pb;
+  const double cf = cost[col];  // nobody writes cost[col] in this launch
+  for (int i = blockIdx.y; i <= rows; i += gridDim.y) {
+    if (i == rows) {
+      if (cf != 0.0)
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+          if (j != col) cost[j] -= cf * prow[j];
+      continue;
+    }
+    double* Ti = T + (size_t)i * cols;
+    if (i == row) {
+      for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+        Ti[j] = prow[j];
+    } else {
+      const double f = fcol[i];
+      if (f != 0.0)
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+          Ti[j] -= f * prow[j];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (i == row) {
+        b[i] = brow;
+        basis[i] = col;
+      } else if (fcol[i] != 0.0) {
+        b[i] -= fcol[i] * brow;
+      }
+    }
+  }
+}
+
+__global__ void zero_cost_col_kernel(double* cost, int col) { cost[col] = 0.0; }
+
+// v_i = a_i x + |a_i| r - b_i over all rows (A column-major m x n)
+__global__ void violation_kernel(const double* __restrict__ A, const double* __restrict__ norms,
+                                 const double* __restrict__ bvec, const double* __restrict__ x,
+                                 double r, int64_t m, int64_t n, double* __restrict__ v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = 0; k < n; ++k) s = fma(A[i + k * m], x[k], s);
+    v[i] = s + norms[i] * r - bvec[i];
+  }
+}
+
+// ------------------------------------------------------------ the solver --
+
+struct Dev {
+  double *T = nullptr, *b = nullptr, *cost = nullptr, *prow = nullptr, *fcol = nullptr;
+  double *pb = nullptr, *ratio = nullptr;
+  int *basis = nullptr, *sel = nullptr;
+  cudaStream_t s = nullptr;
+  ~Dev() {
+    cudaFree(T);
+    cudaFree(b);
+    cudaFree(cost);
+    cudaFree(prow);
+    cudaFree(fcol);
+    cudaFree(pb);
+    cudaFree(ratio);
+    cudaFree(basis);
+    cudaFree(sel);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+int err(std::string* msg, int code, const std::string& text) {
+  *msg = text;
+  return code;
+}
+
+// Dense two-phase simplex: maximise c.x, rows kind (<= or =), x_j >= 0 or free.
+// The rows' right-hand sides are perturbed by up to `perturb` (deterministic
+// per row) so the highly degenerate vertices of the centring LP do not stall
+// the pivoting; the unperturbed rhs rides along as one extra tableau column,
+// so the final basis is evaluated on the original problem.  Returns 0 /
+// EMPTY(5) / UNBOUNDED(7) / CYCLE(10) / CUDA(100), or kPerturbedOnly when the
+// final basis is infeasible for the unperturbed rhs (retry with less).
+constexpr int kPerturbedOnly = 1000;
+
+int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::vector<double>& rhs,
+            const std::vector<int>& is_eq, const std::vector<int>& is_free,
+            const std::vector<double>& obj, int m, int nv, double perturb, double scale,
+            int l1_row, std::vector<double>* x, long* pivots, std::string* msg) {
+  std::vector<int> var_col(nv);
+  int ncols = 0;
+  for (int v = 0; v < nv; ++v) {
+    var_col[v] = ncols;
+    ncols += is_free[v] ? 2 : 1;
+  }
+  int nslack = 0;
+  for (int i = 0; i < m; ++i) nslack += is_eq[i] ? 0 : 1;
+  const int structural = ncols + nslack;
+  // artificials for rows whose slack cannot start basic
+  std::vector<double> sgn(m);
+  int nart = 0;
+  for (int i = 0; i < m; ++i) {
+    sgn[i] = rhs[i] < 0 ? -1.0 : 1.0;
+    if (is_eq[i] || sgn[i] < 0) ++nart;
+  }
+  const int total = structural + nart;  // priced columns
+  const int W = total + 1;              // + the unperturbed rhs column
+  std::vector<double> T((size_t)m * W, 0.0), b(m);
+  std::vector<int> basis(m, -1);
+  int slack = ncols, art = structural;
+  std::vector<char> has_art(m, 0);
+  for (int i = 0; i < m; ++i) {
+    double* row = &T[(size_t)i * W];
+    for (int v = 0; v < nv; ++v) {
+      const double a = sgn[i] * Arow[(size_t)i * nv + v];
+      row[var_col[v]] = a;
+      if (is_free[v]) row[var_col[v] + 1] = i == l1_row ? a : -a;  // l1: x+ + x- <= B
+    }
+    row[total] = sgn[i] * rhs[i];
+    // golden-ratio sequence in [0.5, 1.5): distinct, deterministic per row
+    const double u = 0.5 + std::fmod(0.6180339887498949 * (i + 1), 1.0);
+    b[i] = row[total] + (is_eq[i] ? 0.0 : perturb * u);
+    if (!is_eq[i]) {
+      row[slack] = sgn[i];
+      if (sgn[i] > 0) basis[i] = slack;
+      ++slack;
+    }
+    if (basis[i] < 0) {
+      row[art] = 1.0;
+      basis[i] = art;
+      has_art[i] = 1;
+      ++art;
+    }
+  }
+  Dev d;
+  auto ok = [](cudaError_t e) { return e == cudaSuccess; };
+  if (!ok(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking)) ||
+      !ok(cudaMalloc(&d.T, sizeof(double) * T.size())) ||
+      !ok(cudaMalloc(&d.b, sizeof(double) * m)) || !ok(cudaMalloc(&d.cost, sizeof(double) * W)) ||
+      !ok(cudaMalloc(&d.prow, sizeof(double) * W)) ||
+      !ok(cudaMalloc(&d.fcol, sizeof(double) * m)) || !ok(cudaMalloc(&d.pb, sizeof(double))) ||
+      !ok(cudaMalloc(&d.ratio, sizeof(double))) || !ok(cudaMalloc(&d.basis, sizeof(int) * m)) ||
+      !ok(cudaMalloc(&d.sel, sizeof(int) * 2)))
+    return err(msg, 100, "simplex: device allocation failed");
+  cudaMemcpyAsync(d.T, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice, d.s);
+  cudaMemcpyAsync(d.b, b.data(), sizeof(double) * m, cudaMemcpyHostToDevice, d.s);
+  cudaMemcpyAsync(d.basis, basis.data(), sizeof(int) * m, cudaMemcpyHostToDevice, d.s);
+
+  const long budget = 10000 + 200L * (m + total);
+  long npiv = 0;
+  int rows = m;
+  auto pivot = [&](int row, int col) {
+    capture_kernel<<<std::max(1, std::min(1024, (std::max(rows, W) + 255) / 256)), 256, 0, d.s>>>(
+        d.T, d.b, rows, W, row, col, d.prow, d.fcol, d.pb);
+    const dim3 g((unsigned)std::min(8, (W + 255) / 256), (unsigned)std::min(rows + 1, 65535));
+    pivot_kernel<<<g, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, row, col, d.prow, d.fcol,
+                                     d.pb);
+    zero_cost_col_kernel<<<1, 1, 0, d.s>>>(d.cost, col);
+    ++npiv;
+  };
+  // one phase: 0 optimal, 7 unbounded ray, 10 budget, 100 CUDA
+  auto run_phase = [&](int limit_col) -> int {
+    int stall = 0;
+    bool bland = false;
+    for (;;) {
+      select_kernel<<<1, kThreads, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, limit_col,
+                                             bland ? 1 : 0, d.sel, d.ratio);
+      int sel[2];
+      double ratio;
+      cudaMemcpyAsync(sel, d.sel, sizeof(sel), cudaMemcpyDeviceToHost, d.s);
+      cudaMemcpyAsync(&ratio, d.ratio, sizeof(double), cudaMemcpyDeviceToHost, d.s);
+      if (cudaStreamSynchronize(d.s) != cudaSuccess) return 100;
+      if (sel[0] < 0) return 0;
+      if (sel[1] < 0) return 7;
+      if (ratio < kDegenerateStep) {
+        if (++stall > rows + total) bland = true;
+      } else {
+        stall = 0;
+      }
+      pivot(sel[1], sel[0]);
+      if (npiv > budget) return 10;
+    }
+  };
+  auto fetch_row = [&](int i, double* dst) {
+    cudaMemcpyAsync(dst, d.T + (size_t)i * W, sizeof(double) * W, cudaMemcpyDeviceToHost, d.s);
+    cudaStreamSynchronize(d.s);
+  };
+
+  if (nart > 0) {
+    // phase one: maximise -sum(artificials)
+    std::vector<double> c1(W, 0.0);
+    for (int i = 0; i < m; ++i)
+      if (has_art[i])
+        for (int j = 0; j < structural; ++j) c1[j] += T[(size_t)i * W + j];
+    cudaMemcpyAsync(d.cost, c1.data(), sizeof(double) * W, cudaMemcpyHostToDevice, d.s);
+    const int st = run_phase(total);
+    if (st == 100) return err(msg, 100, "simplex: CUDA failure");
+    if (st == 10) return err(msg, 10, "CYCLE_SUSPECTED: solve_lp: pivot budget exhausted");
+    if (st == 7) return err(msg, 12, "NUMERICAL_FAILURE: phase one reported an unbounded ray");
+    cudaMemcpyAsync(b.data(), d.b, sizeof(double) * m, cudaMemcpyDeviceToHost, d.s);
+    cudaMemcpyAsync(basis.data(), d.basis, sizeof(int) * m, cudaMemcpyDeviceToHost, d.s);
+    cudaStreamSynchronize(d.s);
+    double mass = 0.0;
+    for (int i = 0; i < rows; ++i)
+      if (basis[i] >= structural) mass += b[i];
+    if (mass > kFeasTol * scale + 2.0 * m * perturb)
+      return err(msg, 5, "EMPTY_POLYTOPE: chebyshev_center: constraint system is infeasible");
+    // drive basic artificials out, or drop their rows as redundant
+    std::vector<char> drop(rows, 0);
+    int ndrop = 0;
+    for (int i = 0; i < rows; ++i) {
+      if (basis[i] < structural) continue;
+      double* Ti = &T[(size_t)i * W];
+      fetch_row(i, Ti);
+      int col = -1;
+      for (int j = 0; j < structural && col < 0; ++j)
+        if (std::fabs(Ti[j]) > kDriveOutTol) col = j;
+      if (col >= 0) {
+        pivot(i, col);
+      } else {
+        drop[i] = 1;
+        ++ndrop;
+      }
+    }
+    if (ndrop > 0) {
+      std::vector<int> dbasis(rows);
+      cudaMemcpyAsync(T.data(), d.T, sizeof(double) * (size_t)rows * W, cudaMemcpyDeviceToHost,
+                      d.s);
+      cudaMemcpyAsync(b.data(), d.b, sizeof(double) * rows, cudaMemcpyDeviceToHost, d.s);
+      cudaMemcpyAsync(dbasis.data(), d.basis, sizeof(int) * rows, cudaMemcpyDeviceToHost, d.s);
+      cudaStreamSynchronize(d.s);
+      int k = 0;
+      for (int i = 0; i < rows; ++i) {
+        if (drop[i]) continue;
+        if (k != i) std::memmove(&T[(size_t)k * W], &T[(size_t)i * W], sizeof(double) * W);
+        b[k] = b[i];
+        basis[k] = dbasis[i];
+        ++k;
+      }
+      rows = k;
+      cudaMemcpyAsync(d.T, T.data(), sizeof(double) * (size_t)rows * W, cudaMemcpyHostToDevice,
+                      d.s);
+      cudaMemcpyAsync(d.b, b.data(), sizeof(double) * rows, cudaMemcpyHostToDevice, d.s);
+      cudaMemcpyAsync(d.basis, basis.data(), sizeof(int) * rows, cudaMemcpyHostToDevice, d.s);
+    }
+  }
+  // phase two: reduced costs of the objective against the current basis
+  std::vector<double> c2(W, 0.0);
+  for (int v = 0; v < nv; ++v) {
+    c2[var_col[v]] = obj[v];
+    if (is_free[v]) c2[var_col[v] + 1] = -obj[v];
+  }
+  cudaMemcpyAsync(basis.data(), d.basis, sizeof(int) * rows, cudaMemcpyDeviceToHost, d.s);
+  cudaStreamSynchronize(d.s);
+  std::vector<double> red = c2;
+  for (int i = 0; i < rows; ++i) {
+    const double cb = c2[basis[i]];
+    if (cb == 0.0) continue;
+    std::vector<double> Ti(W);
+    fetch_row(i, Ti.data());
+    for (int j = 0; j < W; ++j) red[j] -= cb * Ti[j];
+  }
+  cudaMemcpyAsync(d.cost, red.data(), sizeof(double) * W, cudaMemcpyHostToDevice, d.s);
+  const int st = run_phase(structural);
+  if (st == 100) return err(msg, 100, "simplex: CUDA failure");
+  if (st == 10) return err(msg, 10, "CYCLE_SUSPECTED: solve_lp: pivot budget exhausted");
+  if (st == 7)
+    return err(msg, 7, "UNBOUNDED_POLYTOPE: chebyshev_center: inscribed radius is unbounded");
+  *pivots += npiv;
+  // the optimal basis applied to the unperturbed rhs
+  std::vector<double> orig(rows);
+  cudaMemcpy2DAsync(orig.data(), sizeof(double), d.T + total, sizeof(double) * W, sizeof(double),
+                    rows, cudaMemcpyDeviceToHost, d.s);
+  cudaMemcpyAsync(basis.data(), d.basis, sizeof(int) * rows, cudaMemcpyDeviceToHost, d.s);
+  if (cudaStreamSynchronize(d.s) != cudaSuccess) return err(msg, 100, "simplex: CUDA failure");
+  std::vector<double> expanded(W, 0.0);
+  for (int i = 0; i < rows; ++i) {
+    if (orig[i] < -1e-9 * scale) return kPerturbedOnly;
+    expanded[basis[i]] = std::max(orig[i], 0.0);
+  }
+  x->assign(nv, 0.0);
+  for (int v = 0; v < nv; ++v)
+    (*x)[v] = is_free[v] ? expanded[var_col[v]] - expanded[var_col[v] + 1] : expanded[var_col[v]];
+  return 0;
+}
+
+}  // namespace
+
+int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const double* a_eq,
+                     const double* b_eq, int64_t me, int64_t n, int device, double* x_out,
+                     double* radius, LpStats* stats, std::string* msg) {
+  if (cudaSetDevice(device) != cudaSuccess) return err(msg, 100, "cudaSetDevice failed");
+  // row norms and scale
+  std::vector<double> norms(m, 0.0);
+  for (int64_t k = 0; k < n; ++k)
+    for (int64_t i = 0; i < m; ++i) norms[i] += a_in[i + k * m] * a_in[i + k * m];
+  for (auto& v : norms) v = std::sqrt(v);
+  double scale = 1.0;
+  for (int64_t i = 0; i < m; ++i) scale = std::max(scale, std::fabs(b_in[i]));
+  // device copies for the violation scan
+  double *dA = nullptr, *dN = nullptr, *dB = nullptr, *dX = nullptr, *dV = nullptr;
+  auto free_all = [&]() {
+    cudaFree(dA);
+    cudaFree(dN);
+    cudaFree(dB);
+    cudaFree(dX);
+    cudaFree(dV);
+  };
+  if (cudaMalloc(&dA, sizeof(double) * m * n) != cudaSuccess ||
+      cudaMalloc(&dN, sizeof(double) * m) != cudaSuccess ||
+      cudaMalloc(&dB, sizeof(double) * m) != cudaSuccess ||
+      cudaMalloc(&dX, sizeof(double) * n) != cudaSuccess ||
+      cudaMalloc(&dV, sizeof(double) * m) != cudaSuccess) {
+    free_all();
+    return err(msg, 100, "chebyshev_center: device allocation failed");
+  }
+  cudaMemcpy(dA, a_in, sizeof(double) * m * n, cudaMemcpyHostToDevice);
+  cudaMemcpy(dN, norms.data(), sizeof(double) * m, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, b_in, sizeof(double) * m, cudaMemcpyHostToDevice);
+
+  // initial working set: per coordinate and sign the row that bounds it most
+  // tightly (largest a_ij / |a_i|), so the restricted LP is usually bounded
+  std::vector<char> in_w(m, 0);
+  std::vector<int64_t> work;
+  for (int64_t k = 0; k < n; ++k)
+    for (int sgn = -1; sgn <= 1; sgn += 2) {
+      int64_t best = -1;
+      double bv = 0.0;
+      for (int64_t i = 0; i < m; ++i) {
+        const double v = sgn * a_in[i + k * m] / std::max(norms[i], 1e-300);
+        if (v > bv) {
+          bv = v;
+          best = i;
+        }
+      }
+      if (best >= 0 && !in_w[best]) {
+        in_w[best] = 1;
+        work.push_back(best);
+      }
+    }
+  if ((int64_t)work.size() == m) {
+    // everything is already in
+  }
+  const double box = 1e6 * scale;  // temporary bound; touching it means unbounded
+  std::vector<double> xr;
+  int rounds = 0;
+  long pivots = 0;
+  int status = 0;
+  for (;;) {
+    ++rounds;
+    const int nv = (int)n + 1;
+    // + one l1 row sum(x+ + x-) <= box keeping the restricted LP bounded
+    const int mw = (int)me + (int)work.size() + 1;
+    std::vector<double> A((size_t)mw * nv, 0.0), rhs(mw);
+    std::vector<int> is_eq(mw, 0), is_free(nv, 1);
+    is_free[n] = 0;
+    int r = 0;
+    for (int64_t i = 0; i < me; ++i, ++r) {
+      for (int64_t k = 0; k < n; ++k) A[(size_t)r * nv + k] = a_eq[i + k * me];
+      rhs[r] = b_eq[i];
+      is_eq[r] = 1;
+    }
+    for (int64_t i : work) {
+      for (int64_t k = 0; k < n; ++k) A[(size_t)r * nv + k] = a_in[i + k * m];
+      A[(size_t)r * nv + n] = norms[i];
+      rhs[r] = b_in[i];
+      ++r;
+    }
+    const int l1_row = r;
+    for (int64_t k = 0; k < n; ++k) A[(size_t)r * nv + k] = 1.0;
+    rhs[r] = box;
+    std::vector<double> obj(nv, 0.0);
+    obj[n] = 1.0;
+    // perturbed first; less (then none) if that basis misses the original
+    for (double eps : {1e-7, 1e-10, 0.0}) {
+      status = simplex(A, rhs, is_eq, is_free, obj, mw, nv, eps * scale, scale, l1_row, &xr,
+                       &pivots, msg);
+      if (status != kPerturbedOnly) break;
+    }
+    if (status) break;
+    // violations over all rows on the GPU
+    cudaMemcpy(dX, xr.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
+    violation_kernel<<<std::max<int64_t>(1, std::min<int64_t>(4096, (m + 255) / 256)), 256>>>(
+        dA, dN, dB, dX, xr[n], m, n, dV);
+    std::vector<double> v(m);
+    if (cudaMemcpy(v.data(), dV, sizeof(double) * m, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      status = err(msg, 100, "chebyshev_center: violation scan failed");
+      break;
+    }
+    std::vector<int64_t> viol;
+    for (int64_t i = 0; i < m; ++i)
+      if (!in_w[i] && v[i] > 1e-10 * scale) viol.push_back(i);
+    if (viol.empty()) break;
+    const size_t add = std::min<size_t>(viol.size(), (size_t)std::max<int64_t>(64, 2 * n));
+    std::partial_sort(viol.begin(), viol.begin() + add, viol.end(),
+                      [&](int64_t a, int64_t b) { return v[a] > v[b]; });
+    for (size_t t = 0; t < add; ++t) {
+      in_w[viol[t]] = 1;
+      work.push_back(viol[t]);
+    }
+  }
+  free_all();
+  if (stats) {
+    stats->rounds = rounds;
+    stats->pivots = pivots;
+    stats->working_rows = (int64_t)work.size();
+  }
+  if (status) return status;
+  double l1 = 0.0;
+  for (int64_t k = 0; k < n; ++k) l1 += std::fabs(xr[k]);
+  if (l1 >= 0.5 * box)  // the centre ran out to the artificial bound
+    return err(msg, 7, "UNBOUNDED_POLYTOPE: chebyshev_center: inscribed radius is unbounded");
+  std::memcpy(x_out, xr.data(), sizeof(double) * n);
+  *radius = xr[n];
+  if (*radius <= 1e-10)  // chebyshev.hpp:21 kMinInteriorRadius
+    return err(msg, 6, "NO_INTERIOR: chebyshev_center: optimal radius " + std::to_string(*radius) +
+                           " leaves no interior to walk in");
+  return 0;
+}
+
+}  // namespace mhar_lp
