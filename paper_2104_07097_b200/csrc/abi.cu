@@ -93,6 +93,8 @@ struct mhar_ctx {
   // fp32 variant (chord_tc32.cuh)
   float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr;
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
+  int tc_group_n = 1;   // tc32 rasterisation band (row tiles); MHAR_TC_GROUP overrides
+  int tc_a_policy = 0;  // L2 policy of the tc32 A stream (evict_normal); MHAR_TC_APOL overrides
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
   double* rows2 = nullptr;
   double* pinned[2] = {nullptr, nullptr};
@@ -246,7 +248,7 @@ int launch_tc32(mhar_ctx* c) {
   p.Alo = c->Alo;
   p.Dhi = c->Dhi;
   p.S = c->S;
-  p.R = c->R;
+  p.R = reinterpret_cast<float*>(c->R);
   p.theta_prev = c->theta;
   p.hi_key = c->hi_key;
   p.lo_key = c->lo_key;
@@ -260,9 +262,10 @@ int launch_tc32(mhar_ctx* c) {
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
   p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 2e-5;
-  p.group_n = 2;
-  const int64_t units = p.row_tiles * p.walk_tiles;
-  const int grid = (int)std::min<int64_t>(units, c->num_sms);
+  p.group_n = c->tc_group_n;
+  p.a_policy = c->tc_a_policy;
+  const int64_t units = p.row_tiles * (p.walk_tiles / 2);  // (row tile, walk-tile pair)
+  const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);  // CTA pairs
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (c->timing) {
     ev = take_events(c);
@@ -656,7 +659,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   c->KT = c->n_pad / BK;
   c->m_pad = round_up(c->m, fp32 ? TC_N : BM);
   c->m_tiles = c->m_pad / BM;
-  c->z_pad = round_up(c->z, fp32 ? TC_M : 64);
+  c->z_pad = round_up(c->z, fp32 ? 2 * TC_M : 64);  // fp32: whole CTA-pair walk tiles
   c->ct64 = c->z_pad / 64;
   if (fp32) {
     c->tc_row_tiles = c->m_pad / TC_N;
@@ -684,6 +687,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     return bail(st);
   c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
   if (const char* g = std::getenv("MHAR_GROUP_M")) c->group_m = std::max(1, std::atoi(g));
+  if (const char* g = std::getenv("MHAR_TC_GROUP")) c->tc_group_n = std::max(1, std::atoi(g));
+  if (const char* g = std::getenv("MHAR_TC_APOL")) c->tc_a_policy = std::atoi(g) % 3;
   if ((st = dalloc(c, &c->redraw_scratch, (size_t)c->redraw_grid * 3 * c->n))) return bail(st);
   if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
     const size_t cache = (size_t)c->m_pad * c->z_pad;

@@ -282,7 +282,10 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
           if (MODE == FUSED_STORE) {
             const int64_t si = cache_index(r, c0[j] + 2 * (lane & 3) + e, p);
             p.S[si] = sl;
-            p.R[si] = ad;
+            if (p.tc_walk_tiles > 0)  // the fp32 variant keeps its rates in fp32
+              reinterpret_cast<float*>(p.R)[si] = (float)ad;
+            else
+              p.R[si] = ad;
           }
         }
     }

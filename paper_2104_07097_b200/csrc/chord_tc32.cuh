@@ -12,14 +12,23 @@
 // exactly feasible despite fp32 rates, chords are taken in the body shrunk
 // by a margin mu (slack - mu), see DESIGN.md "fp32 variant".
 //
-// Tile: M = 128 walks (TMEM lanes) x N = 256 inequality rows (TMEM
-// columns), K step 16 per stage.  With walks on the lanes each epilogue
-// thread owns ONE walk and reduces its 256 rows in registers -- no shuffles.
+// CTA pair (cluster of 2, tcgen05 cta_group::2): one MMA is M = 256 walks
+// (128 per CTA, on each CTA's TMEM lanes) x N = 256 inequality rows, K step
+// 16 per stage.  Each CTA stages its own 128 walks of D and ONE HALF (128
+// rows) of the row tile's A_hi / A_lo, so per SM a stage is 24 KB for the
+// work a single-CTA M = 128 x N = 256 tile needed 40 KB for -- the kernel is
+// bounded by L2 -> SM bandwidth, not by the tensor pipe.  Both CTAs' TMEM
+// hold all 256 rows for their own walks, so each epilogue thread still owns
+// one walk and reduces its 256 rows in registers.
 //
-// Warp roles (192 threads): warp 0 lane 0 = bulk-copy producer, warp 1 lane
-// 0 = MMA issuer (+ TMEM allocation), warps 2..5 = epilogue (TMEM lane
-// quarter = warp % 4).  The 512-column TMEM holds two 256-column
-// accumulators so the epilogue of one tile overlaps the MMAs of the next.
+// Warp roles (192 threads per CTA): warp 0 lane 0 = bulk-copy producer (its
+// CTA's pieces); warp 1 = TMEM allocation (both CTAs), lane 0 = MMA issuer
+// in the even CTA and the "stage landed" relay in the odd one (waits its
+// CTA's full barrier, arrives remotely on the leader's peer barrier); warps
+// 2..9 = epilogue (TMEM lane quarter = warp % 4, two warps per quarter
+// splitting the rows).  Two 256-column
+// accumulators (512 TMEM columns) let the epilogue of one unit overlap the
+// MMAs of the next.
 #pragma once
 
 #include "chord_kernel.cuh"
@@ -27,28 +36,32 @@
 
 namespace mhar_dev {
 
-constexpr int TC_M = 128;             // walks per tile
-constexpr int TC_N = 256;             // rows per tile
+constexpr int TC_M = 128;             // walks per CTA (per unit: 2 x 128)
+constexpr int TC_N = 256;             // rows per unit
+constexpr int TC_NH = 128;            // rows staged by each CTA of the pair
 constexpr int TC_BK = 16;             // k per stage
-constexpr int TC_STAGES = 5;
+constexpr int TC_STAGES = 8;
 constexpr int TC_D_PIECE = TC_M * TC_BK;   // floats per D stage piece (8 KB)
-constexpr int TC_A_PIECE = TC_N * TC_BK;   // floats per A_hi (or A_lo) stage piece (16 KB)
-constexpr int TC_STAGE_FLOATS = TC_D_PIECE + 2 * TC_A_PIECE;  // 40 KB
-constexpr int TC_THREADS = 192;
-constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 256;
+constexpr int TC_A_PIECE = TC_NH * TC_BK;  // floats per A_hi (or A_lo) half piece (8 KB)
+constexpr int TC_STAGE_FLOATS = TC_D_PIECE + 2 * TC_A_PIECE;  // 24 KB
+constexpr int TC_EPI_WARPS = 8;       // two per TMEM lane quarter, each owns half the rows
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
+constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 512;
 
 // Interleaved K-major ("no swizzle") core-matrix layout of one (tile, k_tile)
 // piece of R rows: [k_chunk(4 floats)][row_group(8 rows)][row(8)][4].
 __host__ __device__ inline int64_t tc_piece_index(int64_t r, int64_t kk, int64_t R) {
   return ((kk >> 2) * (R >> 3) + (r >> 3)) * 32 + (r & 7) * 4 + (kk & 3);
 }
-// (walk c, coordinate k) in the packed TF32 direction array.
+// (walk c, coordinate k) in the packed TF32 direction array: [walk_tile(128)][k_tile][piece].
 __host__ __device__ inline int64_t tc_d_index(int64_t c, int64_t k, int64_t KT) {
   return ((c / TC_M) * KT + k / TC_BK) * TC_D_PIECE + tc_piece_index(c % TC_M, k % TC_BK, TC_M);
 }
-// (row r, coordinate k) in the packed fp32 A_hi / A_lo arrays.
+// (row r, coordinate k) in the packed fp32 A_hi / A_lo arrays:
+// [row_tile(256)][k_tile][half(128 rows)][piece] -- CTA h of a pair loads half h.
 __host__ __device__ inline int64_t tc_a_index(int64_t r, int64_t k, int64_t KT) {
-  return ((r / TC_N) * KT + k / TC_BK) * TC_A_PIECE + tc_piece_index(r % TC_N, k % TC_BK, TC_N);
+  return (((r / TC_N) * KT + k / TC_BK) * 2 + (r % TC_N) / TC_NH) * TC_A_PIECE +
+         tc_piece_index(r % TC_NH, k % TC_BK, TC_NH);
 }
 // slack / rate cache for the tc32 tile: [row_tile][walk_tile][row(256)][walk(128)]
 __host__ __device__ inline int64_t tc_s_index(int64_t r, int64_t c, int64_t WT) {
@@ -68,20 +81,55 @@ __device__ inline uint64_t umma_desc(const void* p, uint32_t lbo, uint32_t sbo) 
   d |= (uint64_t)1 << 46;
   return d;
 }
-// instruction descriptor: F32 accumulate, A/B TF32, K-major, M = 128, N = 256
+// instruction descriptor: F32 accumulate, A/B TF32, K-major, M = 256 (pair), N = 256
 constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
-                              ((uint32_t)(TC_M >> 4) << 24);
+                              ((uint32_t)((2 * TC_M) >> 4) << 24);
 
-__device__ inline void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t accumulate) {
+__device__ inline void tc_mma2(uint32_t tmem, uint64_t da, uint64_t db, uint32_t accumulate) {
   asm volatile(
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(TC_IDESC), "r"(accumulate));
 }
-__device__ inline void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
+// arrive on the barrier at the same smem offset in both CTAs of the pair
+// once every previously issued MMA of this thread has completed
+__device__ inline void tc_commit2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((unsigned short)3)
+      : "memory");
+}
+__device__ inline uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ inline void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" :::
+                   "memory");
+}
+// arrive on the barrier at `bar`'s offset in CTA `rank`.  Relaxed: what it
+// publishes is not this thread's writes but completions it has observed (a
+// stage's bulk copies landed, TMEM loads waited on), so the release fence --
+// a MEMBAR.ALL.GPU per stage -- would only slow the pipeline.
+__device__ inline void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                : "memory");
+}
+// wait with cluster-scope acquire (pairs with mbar_arrive_remote)
+__device__ inline void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 __device__ inline void tc_ld32(uint32_t addr, float (&v)[32]) {
   uint32_t r[32];
@@ -104,7 +152,7 @@ struct TcParams {
   const float* Alo;
   const float* Dhi;  // tc_d_index layout, TF32-exact directions
   double* S;         // tc_s_index layout, fp64 slack
-  double* R;         // fp64 rates of the previous iterate
+  float* R;          // rates of the previous iterate (fp32: what the MMA produced)
   const double* theta_prev;
   long long* hi_key;
   long long* lo_key;
@@ -112,81 +160,92 @@ struct TcParams {
   unsigned* sides;
   const unsigned long long* err;
   int64_t row_tiles;   // m_pad / 256
-  int64_t walk_tiles;  // z_pad / 128
+  int64_t walk_tiles;  // z_pad / 128 (even: units take walk-tile pairs)
   int64_t KT;          // n_pad / 16
   int64_t m;           // live rows
   int64_t z;           // live walks
   double eps_dir;
   double margin;       // mu: chords of {A x <= b - mu}
   int group_n;         // rasterisation band (row tiles)
+  int a_policy;        // L2 policy of the A_hi/A_lo stream: 0 normal, 1 evict_last, 2 evict_first
 };
 
-__device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_t* wt) {
-  const int64_t band_units = (int64_t)p.group_n * p.walk_tiles;
+// unit u -> (row tile, walk-tile pair), banded over group_n row tiles
+__device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_t* wp) {
+  const int64_t pairs = p.walk_tiles / 2;
+  const int64_t band_units = (int64_t)p.group_n * pairs;
   const int64_t band = u / band_units;
   const int64_t in_band = u - band * band_units;
   const int64_t start = band * p.group_n;
   const int64_t h = (p.row_tiles - start < p.group_n) ? p.row_tiles - start : p.group_n;
   *rt = start + in_band % h;
-  *wt = in_band / h;
+  *wp = in_band / h;
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParams p) {
-  if (*p.err != kNoError) return;
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+    chord_tc32_kernel(const TcParams p) {
+  if (*p.err != kNoError) return;  // read identically by both CTAs of the pair
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   float* ring = reinterpret_cast<float*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)TC_STAGES * TC_STAGE_FLOATS * 4);
   uint64_t* empty = full + TC_STAGES;
-  uint64_t* tfull = empty + TC_STAGES;  // [2] accumulator ready
-  uint64_t* tempty = tfull + 2;         // [2] accumulator drained
+  uint64_t* peer_full = empty + TC_STAGES;  // leader: the odd CTA's stage landed
+  uint64_t* tfull = peer_full + TC_STAGES;  // [2] accumulator ready (both CTAs)
+  uint64_t* tempty = tfull + 2;             // [2] accumulator drained (leader, 8 warps)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t n_units = p.row_tiles * p.walk_tiles;
-  const int my_units =
-      (blockIdx.x < n_units) ? (int)((n_units - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const uint32_t rank = cluster_rank();
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int64_t n_units = p.row_tiles * (p.walk_tiles / 2);
+  const int my_units = (pair < n_units) ? (int)((n_units - 1 - pair) / npairs + 1) : 0;
   const int KT = (int)p.KT;
 
   if (tid == 0) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&peer_full[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 4);  // one arrive per epilogue warp
+      mbar_init(&tempty[b], 2 * TC_EPI_WARPS);  // every epilogue warp of both CTAs
     }
     fence_barrier_init();
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tptr)),
                  "n"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tptr;
 
   if (warp == 0) {
-    // ---------------- producer ----------------
+    // ---------------- producer: this CTA's D tile + A half ----------------
     if (lane == 0) {
-      uint64_t keep = policy_evict_last();
+      const uint64_t keep = policy_evict_last();  // D: re-read by every row tile
+      const uint64_t apol = p.a_policy == 1   ? keep
+                            : p.a_policy == 2 ? policy_evict_first()
+                                              : policy_evict_normal();
       int stage = 0, round = 0;
       for (int ui = 0; ui < my_units; ++ui) {
-        int64_t rt, wt;
-        tc_unit(blockIdx.x + (int64_t)ui * gridDim.x, p, &rt, &wt);
+        int64_t rt, wp;
+        tc_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+        const int64_t wt = 2 * wp + rank;
         for (int kt = 0; kt < KT; ++kt) {
           if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
           float* st = ring + (size_t)stage * TC_STAGE_FLOATS;
           mbar_arrive_expect_tx(&full[stage], TC_STAGE_FLOATS * 4);
           const int64_t doff = (wt * p.KT + kt) * TC_D_PIECE;
-          const int64_t aoff = (rt * p.KT + kt) * TC_A_PIECE;
+          const int64_t aoff = ((rt * p.KT + kt) * 2 + rank) * TC_A_PIECE;
           bulk_g2s_hint(st, p.Dhi + doff, TC_D_PIECE * 4, &full[stage], keep);
-          bulk_g2s_hint(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage], keep);
+          bulk_g2s_hint(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage], apol);
           bulk_g2s_hint(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage],
-                        keep);
+                        apol);
           if (++stage == TC_STAGES) {
             stage = 0;
             ++round;
@@ -195,16 +254,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA) ----------------
       int stage = 0, phase = 0;
       for (int ui = 0; ui < my_units; ++ui) {
         const int ab = ui & 1;
-        if (ui >= 2) mbar_wait(&tempty[ab], (uint32_t)(((ui >> 1) - 1) & 1));
+        if (ui >= 2) mbar_wait_cluster(&tempty[ab], (uint32_t)(((ui >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t acc = tmem + (uint32_t)(ab * TC_N);
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], (uint32_t)phase);
+          mbar_wait_cluster(&peer_full[stage], (uint32_t)phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const float* sd = ring + (size_t)stage * TC_STAGE_FLOATS;
           const float* sa_hi = sd + TC_D_PIECE;
@@ -212,50 +272,65 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
 #pragma unroll
           for (int k = 0; k < TC_BK / 8; ++k) {
             // K step k: k-chunks 2k, 2k+1; LBO = stride between k-chunks
-            const uint32_t dofs = 2 * k * (TC_M * 4), aofs = 2 * k * (TC_N * 4);
+            const uint32_t dofs = 2 * k * (TC_M * 4), aofs = 2 * k * (TC_NH * 4);
             const uint64_t dd = umma_desc(sd + dofs, TC_M * 16, 128);
-            const uint64_t ah = umma_desc(sa_hi + aofs, TC_N * 16, 128);
-            const uint64_t al = umma_desc(sa_lo + aofs, TC_N * 16, 128);
-            tc_mma(acc, dd, ah, (kt | k) ? 1u : 0u);
-            tc_mma(acc, dd, al, 1u);
+            const uint64_t ah = umma_desc(sa_hi + aofs, TC_NH * 16, 128);
+            const uint64_t al = umma_desc(sa_lo + aofs, TC_NH * 16, 128);
+            tc_mma2(acc, dd, ah, (kt | k) ? 1u : 0u);
+            tc_mma2(acc, dd, al, 1u);
           }
-          tc_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+          tc_commit2(&empty[stage]);  // frees the slot in both CTAs when these MMAs finish
           if (++stage == TC_STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tfull[ab]);
+        tc_commit2(&tfull[ab]);
       }
+    } else if (lane == 0) {
+      // ---------------- relay (odd CTA): my stage landed -> leader ----------------
+      int stage = 0, phase = 0;
+      for (int ui = 0; ui < my_units; ++ui)
+        for (int kt = 0; kt < KT; ++kt) {
+          mbar_wait(&full[stage], (uint32_t)phase);
+          mbar_arrive_remote(&peer_full[stage], 0);
+          if (++stage == TC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
     }
   } else {
-    // ---------------- epilogue: thread = walk ----------------
-    const int q = warp & 3;              // TMEM lane quarter of this warp
-    const int wl = q * 32 + lane;        // walk within the tile
+    // ---------------- epilogue: thread = walk, warp = (lane quarter, row half) ----------------
+    const int q = warp & 3;                      // TMEM lane quarter this warp may access
+    const int rh = (warp - 2) / 4;               // which 128 of the unit's 256 rows
+    const int wl = q * 32 + lane;                // walk within this CTA's tile
     const uint64_t stream_policy = policy_evict_first();  // the slack stream must not evict A
+    const float eps = (float)p.eps_dir, mu = (float)p.margin;
     for (int ui = 0; ui < my_units; ++ui) {
-      int64_t rt, wt;
-      tc_unit(blockIdx.x + (int64_t)ui * gridDim.x, p, &rt, &wt);
+      int64_t rt, wp;
+      tc_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+      const int64_t wt = 2 * wp + rank;
       const int ab = ui & 1;
       mbar_wait(&tfull[ab], (uint32_t)((ui >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int64_t c = wt * TC_M + wl;
       const double th = p.theta_prev[c];
-      double hi = keyd(*(volatile long long*)(p.hi_key + c));
-      double lo = keyd(*(volatile long long*)(p.lo_key + c));
-      double viol = __longlong_as_double((long long)0xFFF0000000000000ULL);
+      float hi = __int_as_float(0x7F800000), lo = -hi, viol = -hi;
       unsigned sd = 0u;
       const int64_t sbase = (rt * p.walk_tiles + wt) * TC_N * TC_M + wl;
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * TC_N);
       const double* __restrict__ Sin = p.S + sbase;
-      const double* __restrict__ Rin = p.R + sbase;
+      const float* __restrict__ Rin = p.R + sbase;
       double* __restrict__ Sout = p.S + sbase;
-      double* __restrict__ Rout = p.R + sbase;
+      float* __restrict__ Rout = p.R + sbase;
       // 16 rows at a time: all loads of the group in flight before any store
-      // (the cache is read and rewritten in place; interleaving them would
-      // cost one DRAM latency per row)
+      // (the cache is read and rewritten in place).  Only the slack update is
+      // fp64; the ratio test runs on the fp32 pipes, branch-free -- the chord
+      // is already that of the body shrunk by mu >> fp32 rounding of s / ad.
       auto rows16 = [&](int r0, const float* vv) {
-        double so[16], ro[16];
+        double so[16];
+        float ro[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           so[j] = ld_policy(Sin + (int64_t)(r0 + j) * TC_M, stream_policy);
@@ -263,15 +338,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const double ad = (double)vv[j];
-          const double s = fma(-th, ro[j], so[j]);
+          const double s = fma(-th, (double)ro[j], so[j]);
           st_policy(Sout + (int64_t)(r0 + j) * TC_M, s, stream_policy);
-          st_policy(Rout + (int64_t)(r0 + j) * TC_M, ad, stream_policy);
-          viol = fmax(viol, -s);
-          scan_row(s - p.margin, ad, p.eps_dir, hi, lo, sd);
+          st_policy(Rout + (int64_t)(r0 + j) * TC_M, vv[j], stream_policy);
+          const float sf = (float)s, ad = vv[j];
+          viol = fmaxf(viol, -sf);
+          const float qt = __fdividef(sf - mu, ad);
+          const bool up = ad > eps, dn = ad < -eps;
+          sd |= (up ? 1u : 0u) | (dn ? 2u : 0u);
+          hi = up ? fminf(hi, qt) : hi;
+          lo = dn ? fmaxf(lo, qt) : lo;
         }
       };
-      for (int c0 = 0; c0 < TC_N; c0 += 32) {
+      for (int c0 = rh * (TC_N / 2); c0 < (rh + 1) * (TC_N / 2); c0 += 32) {
         float v[32];
         tc_ld32(taddr + (uint32_t)c0, v);
         rows16(c0, v);
@@ -279,9 +358,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[ab]);
+      if (lane == 0) {
+        if (rank == 0)
+          mbar_arrive(&tempty[ab]);
+        else
+          mbar_arrive_remote(&tempty[ab], 0);
+      }
       if (c < p.z) {
-        const long long vk = dkey(viol), hk = dkey(hi), lk = dkey(lo);
+        const long long vk = dkey((double)viol), hk = dkey((double)hi), lk = dkey((double)lo);
         if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
         if (hk < *(volatile long long*)(p.hi_key + c)) atomicMin(p.hi_key + c, hk);
         if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
@@ -290,9 +374,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) chord_tc32_kernel(const TcParam
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  __syncthreads();
+  cluster_sync_all();  // all MMAs done and consumed in both CTAs before TMEM is freed
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
 }
 
 // fp64 polytope rows -> (A_hi, A_lo) with A_used = A_hi + A_lo written back

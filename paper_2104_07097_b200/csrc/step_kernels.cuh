@@ -409,10 +409,11 @@ __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
           ad = fma(a, ds[k], ad);
         }
         const double sl = rp.b[r] - ax;
-        if (rp.R)
-          rp.R[rp.tc_walk_tiles > 0
-                   ? (((r / 256) * rp.tc_walk_tiles + c / 128) * 256 + r % 256) * 128 + c % 128
-                   : s_index(r, c, rp.ct64)] = ad;
+        if (rp.R && rp.tc_walk_tiles > 0)  // fp32 variant: fp32 rate cache, tc_s_index
+          reinterpret_cast<float*>(rp.R)[(((r / 256) * rp.tc_walk_tiles + c / 128) * 256 +
+                                          r % 256) * 128 + c % 128] = (float)ad;
+        else if (rp.R)
+          rp.R[s_index(r, c, rp.ct64)] = ad;
         if (ad > rp.eps_dir) {
           pos = 1.0;
           thi = fmin(thi, sl / ad);
