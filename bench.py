@@ -46,6 +46,25 @@ def fp64_peak():
     return best
 
 
+NCU_FILE = os.path.join(ROOT, "profiles", "ncu_full_r01.json")
+
+
+def ncu_traffic(capture: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum, GB)
+    of the dominant kernel from the committed `ncu --set full` capture
+    (tools/ncu_capture.sh), or None."""
+    try:
+        with open(NCU_FILE) as f:
+            d = json.load(f)[capture]
+        scale = {"Gbyte": 1.0, "Mbyte": 1e-3, "Tbyte": 1e3}
+        tot = 0.0
+        for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            tot += float(d[k]["value"]) * scale[d[k]["unit"]]
+        return tot
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def tf32_dense_peak():
     """TF32 tensor-core peak: the driver-measured dense bf16 GEMM rate
     (MEASURED_PEAKS.json) halved -- TF32 runs at half the bf16 rate on
@@ -373,6 +392,8 @@ def run_engine(args, world, rank, local):
                 "kernel": "chord_tc32_kernel (tcgen05.mma kind::tf32, TMEM, bulk-copy ring)",
                 "roofline": {"bound": "tensor", "achieved": tf32_exec, "peak": tf32_peak,
                              "unit": "TFLOP/s (TF32 executed)", "frac": tf32_exec / tf32_peak,
+                             "traffic": ncu_traffic("tc32_full"),
+                             "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
                              "peak_source": "MEASURED_PEAKS.json bf16 dense / 2"},
                 "all_inside_eps_feas": bool(bad32 == -1)}
 
@@ -397,7 +418,12 @@ def run_engine(args, world, rank, local):
                    "parallelism": f"walk-sharded x{world}",
                    "l2": "inputs larger than L2 (A_I is %.1f GB)" % (p.a_in.nbytes / 1e9)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak if peak else None, "traffic": None,
+                     "frac": achieved / peak if peak else None,
+                     "traffic": ncu_traffic("chord2_full"),
+                     "traffic_unit": "GB DRAM read+write per launch (ncu --set full, "
+                                     "profiles/ncu_full_r01.json)",
+                     "algorithmic_bytes_GB": (p.a_in.nbytes + 4 * 8 * z * p.num_inequalities()
+                                              + 8 * z * p.dim()) / 1e9,
                      "kernel": "chord_kernel (DMMA A_I [X|D] / A_I D + fused chord reduce)",
                      "avg_launch_ms": chord_avg_ms, "launches": st["chord_timed"],
                      "peak_source": "fp64 DMMA microbench, profiles/fp64_peaks_r01.json"},
@@ -422,6 +448,7 @@ def run_engine(args, world, rank, local):
                                  "unit": "TFLOP/s (TF32 executed)",
                                  "frac": 2.0 * achieved / tf32_dense_peak(),
                                  "kernel": "chord_tc32_kernel",
+                                 "traffic": ncu_traffic("tc32_full"),
                                  "peak_source": "MEASURED_PEAKS.json bf16 dense / 2"})
     print(json.dumps(line), flush=True)
 
@@ -440,7 +467,7 @@ def main():
     ap.add_argument("--reproject", type=int, default=1000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-walks", type=int, default=256)
-    ap.add_argument("--cpu-iters", type=int, default=2)
+    ap.add_argument("--cpu-iters", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-variant measurement")
     ap.add_argument("--sweep-z", default="",
