@@ -65,6 +65,24 @@ def ncu_traffic(capture: str):
         return None
 
 
+I8_MMAS_PER_KSTEP = 34  # slice-pair products per k step (chord_i8.cuh)
+
+
+def int8_dense_peak():
+    """Dense int8 tensor-core peak on this pool's B200: the best tcgen05
+    kind::i8 rate of the MMA-only microbenchmark (tools/i8_probe.cu,
+    profiles/int8_probe_r01.jsonl); fallback 4500 TOPS (nominal)."""
+    best = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_probe_r01.jsonl")) as f:
+            for line in f:
+                v = json.loads(line).get("int8_tops")
+                best = v if best is None else max(best, v)
+    except (OSError, ValueError):
+        pass
+    return best or 4500.0
+
+
 def tf32_dense_peak():
     """TF32 tensor-core peak: the driver-measured dense bf16 GEMM rate
     (MEASURED_PEAKS.json) halved -- TF32 runs at half the bf16 rate on
@@ -311,7 +329,7 @@ def run_engine(args, world, rank, local):
     reproject = args.reproject if p.num_equalities() else 0
     eng = mh.Engine(p, z, seed=args.seed, projector=projector, slack=args.slack,
                     refresh_every=args.refresh, device=local, chain_offset=rank * z,
-                    precision=args.precision)
+                    precision=args.precision, f64_engine=args.f64_engine)
     X0 = np.zeros((p.dim(), z), order="F")
     X0[:] = w.x0[:, None]
     eng.set_state(X0)
@@ -367,6 +385,36 @@ def run_engine(args, world, rank, local):
     achieved = st["chord_flops"] / max(st["chord_ms"] * 1e-3, 1e-30) / 1e12
     peak = fp64_peak()
     eng.close()
+
+    # the int8-slice fp64 engine (Ozaki scheme on the tcgen05 int8 tensor cores)
+    # on the same workload: fp64-accurate rates, reported beside the DMMA line
+    i8 = None
+    if args.precision == 64 and not args.no_i8 and p.dim() <= 4608:
+        e8 = mh.Engine(p, z, seed=args.seed, projector=projector, refresh_every=args.refresh,
+                       device=local, chain_offset=rank * z, f64_engine="int8")
+        e8.set_state(X0)
+        e8.step_timed(args.warmup, reproject)
+        e8.reset_stats()
+        e8.set_timing(True)
+        barrier(world)
+        ms8 = max_over_ranks(e8.step_timed(args.steps, reproject), world)
+        s8 = e8.stats()
+        bad8, viol8, _ = e8.check_state(e8.eps_feas)
+        e8.close()
+        alg8 = s8["chord_flops"] / max(s8["chord_ms"] * 1e-3, 1e-30) / 1e12
+        ops8 = I8_MMAS_PER_KSTEP * alg8  # int8 tensor ops executed (34 slice-pair products)
+        i8_peak = int8_dense_peak()
+        i8 = {"value": z * world * args.steps / (ms8 * 1e-3), "unit": "chain-steps/s",
+              "ms_per_step": ms8 / args.steps,
+              "dtype": "f64 results: A_I and d as 53-bit fixed point in 7 int8 slices, exact "
+                       "int32 slice products (levels 0..7), fp64 combine; slack and walks f64",
+              "kernel": "chord_i8_kernel (tcgen05.mma kind::i8, CTA pair, 8 TMEM level accumulators)",
+              "fp64_equivalent_tflops": alg8, "fp64_equivalent_frac_of_dmma_peak": alg8 / peak,
+              "roofline": {"bound": "tensor", "achieved": ops8, "peak": i8_peak,
+                           "unit": "TOPS (int8 executed)", "frac": ops8 / i8_peak,
+                           "traffic": ncu_traffic("i8_full"),
+                           "peak_source": "tcgen05 kind::i8 microbench, profiles/int8_probe_r01.jsonl"},
+              "all_inside_eps_feas": bool(bad8 == -1)}
 
     # the north star's fp32 variant on the same workload (A_I rounded to fp32,
     # rates on tcgen05 tensor cores): same timing protocol, reported beside
@@ -442,6 +490,8 @@ def run_engine(args, world, rank, local):
         line["cpu_baseline"] = cpu
     if fp32:
         line["fp32_variant"] = fp32
+    if i8:
+        line["fp64_int8_variant"] = i8
     if args.precision == 32:
         line["dtype"] = "f32 rates (tcgen05 TF32 split), f64 slack/state"
         line["roofline"].update({"achieved": 2.0 * achieved, "peak": tf32_dense_peak(),
@@ -470,6 +520,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-variant measurement")
+    ap.add_argument("--no-i8", action="store_true", help="skip the int8-slice fp64 engine")
+    ap.add_argument("--f64-engine", default="dmma", choices=["dmma", "int8"],
+                    help="engine of the headline fp64 line (default: DMMA)")
     ap.add_argument("--sweep-z", default="",
                     help="comma-separated walk counts: padding sweep instead of the bench line")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],

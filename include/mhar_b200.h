@@ -100,7 +100,15 @@ typedef struct {
                             fp32, rates A_I d on tcgen05 tensor cores (3xTF32, fp32 accuracy),
                             fp64 slack/state, chords of {A_I x <= b_I - fp32_margin} */
   double fp32_margin;    /* precision 32: slack margin mu (0 = default 1e-6) */
+  int f64_engine;        /* precision 64 only.  MHAR_F64_DMMA (default): A_I d on the fp64
+                            tensor cores (DMMA).  MHAR_F64_INT8: A_I d formed exactly from
+                            53-bit fixed-point operands split into int8 slices on the
+                            tcgen05 int8 tensor cores (Ozaki scheme, fp64-accurate rates,
+                            n <= 4608); refreshes and containment checks stay on DMMA */
 } mhar_options;
+
+#define MHAR_F64_DMMA 0
+#define MHAR_F64_INT8 1
 
 /* Fills o with the reference defaults (sampler.hpp:16-25): eps_dir 1e-11,
  * eps_feas 1e-9, Philox, incremental slack, device 0. */
@@ -124,6 +132,10 @@ int mhar_get_state(mhar_ctx* ctx, double* x);
  * (the sample layout of SampleSet::samples, sampler.hpp:83); used to gather
  * samples across ranks without a host round trip. */
 int mhar_get_state_rows_device(mhar_ctx* ctx, double* dev_rows);
+/* Test hook: the last iterate's directions D (n x z column-major, as moved
+ * along -- quantised by the int8-slice engine) and chord bounds / positions
+ * (z each).  Any pointer may be NULL. */
+int mhar_debug_last_iterate(mhar_ctx* ctx, double* d, double* lower, double* upper, double* theta);
 
 /* `iters` iterates of every walk (step(), sampler.cpp:235-272).  When the
  * polytope has equalities and reproject_every > 0, walks are pulled back onto

@@ -46,6 +46,8 @@ RNG_PHILOX = 0
 RNG_REFERENCE = 1
 SLACK_RECOMPUTE = 0
 SLACK_INCREMENTAL = 1
+F64_DMMA = 0
+F64_INT8 = 1
 
 
 class ErrorCode:
@@ -96,7 +98,8 @@ class _Options(C.Structure):
     _fields_ = [("z", C.c_int64), ("chain_offset", C.c_int64), ("seed", C.c_uint64),
                 ("eps_dir", C.c_double), ("eps_feas", C.c_double), ("rng", C.c_int),
                 ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int),
-                ("small_path", C.c_int), ("precision", C.c_int), ("fp32_margin", C.c_double)]
+                ("small_path", C.c_int), ("precision", C.c_int), ("fp32_margin", C.c_double),
+                ("f64_engine", C.c_int)]
 
 
 class _RunConfig(C.Structure):
@@ -130,7 +133,7 @@ EXPORTED_SYMBOLS = [
     "mhar_compute_projection", "mhar_get_stats", "mhar_set_timing", "mhar_reset_stats",
     "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
     "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
-    "mhar_select_points", "mhar_chebyshev_center",
+    "mhar_select_points", "mhar_chebyshev_center", "mhar_debug_last_iterate",
 ]
 
 
@@ -168,6 +171,8 @@ def lib():
     L.mhar_set_state.argtypes = [C.c_void_p, _dp]
     L.mhar_get_state.argtypes = [C.c_void_p, _dp]
     L.mhar_get_state_rows_device.argtypes = [C.c_void_p, C.c_void_p]
+    L.mhar_debug_last_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
+    L.mhar_debug_last_iterate.restype = C.c_int
     L.mhar_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
     L.mhar_sync.argtypes = [C.c_void_p]
     L.mhar_step_timed.argtypes = [C.c_void_p, C.c_int64, C.c_int64, _dp]
@@ -363,14 +368,17 @@ class Engine:
     streams: column stream k and the shared theta stream, rng.hpp:42-55).
     slack: "incremental" (default) or "recompute" (one fused A_I[X|D] pass
     per iterate).  small_path: allow the walk-resident kernel for bodies that
-    fit in shared memory (Philox only).
+    fit in shared memory (Philox only).  f64_engine (precision 64): "dmma"
+    (default, fp64 tensor cores) or "int8" (A_I d formed exactly from 53-bit
+    fixed-point operands split into int8 slices on the tcgen05 int8 tensor
+    cores -- the Ozaki scheme; n <= 4608; refreshes and checks stay DMMA).
     """
 
     def __init__(self, p: Polytope, z: int, seed: int = 0, projector: Optional[ProjectionOperator] = None,
                  eps_dir: float = 1e-11, eps_feas: float = 1e-9, rng: str = "philox",
                  slack: str = "incremental", refresh_every: int = 128, device: int = 0,
                  chain_offset: int = 0, small_path: bool = True, precision: int = 64,
-                 fp32_margin: float = 0.0):
+                 fp32_margin: float = 0.0, f64_engine: str = "dmma"):
         L = lib()
         self.p = p
         self.n = p.dim()
@@ -399,7 +407,9 @@ class Engine:
         opt.small_path = 1 if small_path else 0
         opt.precision = int(precision)
         opt.fp32_margin = float(fp32_margin)
+        opt.f64_engine = {"dmma": F64_DMMA, "int8": F64_INT8}[f64_engine]
         self.precision = int(precision)
+        self.f64_engine = f64_engine
         P = G = None
         if projector is not None:
             P = _f(projector.p)
@@ -496,6 +506,13 @@ class Engine:
         _check(lib().mhar_lambda_intervals(self._h, _d(X), _d(D), _d(lo), _d(hi),
                                            fl.ctypes.data_as(_u8p)))
         return LambdaIntervals(lo, hi, (fl & FLAG_DEGENERATE).astype(np.uint8), fl)
+
+    def debug_last_iterate(self):
+        """Test hook: (D n x z, lower, upper, theta) of the last iterate."""
+        d = np.empty((self.n, self.z), order="F")
+        lo, hi, th = np.empty(self.z), np.empty(self.z), np.empty(self.z)
+        _check(lib().mhar_debug_last_iterate(self._h, _d(d), _d(lo), _d(hi), _d(th)))
+        return d, lo, hi, th
 
     def check_state(self, eps: float):
         """(first_bad or -1, max_i (A x - b)_i per walk, max |A_E x - b_E| per walk)."""

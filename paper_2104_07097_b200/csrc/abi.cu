@@ -25,6 +25,7 @@
 #include "step_kernels.cuh"
 #include "small_kernel.cuh"
 #include "chord_tc32.cuh"
+#include "chord_i8.cuh"
 #include "stats_kernels.cuh"
 
 using namespace mhar_dev;
@@ -95,6 +96,12 @@ struct mhar_ctx {
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
   int tc_group_n = 1;   // tc32 rasterisation band (row tiles); MHAR_TC_GROUP overrides
   int tc_a_policy = 0;  // L2 policy of the tc32 A stream (evict_normal); MHAR_TC_APOL overrides
+  int64_t cache_rows = 0;  // row tile of the tcgen05 cache layout (256 tc32, 64 int8)
+  // int8-slice fp64 engine (chord_i8.cuh)
+  uint8_t *A8 = nullptr, *D8 = nullptr;
+  double *rsc = nullptr, *csc = nullptr;
+  int* rexp = nullptr;
+  int64_t KS = 0, i8_row_tiles = 0;
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
   double* rows2 = nullptr;
   double* pinned[2] = {nullptr, nullptr};
@@ -129,6 +136,16 @@ int dalloc(mhar_ctx* c, T** p, size_t count) {
   if (e != cudaSuccess)
     return fail(MHAR_ERR_CUDA, "cudaMalloc(" + std::to_string(bytes) + " B): " +
                                    cudaGetErrorString(e));
+  // Fresh allocations start zeroed; MHAR_POISON=<hex mask> instead fills the
+  // allocations whose creation index is in the mask with 0xFF (NaN) bytes --
+  // a debugging aid that exposes reads of never-written device memory.
+  static const unsigned long long poison = [] {
+    const char* e = std::getenv("MHAR_POISON");
+    return e ? std::strtoull(e, nullptr, 16) : 0ull;
+  }();
+  const size_t idx = c->allocs.size();
+  const bool bad = idx < 64 && ((poison >> idx) & 1ull);
+  cudaMemsetAsync(q, bad ? 0xFF : 0, bytes, c->stream);
   c->allocs.push_back(q);
   *p = static_cast<T*>(q);
   return 0;
@@ -202,6 +219,8 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   p.eps_dir = c->opt.eps_dir;
   p.group_m = c->group_m;
   p.tc_walk_tiles = c->tc_walk_tiles;
+  p.cache_rows = c->cache_rows;
+  p.rate_f32 = c->Ahi != nullptr;
   return p;
 }
 
@@ -282,6 +301,54 @@ int launch_tc32(mhar_ctx* c) {
   return 0;
 }
 
+// int8-slice fp64 engine: incremental chord with exact slice products.
+int launch_i8(mhar_ctx* c) {
+  I8Params p;
+  p.A8 = c->A8;
+  p.rsc = c->rsc;
+  p.D8 = c->D8;
+  p.csc = c->csc;
+  p.S = c->S;
+  p.R = c->R;
+  p.theta_prev = c->theta;
+  p.hi_key = c->hi_key;
+  p.lo_key = c->lo_key;
+  p.viol_key = c->viol_key;
+  p.sides = c->sides;
+  p.err = c->err;
+  p.row_tiles = c->i8_row_tiles;
+  p.walk_tiles = c->tc_walk_tiles;
+  p.KS = c->KS;
+  p.z = c->z;
+  p.eps_dir = c->opt.eps_dir;
+  const int64_t units = p.row_tiles * (p.walk_tiles / 2);
+  const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (c->timing) {
+    ev = take_events(c);
+    cudaEventRecord(ev.first, c->stream);
+  }
+  chord_i8_kernel<<<grid, I8_THREADS, I8_SMEM, c->stream>>>(p);
+  if (cudaPeekAtLastError() != cudaSuccess) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, chord_i8_kernel);
+    const cudaError_t e = cudaGetLastError();
+    return fail(MHAR_ERR_CUDA, std::string("chord_i8_kernel: ") + cudaGetErrorString(e) +
+                                   " (regs " + std::to_string(fa.numRegs) + ", max threads " +
+                                   std::to_string(fa.maxThreadsPerBlock) + ", local " +
+                                   std::to_string(fa.localSizeBytes) + " B, max dyn smem " +
+                                   std::to_string(fa.maxDynamicSharedSizeBytes) + ")");
+  }
+  LAUNCH_OK(c, "chord_i8_kernel");
+  ++c->chord_launches;
+  if (c->timing) {
+    cudaEventRecord(ev.second, c->stream);
+    c->pending.push_back(ev);
+    c->pending_flops.push_back(2.0 * (double)c->m * (double)c->n * (double)c->z);
+  }
+  return 0;
+}
+
 int launch_finalize(mhar_ctx* c, bool queue_redraws, bool advance_streams) {
   FinalizeParams fp;
   fp.hi_key = c->hi_key;
@@ -341,6 +408,8 @@ int launch_redraw(mhar_ctx* c) {
   rp.R = (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) ? c->R : nullptr;
   rp.ct64 = c->ct64;
   rp.tc_walk_tiles = c->tc_walk_tiles;
+  rp.cache_rows = c->cache_rows;
+  rp.rate_f32 = c->Ahi != nullptr;
   rp.scratch = c->redraw_scratch;
   rp.lower = c->lower;
   rp.upper = c->upper;
@@ -448,7 +517,23 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
         c->D, c->n, c->z_pad, c->KT, c->Dhi, c->err);
     LAUNCH_OK(c, "tc_split_d_kernel");
   }
-  if (c->Ahi && injected) {
+  if (c->A8) {
+    // int8-slice engine: per-walk fixed point, slices; D becomes the quantised direction
+    i8_split_d_kernel<<<(unsigned)c->ct64, 256, 0, c->stream>>>(c->D, c->n, c->KT, c->KS, c->D8,
+                                                                 c->csc, c->err);
+    LAUNCH_OK(c, "i8_split_d_kernel");
+  }
+  if (c->A8 && injected) {
+    // test hook: exact fp64 slack of X into the cache, then the slice rates with theta = 0
+    if ((s = launch_chord(c, FUSED_STORE, c->X))) return s;
+    fill_keys_kernel<<<blocks_for(c->z_pad, 256, 1 << 20), 256, 0, c->stream>>>(
+        c->hi_key, c->lo_key, c->viol_key, c->sides, c->z_pad);
+    LAUNCH_OK(c, "fill_keys_kernel");
+    CK(cudaMemsetAsync(c->theta, 0, sizeof(double) * c->z_pad, c->stream));
+    s = launch_i8(c);
+  } else if (c->A8 && mode == INCREMENTAL) {
+    s = launch_i8(c);
+  } else if (c->Ahi && injected) {
     // test hook of the fp32 path: exact fp64 slack of X into the cache, the
     // chord of that pass discarded, then the tensor-core rates with theta = 0
     if ((s = launch_chord(c, FUSED_STORE, c->X))) return s;
@@ -627,10 +712,17 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   if (opt->precision != 0 && opt->precision != 32 && opt->precision != 64)
     return fail(MHAR_ERR_INVALID_ARGUMENT, "options: precision must be 64 or 32");
 
+  if (opt->f64_engine != MHAR_F64_DMMA && opt->f64_engine != MHAR_F64_INT8)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "options: unknown f64_engine");
+  const bool i8 = opt->f64_engine == MHAR_F64_INT8 && opt->precision != 32;
+  if (i8 && round_up(p->n, I8_BK) > I8_MAX_K)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "options: the int8-slice engine needs n <= 4608");
+
   mhar_ctx* c = new mhar_ctx();
   c->opt = *opt;
   const bool fp32 = opt->precision == 32;
-  if (fp32) {
+  const bool tiles = fp32 || i8;  // tcgen05 kernels: CTA-pair walk tiles, tile cache layout
+  if (tiles) {
     // the fp32 variant is the incremental tensor-core path (fp64 refreshes)
     c->opt.slack_mode = MHAR_SLACK_INCREMENTAL;
     c->opt.small_path = 0;
@@ -659,11 +751,16 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   c->KT = c->n_pad / BK;
   c->m_pad = round_up(c->m, fp32 ? TC_N : BM);
   c->m_tiles = c->m_pad / BM;
-  c->z_pad = round_up(c->z, fp32 ? 2 * TC_M : 64);  // fp32: whole CTA-pair walk tiles
+  c->z_pad = round_up(c->z, tiles ? 2 * TC_M : 64);  // tcgen05: whole CTA-pair walk tiles
   c->ct64 = c->z_pad / 64;
-  if (fp32) {
+  if (tiles) {
     c->tc_row_tiles = c->m_pad / TC_N;
     c->tc_walk_tiles = c->z_pad / TC_M;
+    c->cache_rows = fp32 ? TC_N : I8_N;
+  }
+  if (i8) {
+    c->KS = round_up(c->n, I8_BK) / I8_BK;
+    c->i8_row_tiles = c->m_pad / I8_N;
   }
   c->p_rows_pad = round_up(c->n, BM);
 
@@ -695,7 +792,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     if (2 * cache * sizeof(double) + (1ull << 30) > free_b) {
-      if (fp32) return bail(fail(MHAR_ERR_CUDA, "precision 32: not enough HBM for the slack cache"));
+      if (tiles) return bail(fail(MHAR_ERR_CUDA, "tcgen05 engine: not enough HBM for the slack cache"));
       c->opt.slack_mode = MHAR_SLACK_RECOMPUTE;  // not enough HBM for the slack cache
     } else if ((st = dalloc(c, &c->S, cache)) || (st = dalloc(c, &c->R, cache))) {
       return bail(st);
@@ -707,7 +804,11 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     double* tmp = nullptr;
     e = cudaMalloc(&tmp, sizeof(double) * (size_t)c->m * c->n);
     if (e != cudaSuccess) return bail(fail(MHAR_ERR_CUDA, "cudaMalloc(A staging) failed"));
-    cudaMemcpy(tmp, p->a_in, sizeof(double) * (size_t)c->m * c->n, cudaMemcpyHostToDevice);
+    // H2D copies are ordered on the context's (non-blocking) stream: a legacy-stream
+    // cudaMemcpy from pageable memory may return before its DMA lands and would
+    // race the packing kernels below
+    cudaMemcpyAsync(tmp, p->a_in, sizeof(double) * (size_t)c->m * c->n, cudaMemcpyHostToDevice,
+                    c->stream);
     const int64_t total = c->m_pad * c->KT * BK;
     pack_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
         tmp, c->m, c->n, c->m, c->m_pad, c->KT, c->A);
@@ -729,6 +830,27 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaFuncSetAttribute(chord_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TC_SMEM);
     }
+    if (i8) {
+      // A_I as 7 int8 slices of its per-row 53-bit fixed point
+      const size_t an = (size_t)I8_SLICES * c->m_pad * c->KS * I8_BK;
+      const size_t dn = (size_t)I8_SLICES * c->z_pad * c->KS * I8_BK;
+      if ((st = dalloc(c, &c->A8, an)) || (st = dalloc(c, &c->D8, dn)) ||
+          (st = dalloc(c, &c->rsc, c->m_pad)) || (st = dalloc(c, &c->csc, c->z_pad)) ||
+          (st = dalloc(c, &c->rexp, c->m_pad))) {
+        cudaFree(tmp);
+        return bail(st);
+      }
+      i8_row_scale_kernel<<<blocks_for(c->m_pad, 256, c->num_sms * 8), 256, 0, c->stream>>>(
+          tmp, c->m, c->n, c->m_pad, c->rexp, c->rsc);
+      const int64_t groups = c->m_pad * c->KS * (I8_BK / 16);
+      i8_split_a_kernel<<<blocks_for(groups, 256, c->num_sms * 32), 256, 0, c->stream>>>(
+          tmp, c->m, c->n, c->m_pad, c->KS, c->rexp, c->A8);
+      c->launches += 2;
+      cudaMemsetAsync(c->D8, 0, dn, c->stream);
+      cudaStreamSynchronize(c->stream);
+      cudaFuncSetAttribute(chord_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)I8_SMEM);
+    }
     // small bodies: keep the column-major copy for the walk-resident kernel
     c->small_ns = (int)(c->n | 1);
     const size_t small_bytes =
@@ -742,7 +864,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     }
     std::vector<double> bp(c->m_pad, __builtin_huge_val());
     std::memcpy(bp.data(), p->b_in, sizeof(double) * c->m);
-    cudaMemcpy(c->b, bp.data(), sizeof(double) * c->m_pad, cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(c->b, bp.data(), sizeof(double) * c->m_pad, cudaMemcpyHostToDevice, c->stream);
+    cudaStreamSynchronize(c->stream);  // bp is a local
   }
   if (c->me > 0) {
     std::vector<double> P((size_t)c->n * c->n), G((size_t)c->me * c->me);
@@ -761,10 +884,11 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         (st = dalloc(c, &c->eqres, (size_t)c->me * c->z)) ||
         (st = dalloc(c, &c->eqg, (size_t)c->me * c->z)))
       return bail(st);
-    cudaMemcpy(c->Pcm, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice);
-    cudaMemcpy(c->AE, p->a_eq, sizeof(double) * c->me * c->n, cudaMemcpyHostToDevice);
-    cudaMemcpy(c->bE, p->b_eq, sizeof(double) * c->me, cudaMemcpyHostToDevice);
-    cudaMemcpy(c->G, G.data(), sizeof(double) * G.size(), cudaMemcpyHostToDevice);
+    cudaMemcpyAsync(c->Pcm, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->AE, p->a_eq, sizeof(double) * c->me * c->n, cudaMemcpyHostToDevice,
+                    c->stream);
+    cudaMemcpyAsync(c->bE, p->b_eq, sizeof(double) * c->me, cudaMemcpyHostToDevice, c->stream);
+    cudaMemcpyAsync(c->G, G.data(), sizeof(double) * G.size(), cudaMemcpyHostToDevice, c->stream);
     const int64_t total = c->p_rows_pad * c->KT * BK;
     pack_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
         c->Pcm, c->n, c->n, c->n, c->p_rows_pad, c->KT, c->Ppk);
@@ -864,6 +988,22 @@ int mhar_get_state(mhar_ctx* c, double* x) {
       c->X, c->n, c->z, c->KT, c->rows);
   LAUNCH_OK(c, "unpack_b_kernel");
   CK(cudaMemcpyAsync(x, c->rows, sizeof(double) * c->n * c->z, cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int mhar_debug_last_iterate(mhar_ctx* c, double* d, double* lower, double* upper, double* theta) {
+  if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "debug_last_iterate: null context");
+  CK(cudaSetDevice(c->device));
+  if (d) {
+    unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->D, c->n, c->z, c->KT, c->rows);
+    LAUNCH_OK(c, "unpack_b_kernel");
+    CK(cudaMemcpyAsync(d, c->rows, sizeof(double) * c->n * c->z, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (lower) CK(cudaMemcpyAsync(lower, c->lower, sizeof(double) * c->z, cudaMemcpyDeviceToHost, c->stream));
+  if (upper) CK(cudaMemcpyAsync(upper, c->upper, sizeof(double) * c->z, cudaMemcpyDeviceToHost, c->stream));
+  if (theta) CK(cudaMemcpyAsync(theta, c->theta, sizeof(double) * c->z, cudaMemcpyDeviceToHost, c->stream));
   CK(cudaStreamSynchronize(c->stream));
   return 0;
 }

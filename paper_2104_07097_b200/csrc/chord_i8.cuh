@@ -1,0 +1,520 @@
+// chord_i8.cuh -- fp64-accurate rates A_I d on the int8 tensor cores
+// (tcgen05.mma kind::i8), the "int8 slice" engine of the incremental chord.
+//
+// Same computation as chord2_kernel<INCREMENTAL> (compute_lambda_intervals,
+// /root/reference/proj/src/sampler.cpp:150-208, slack carried incrementally),
+// but the product A_I d is formed EXACTLY from 53-bit fixed-point operands
+// split into int8 slices (the Ozaki scheme):
+//
+//   a_rk = 2^(e_r - 52) v_rk,   v = s0 2^48 + s1 2^40 + ... + s6        (|v| <= 2^52)
+//   d_kc = 2^(f_c - 52) w_kc,   w = t0 2^48 + t1 2^40 + ... + t6
+//
+// with s0, t0 signed in [-16, 16] and s1..s6, t1..t6 unsigned bytes; e_r / f_c
+// are the exponents of the row / walk maxima, so v and w are the operands
+// rounded to 53 bits relative to their row (walk) maximum -- exactly
+// representable fp64 values.  Then
+//
+//   a . d = 2^(e_r + f_c - 8) sum_l 2^(-8 l) L_l,   L_l = sum_{i+j=l} sum_k s_i t_j
+//
+// and each level L_l is an exact int32 tensor-core accumulation (|L_l| <
+// 7 * 255^2 * K < 2^31 for K <= 4608).  Levels 0..7 are kept (34 slice-pair
+// MMAs per k step); the dropped levels weigh <= 2^-56 of max|a| max|d| per
+// term, below fp64 rounding of the product.  The walk moves along the
+// quantised direction (D is replaced by 2^(f_c-52) w), so the cached rates are
+// exactly the rates of the direction taken.
+//
+// CTA pair (cluster of 2, cta_group::2): one MMA is M = 256 walks (128 per CTA,
+// on each CTA's TMEM lanes) x N = 128 rows x K = 32.  An MMA with N < 128 costs
+// as much as one with N = 128 (measured, tools/i8_probe.cu), so the unit is
+// 128 rows and the 8 levels are accumulated in TWO passes over k, four level
+// accumulators (4 x 128 = all 512 TMEM columns) at a time:
+//   pass 0: levels 0..3 -- slices 0..3 of both operands, 10 MMAs per k step;
+//   pass 1: levels 4..7 -- slices 0..6, 24 MMAs per k step.
+// Each CTA stages its own 128 walks' direction slices (4 KB each) and one half
+// (64 rows) of the row tile's A slices (2 KB each) per k step.  The epilogue
+// drains pass 0 into a per-thread fp64 partial (registers), releases TMEM to
+// pass 1, then combines pass 1, releases TMEM to the next unit and runs the
+// slack update and chord scan of chord2_kernel<INCREMENTAL> (fp64, exact
+// division filter) while the tensor cores work on.
+//
+// Warp roles (320 threads per CTA): warp 0 lane 0 = bulk-copy producer;
+// warp 1 = TMEM allocation, lane 0 = MMA issuer (even CTA) / stage relay (odd
+// CTA); warps 2..9 = epilogue (lane quarter = warp % 4, two warps per quarter
+// splitting the 128 rows).
+#pragma once
+
+#include "chord_tc32.cuh"
+#include "common.cuh"
+
+namespace mhar_dev {
+
+constexpr int I8_M = 128;       // walks per CTA (unit: 2 x 128)
+constexpr int I8_N = 128;       // rows per unit
+constexpr int I8_NH = 64;       // rows staged by each CTA of the pair
+constexpr int I8_BK = 32;       // k per stage (one MMA k step)
+constexpr int I8_SLICES = 7;    // 5-bit signed top slice + 6 unsigned bytes = 53 bits
+constexpr int I8_LEVELS = 8;    // slice-pair levels i + j = 0..7
+constexpr int I8_PASS_LEVELS = 4;  // level accumulators live per pass (4 x 128 TMEM columns)
+constexpr int I8_D_PIECE = I8_M * I8_BK;   // bytes per direction slice piece (4 KB)
+constexpr int I8_A_PIECE = I8_NH * I8_BK;  // bytes per A slice half piece (2 KB)
+constexpr int I8_D_STAGE = I8_SLICES * I8_D_PIECE;            // 28 KB
+constexpr int I8_STAGE = I8_SLICES * (I8_D_PIECE + I8_A_PIECE);  // 42 KB
+constexpr int I8_STAGES = 5;
+constexpr int I8_EPI_WARPS = 8;
+constexpr int I8_THREADS = 64 + 32 * I8_EPI_WARPS;
+constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 512;
+constexpr int64_t I8_MAX_K = 4608;  // keeps every level accumulator inside int32
+constexpr int I8_ROWS_PER_WARP = I8_N / 2;
+constexpr int I8_MMAS = 34;         // slice-pair products per k step (10 + 24)
+
+// slices a pass needs of each operand: pass 0 -> 0..3, pass 1 -> 0..6
+__host__ __device__ constexpr int i8_pass_slices(int pass) { return pass == 0 ? 4 : I8_SLICES; }
+
+// Interleaved K-major ("no swizzle") core-matrix layout of one (tile, k step)
+// slice piece of R rows, in bytes: [k_chunk(16 B)][row_group(8 rows)][row(8)][16].
+__host__ __device__ inline int64_t i8_piece_index(int64_t r, int64_t kk, int64_t R) {
+  return ((kk >> 4) * (R >> 3) + (r >> 3)) * 128 + (r & 7) * 16 + (kk & 15);
+}
+// direction slice s of (walk c, coordinate k): [walk_tile(128)][k_step][slice][piece]
+__host__ __device__ inline int64_t i8_d_index(int64_t c, int64_t k, int s, int64_t KS) {
+  return (((c / I8_M) * KS + k / I8_BK) * I8_SLICES + s) * I8_D_PIECE +
+         i8_piece_index(c % I8_M, k % I8_BK, I8_M);
+}
+// A slice s of (row r, coordinate k): [row_tile(128)][k_step][half(64 rows)][slice][piece]
+__host__ __device__ inline int64_t i8_a_index(int64_t r, int64_t k, int s, int64_t KS) {
+  return ((((r / I8_N) * KS + k / I8_BK) * 2 + (r % I8_N) / I8_NH) * I8_SLICES + s) * I8_A_PIECE +
+         i8_piece_index(r % I8_NH, k % I8_BK, I8_NH);
+}
+// slack / rate cache of this tile: [row_tile(128)][walk_tile(128)][row(128)][walk(128)]
+__host__ __device__ inline int64_t i8_s_index(int64_t r, int64_t c, int64_t WT) {
+  return tile_cache_index(r, c, WT, I8_N);
+}
+
+// exponent e with max < 2^e (0 for an all-zero row / walk)
+__device__ inline int i8_exponent(double mx) { return mx > 0.0 ? ilogb(mx) + 1 : 0; }
+
+// 53-bit fixed point w = rint(x 2^(52 - e)) and its 7 slices (top signed)
+__device__ inline long long i8_fixed(double x, int e) { return __double2ll_rn(ldexp(x, 52 - e)); }
+__device__ inline uint8_t i8_slice(long long w, int s) {
+  return s == 0 ? (uint8_t)(int8_t)(w >> 48) : (uint8_t)((w >> (48 - 8 * s)) & 255);
+}
+
+// instruction descriptor: S32 accumulate, A (walks) / B (rows) int8 with the
+// signedness of the slice (top slice signed), K-major, M = 256 (pair), N = 128
+__host__ __device__ constexpr uint32_t i8_idesc(int a_signed, int b_signed) {
+  return (2u << 4) | ((uint32_t)a_signed << 7) | ((uint32_t)b_signed << 10) |
+         ((uint32_t)(I8_N >> 3) << 17) | ((uint32_t)((2 * I8_M) >> 4) << 24);
+}
+
+__device__ inline void i8_mma2(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
+}
+
+__device__ inline void tc_ld8_issue(uint32_t addr, uint32_t (&r)[8]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "r"(addr));
+}
+__device__ inline void tc_ld4_issue(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ inline void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+// int32 -> fp64 through the exponent trick (one LOP + one DADD instead of the
+// quarter-rate I2F.F64): 2^52 + 2^31 + v is exact, then subtract the bias
+__device__ inline double i8_i2d(uint32_t v) {
+  return __hiloint2double(0x43300000, (int)(v ^ 0x80000000u)) - 4503601774854144.0;
+}
+
+struct I8Params {
+  const uint8_t* A8;    // i8_a_index layout
+  const double* rsc;    // per row: 2^(e_r - 4)
+  const uint8_t* D8;    // i8_d_index layout
+  const double* csc;    // per walk: 2^(f_c - 4)
+  double* S;            // i8_s_index layout, fp64 slack
+  double* R;            // i8_s_index layout, fp64 rates of the previous iterate
+  const double* theta_prev;
+  long long* hi_key;
+  long long* lo_key;
+  long long* viol_key;
+  unsigned* sides;
+  const unsigned long long* err;
+  int64_t row_tiles;   // m_pad / 128
+  int64_t walk_tiles;  // z_pad / 128 (even)
+  int64_t KS;          // k steps of 32
+  int64_t z;           // live walks
+  double eps_dir;
+};
+
+// unit u -> (row tile, walk-tile pair): walk pairs inner, so the pairs in
+// flight share a few A tiles and every direction tile stays L2-resident
+__device__ inline void i8_unit(int64_t u, const I8Params& p, int64_t* rt, int64_t* wp) {
+  const int64_t pairs = p.walk_tiles / 2;
+  *rt = u / pairs;
+  *wp = u - *rt * pairs;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
+    chord_i8_kernel(const I8Params p) {
+  if (*p.err != kNoError) return;  // read identically by both CTAs of the pair
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint8_t* ring = smem_raw;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)I8_STAGES * I8_STAGE);
+  uint64_t* empty = full + I8_STAGES;
+  uint64_t* peer_full = empty + I8_STAGES;  // leader: the odd CTA's stage landed
+  uint64_t* tfull = peer_full + I8_STAGES;  // a pass's accumulators ready (both CTAs)
+  uint64_t* tempty = tfull + 1;             // a pass's accumulators drained (leader, 16 warps)
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 1);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int64_t n_units = p.row_tiles * (p.walk_tiles / 2);
+  const int my_units = (pair < n_units) ? (int)((n_units - 1 - pair) / npairs + 1) : 0;
+  const int KS = (int)p.KS;
+
+  if (tid == 0) {
+    for (int s = 0; s < I8_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&peer_full[s], 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, 2 * I8_EPI_WARPS);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tptr)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tptr;
+
+  if (warp == 0) {
+    // ---------------- producer: this CTA's direction slices + A half ----------------
+    if (lane == 0) {
+      const uint64_t keep = policy_evict_last();  // direction slices: re-read by every row tile
+      const uint64_t apol = policy_evict_normal();
+      int stage = 0, round = 0;
+      for (int ui = 0; ui < my_units; ++ui) {
+        int64_t rt, wp;
+        i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+        const int64_t wt = 2 * wp + rank;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int ns = i8_pass_slices(pass);
+          for (int ks = 0; ks < KS; ++ks) {
+            if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
+            uint8_t* st = ring + (size_t)stage * I8_STAGE;
+            mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * (I8_D_PIECE + I8_A_PIECE)));
+            const int64_t doff = (wt * p.KS + ks) * (int64_t)I8_D_STAGE;
+            const int64_t aoff =
+                ((rt * p.KS + ks) * 2 + rank) * (int64_t)(I8_SLICES * I8_A_PIECE);
+            bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
+            bulk_g2s_hint(st + I8_D_STAGE, p.A8 + aoff, ns * I8_A_PIECE, &full[stage], apol);
+            if (++stage == I8_STAGES) {
+              stage = 0;
+              ++round;
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // ---------------- MMA issuer (leader CTA) ----------------
+      int stage = 0, phase = 0;
+      for (int ui = 0; ui < my_units; ++ui) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const int ph = 2 * ui + pass;  // accumulator phase
+          if (ph >= 1) mbar_wait_cluster(tempty, (uint32_t)((ph - 1) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          for (int ks = 0; ks < KS; ++ks) {
+            mbar_wait(&full[stage], (uint32_t)phase);
+            mbar_wait_cluster(&peer_full[stage], (uint32_t)phase);
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint8_t* sd = ring + (size_t)stage * I8_STAGE;
+            const uint8_t* sa = sd + I8_D_STAGE;
+            uint64_t dd[I8_SLICES], da[I8_SLICES];
+#pragma unroll
+            for (int s = 0; s < I8_SLICES; ++s) {
+              dd[s] = umma_desc(sd + s * I8_D_PIECE, I8_M * 16, 128);
+              da[s] = umma_desc(sa + s * I8_A_PIECE, I8_NH * 16, 128);
+            }
+            if (pass == 0) {
+#pragma unroll
+              for (int l = 0; l < I8_PASS_LEVELS; ++l) {
+                const uint32_t acc = tmem + (uint32_t)(l * I8_N);
+#pragma unroll
+                for (int i = 0; i <= l; ++i)
+                  i8_mma2(acc, dd[l - i], da[i], i8_idesc(l - i == 0, i == 0),
+                          (ks > 0 || i > 0) ? 1u : 0u);
+              }
+            } else {
+#pragma unroll
+              for (int l = I8_PASS_LEVELS; l < I8_LEVELS; ++l) {
+                const uint32_t acc = tmem + (uint32_t)((l - I8_PASS_LEVELS) * I8_N);
+                const int i0 = l > I8_SLICES - 1 ? l - (I8_SLICES - 1) : 0;
+                const int i1 = l < I8_SLICES - 1 ? l : I8_SLICES - 1;
+#pragma unroll
+                for (int i = i0; i <= i1; ++i)
+                  i8_mma2(acc, dd[l - i], da[i], i8_idesc(l - i == 0, i == 0),
+                          (ks > 0 || i > i0) ? 1u : 0u);
+              }
+            }
+            tc_commit2(&empty[stage]);  // frees the slot in both CTAs when these MMAs finish
+            if (++stage == I8_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          tc_commit2(tfull);
+        }
+      }
+    } else if (lane == 0) {
+      // ---------------- relay (odd CTA): my stage landed -> leader ----------------
+      int stage = 0, phase = 0;
+      for (int ui = 0; ui < my_units; ++ui)
+        for (int pass = 0; pass < 2; ++pass)
+          for (int ks = 0; ks < KS; ++ks) {
+            mbar_wait(&full[stage], (uint32_t)phase);
+            mbar_arrive_remote(&peer_full[stage], 0);
+            if (++stage == I8_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+    }
+  } else {
+    // ---------------- epilogue: thread = walk, warp = (lane quarter, row half) ----------------
+    const int q = warp & 3;
+    const int rh = (warp - 2) / 4;
+    const int wl = q * 32 + lane;
+    const uint64_t stream_policy = policy_evict_first();  // the slack stream must not evict A
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(rh * I8_ROWS_PER_WARP);
+    auto release = [&]() {
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) {
+        if (rank == 0)
+          mbar_arrive(tempty);
+        else
+          mbar_arrive_remote(tempty, 0);
+      }
+    };
+    for (int ui = 0; ui < my_units; ++ui) {
+      int64_t rt, wp;
+      i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+      const int64_t wt = 2 * wp + rank;
+      const int64_t c = wt * I8_M + wl;
+      const int64_t r0 = rt * I8_N + rh * I8_ROWS_PER_WARP;
+      const double th = p.theta_prev[c];
+      const double cs = p.csc[c];
+      double ad[I8_ROWS_PER_WARP];
+      // pass 0: levels 0..3 -> ad = L0 + 2^-8 L1 + 2^-16 L2 + 2^-24 L3
+      mbar_wait(tfull, 0u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int g = 0; g < I8_ROWS_PER_WARP / 4; ++g) {
+        uint32_t lv[I8_PASS_LEVELS][4];
+#pragma unroll
+        for (int l = 0; l < I8_PASS_LEVELS; ++l) tc_ld4_issue(tbase + (uint32_t)(l * I8_N + g * 4), lv[l]);
+        tc_wait_ld();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double t = i8_i2d(lv[3][r]);
+          t = fma(t, 0.00390625, i8_i2d(lv[2][r]));
+          t = fma(t, 0.00390625, i8_i2d(lv[1][r]));
+          ad[g * 4 + r] = fma(t, 0.00390625, i8_i2d(lv[0][r]));
+        }
+      }
+      release();
+      // pass 1: levels 4..7, weight 2^-32 relative to pass 0
+      mbar_wait(tfull, 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int g = 0; g < I8_ROWS_PER_WARP / 4; ++g) {
+        uint32_t lv[I8_PASS_LEVELS][4];
+#pragma unroll
+        for (int l = 0; l < I8_PASS_LEVELS; ++l) tc_ld4_issue(tbase + (uint32_t)(l * I8_N + g * 4), lv[l]);
+        tc_wait_ld();
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          double t = i8_i2d(lv[3][r]);
+          t = fma(t, 0.00390625, i8_i2d(lv[2][r]));
+          t = fma(t, 0.00390625, i8_i2d(lv[1][r]));
+          t = fma(t, 0.00390625, i8_i2d(lv[0][r]));
+          ad[g * 4 + r] = fma(t, 2.3283064365386963e-10, ad[g * 4 + r]) * cs;
+        }
+      }
+      release();
+      // slack update + chord scan (as chord2_kernel<INCREMENTAL>), overlapping the
+      // next unit's MMAs
+      double hi = INFINITY, lo = -INFINITY, viol = -INFINITY;
+      unsigned sd = 0u;
+      const int64_t sbase = ((rt * p.walk_tiles + wt) * I8_N + rh * I8_ROWS_PER_WARP) * I8_M + wl;
+      const double* __restrict__ Sin = p.S + sbase;
+      const double* __restrict__ Rin = p.R + sbase;
+      double* __restrict__ Sout = p.S + sbase;
+      double* __restrict__ Rout = p.R + sbase;
+#pragma unroll
+      for (int g = 0; g < I8_ROWS_PER_WARP / 4; ++g) {
+        double so[4], ro[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          so[j] = ld_policy(Sin + (int64_t)(g * 4 + j) * I8_M, stream_policy);
+          ro[j] = ld_policy(Rin + (int64_t)(g * 4 + j) * I8_M, stream_policy);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const double a = ad[g * 4 + j] * __ldg(p.rsc + r0 + g * 4 + j);
+          const double s = fma(-th, ro[j], so[j]);
+          st_policy(Sout + (int64_t)(g * 4 + j) * I8_M, s, stream_policy);
+          st_policy(Rout + (int64_t)(g * 4 + j) * I8_M, a, stream_policy);
+          viol = fmax(viol, -s);
+          scan_row(s, a, p.eps_dir, hi, lo, sd);
+        }
+      }
+      if (c < p.z) {
+        const long long vk = dkey(viol), hk = dkey(hi), lk = dkey(lo);
+        if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
+        if (hk < *(volatile long long*)(p.hi_key + c)) atomicMin(p.hi_key + c, hk);
+        if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
+        if (sd & ~*(volatile unsigned*)(p.sides + c)) atomicOr(p.sides + c, sd);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  cluster_sync_all();  // all MMAs done and consumed in both CTAs before TMEM is freed
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+// ---------------------------------------------------------------------------
+// Operand preparation
+// ---------------------------------------------------------------------------
+
+// Per row of the column-major A_I: e_r (max|a_r| < 2^e_r) and rsc = 2^(e_r - 4).
+__global__ void i8_row_scale_kernel(const double* __restrict__ Acm, int64_t m, int64_t n,
+                                    int64_t m_pad, int* __restrict__ rexp,
+                                    double* __restrict__ rsc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m_pad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double mx = 0.0;
+    if (r < m)
+      for (int64_t k = 0; k < n; ++k) mx = fmax(mx, fabs(Acm[r + k * m]));
+    const int e = i8_exponent(mx);
+    rexp[r] = e;
+    rsc[r] = ldexp(1.0, e - 4);
+  }
+}
+
+// A_I -> 7 int8 slices per entry (i8_a_index); thread = (row, 16 coordinates).
+__global__ void i8_split_a_kernel(const double* __restrict__ Acm, int64_t m, int64_t n,
+                                  int64_t m_pad, int64_t KS, const int* __restrict__ rexp,
+                                  uint8_t* __restrict__ A8) {
+  const int64_t groups = KS * (I8_BK / 16);
+  const int64_t total = m_pad * groups;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % m_pad, k0 = (i / m_pad) * 16;
+    const int e = rexp[r];
+    uint8_t sl[I8_SLICES][16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int64_t k = k0 + kk;
+      const double a = (r < m && k < n) ? Acm[r + k * m] : 0.0;
+      const long long w = i8_fixed(a, e);
+#pragma unroll
+      for (int s = 0; s < I8_SLICES; ++s) sl[s][kk] = i8_slice(w, s);
+    }
+#pragma unroll
+    for (int s = 0; s < I8_SLICES; ++s)
+      *reinterpret_cast<uint4*>(A8 + i8_a_index(r, k0, s, KS)) = *reinterpret_cast<uint4*>(sl[s]);
+  }
+}
+
+// Per iterate: directions (packed b_index, fp64) -> per-walk exponent f_c,
+// csc = 2^(f_c - 4), 7 int8 slices per entry, and D replaced by the
+// quantised direction 2^(f_c - 52) w that the slices represent exactly.
+// One CTA per 64-walk tile.
+__global__ void __launch_bounds__(256) i8_split_d_kernel(double* __restrict__ D, int64_t n,
+                                                         int64_t KT, int64_t KS,
+                                                         uint8_t* __restrict__ D8,
+                                                         double* __restrict__ csc,
+                                                         const unsigned long long* err) {
+  if (*err != kNoError) return;
+  __shared__ unsigned long long wmax[BC];
+  __shared__ int wexp[BC];
+  const int tid = threadIdx.x;
+  const int64_t ct = blockIdx.x;
+  double* Dt = D + ct * KT * B_PIECE;  // this tile's packed pieces
+  if (tid < BC) wmax[tid] = 0ull;
+  __syncthreads();
+  // (1) per-walk max |d|: element (tid + 256 j) of every piece belongs to a fixed walk
+  unsigned long long mx[4] = {0ull, 0ull, 0ull, 0ull};
+  for (int64_t kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const double v = fabs(Dt[kt * B_PIECE + tid + 256 * j]);
+      const unsigned long long bits = (unsigned long long)__double_as_longlong(v);
+      mx[j] = bits > mx[j] ? bits : mx[j];
+    }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int64_t c, k;
+    b_coords(tid + 256 * j, KT, &c, &k);
+    atomicMax(&wmax[c], mx[j]);
+  }
+  __syncthreads();
+  if (tid < BC) {
+    const int e = i8_exponent(__longlong_as_double((long long)wmax[tid]));
+    wexp[tid] = e;
+    csc[ct * BC + tid] = ldexp(1.0, e - 4);
+  }
+  __syncthreads();
+  // (2) quantise in place (same element -> thread map)
+  for (int64_t kt = 0; kt < KT; ++kt)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int64_t c, k;
+      b_coords(tid + 256 * j, KT, &c, &k);
+      double* dp = Dt + kt * B_PIECE + tid + 256 * j;
+      const int e = wexp[c];
+      *dp = ldexp((double)i8_fixed(*dp, e), e - 52);
+    }
+  __syncthreads();
+  // (3) slices: thread = (walk, 16 coordinates); 16 bytes per slice store
+  const int64_t groups = KS * (I8_BK / 16);
+  for (int64_t i = tid; i < BC * groups; i += 256) {
+    const int cl = (int)(i % BC);
+    const int64_t k0 = (i / BC) * 16;
+    const int64_t c = ct * BC + cl;
+    const int e = wexp[cl];
+    uint8_t sl[I8_SLICES][16];
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int64_t k = k0 + kk;
+      const double d = k < KT * BK ? D[b_index(c, k, KT)] : 0.0;
+      const long long w = i8_fixed(d, e);
+#pragma unroll
+      for (int s = 0; s < I8_SLICES; ++s) sl[s][kk] = i8_slice(w, s);
+    }
+#pragma unroll
+    for (int s = 0; s < I8_SLICES; ++s)
+      *reinterpret_cast<uint4*>(D8 + i8_d_index(c, k0, s, KS)) = *reinterpret_cast<uint4*>(sl[s]);
+  }
+}
+
+}  // namespace mhar_dev

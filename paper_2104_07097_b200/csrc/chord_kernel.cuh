@@ -67,13 +67,14 @@ struct ChordParams {
   int64_t z;          // live walks
   double eps_dir;
   int group_m;        // rasterisation band height (m tiles)
-  int64_t tc_walk_tiles;  // > 0: the slack cache uses the fp32-variant layout (tc_s_index)
+  int64_t tc_walk_tiles;  // > 0: the slack cache uses a tcgen05 tile layout (tile_cache_index)
+  int64_t cache_rows;     // its row tile: 256 (fp32 variant, fp32 rates) or 64 (int8 slices)
+  int rate_f32;           // 1: the rate cache holds fp32 (fp32 variant)
 };
 
 // Slack-cache index for FUSED_STORE: the layout of whichever kernel consumes it.
 __device__ inline int64_t cache_index(int64_t r, int64_t c, const ChordParams& p) {
-  if (p.tc_walk_tiles > 0)  // tc_s_index (chord_tc32.cuh): [rt(256)][wt(128)][row][walk]
-    return (((r / 256) * p.tc_walk_tiles + c / 128) * 256 + r % 256) * 128 + c % 128;
+  if (p.tc_walk_tiles > 0) return tile_cache_index(r, c, p.tc_walk_tiles, p.cache_rows);
   return s_index(r, c, p.col_tiles);
 }
 
@@ -282,7 +283,7 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
           if (MODE == FUSED_STORE) {
             const int64_t si = cache_index(r, c0[j] + 2 * (lane & 3) + e, p);
             p.S[si] = sl;
-            if (p.tc_walk_tiles > 0)  // the fp32 variant keeps its rates in fp32
+            if (p.rate_f32)  // the fp32 variant keeps its rates in fp32
               reinterpret_cast<float*>(p.R)[si] = (float)ad;
             else
               p.R[si] = ad;

@@ -65,7 +65,7 @@ __host__ __device__ inline int64_t tc_a_index(int64_t r, int64_t k, int64_t KT) 
 }
 // slack / rate cache for the tc32 tile: [row_tile][walk_tile][row(256)][walk(128)]
 __host__ __device__ inline int64_t tc_s_index(int64_t r, int64_t c, int64_t WT) {
-  return (((r / TC_N) * WT + c / TC_M) * TC_N + r % TC_N) * TC_M + c % TC_M;
+  return tile_cache_index(r, c, WT, TC_N);
 }
 
 __device__ inline float tf32_trunc(float x) {

@@ -62,6 +62,12 @@ __host__ __device__ inline void b_coords(int64_t i, int64_t KT, int64_t* c, int6
 // writes 512 contiguous bytes per fragment:
 // [m_tile][walk_tile64][warp(8)][i(4)][j(4)][lane(32)][2].
 constexpr int64_t S_WARP_BLOCK = 4 * 4 * 32 * 2;  // doubles per warp per tile
+// Slack/rate cache of the tensor-core (tcgen05) chord kernels: [row_tile(rows)]
+// [walk_tile(128)][row][walk] -- rows = 256 (fp32 variant), 64 (int8-slice engine).
+__host__ __device__ inline int64_t tile_cache_index(int64_t r, int64_t c, int64_t WT, int64_t rows) {
+  return (((r / rows) * WT + c / 128) * rows + r % rows) * 128 + c % 128;
+}
+
 __host__ __device__ inline int64_t s_index(int64_t r, int64_t c, int64_t CT64) {
   const int64_t mt = r / BM, rr = r % BM, wm = rr / 32, i = (rr % 32) / 8, rq = rr % 8;
   const int64_t ct = c / BC, cc = c % BC, wn = cc / 32, j = (cc % 32) / 8, cq = (cc % 8) / 2,

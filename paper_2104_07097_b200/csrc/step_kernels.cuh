@@ -299,7 +299,9 @@ struct RedrawParams {
   const double* P;        // n x n column-major, or null
   double* R;              // incremental rate cache (s_index) or null
   int64_t ct64;
-  int64_t tc_walk_tiles;  // > 0: fp32-variant cache layout
+  int64_t tc_walk_tiles;  // > 0: tcgen05 tile cache layout (tile_cache_index)
+  int64_t cache_rows;     // its row tile
+  int rate_f32;           // 1: fp32 rate cache (fp32 variant)
   double* scratch;        // 3 n doubles per CTA
   double* lower;
   double* upper;
@@ -409,9 +411,11 @@ __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
           ad = fma(a, ds[k], ad);
         }
         const double sl = rp.b[r] - ax;
-        if (rp.R && rp.tc_walk_tiles > 0)  // fp32 variant: fp32 rate cache, tc_s_index
-          reinterpret_cast<float*>(rp.R)[(((r / 256) * rp.tc_walk_tiles + c / 128) * 256 +
-                                          r % 256) * 128 + c % 128] = (float)ad;
+        if (rp.R && rp.tc_walk_tiles > 0 && rp.rate_f32)  // fp32 variant: fp32 rate cache
+          reinterpret_cast<float*>(rp.R)[tile_cache_index(r, c, rp.tc_walk_tiles, rp.cache_rows)] =
+              (float)ad;
+        else if (rp.R && rp.tc_walk_tiles > 0)  // int8-slice engine: fp64 rates, tile layout
+          rp.R[tile_cache_index(r, c, rp.tc_walk_tiles, rp.cache_rows)] = ad;
         else if (rp.R)
           rp.R[s_index(r, c, rp.ct64)] = ad;
         if (ad > rp.eps_dir) {
