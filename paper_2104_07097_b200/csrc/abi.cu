@@ -102,6 +102,7 @@ struct mhar_ctx {
   double *rsc = nullptr, *csc = nullptr;
   int* rexp = nullptr;
   int64_t KS = 0, i8_row_tiles = 0;
+  unsigned long long* i8_prof = nullptr;  // MHAR_I8_PROFILE: per-CTA wait cycles of the last launch
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
   double* rows2 = nullptr;
   double* pinned[2] = {nullptr, nullptr};
@@ -321,6 +322,8 @@ int launch_i8(mhar_ctx* c) {
   p.KS = c->KS;
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
+  p.prof = c->i8_prof;
+  if (c->i8_prof) cudaMemsetAsync(c->i8_prof, 0, 8 * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
@@ -850,6 +853,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)I8_SMEM);
+      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->i8_prof, 8 * (size_t)c->num_sms))) {
+        cudaFree(tmp);
+        return bail(st);
+      }
     }
     // small bodies: keep the column-major copy for the walk-resident kernel
     c->small_ns = (int)(c->n | 1);
@@ -933,6 +940,27 @@ int mhar_ctx_destroy(mhar_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->i8_prof) {  // debugging aid: where the int8 engine's MMA issuer and producer wait
+    std::vector<unsigned long long> h(8 * (size_t)c->num_sms);
+    cudaMemcpy(h.data(), c->i8_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    double tot = 0, te = 0, tf = 0, tp = 0, emp = 0, ed = 0, es = 0, ew = 0;
+    int n = 0;
+    double atom = 0;
+    (void)atom;
+    for (int b = 0; b < c->num_sms; b += 2) {
+      if (!h[8 * b]) continue;
+      tot += h[8 * b]; te += h[8 * b + 1]; tf += h[8 * b + 2]; tp += h[8 * b + 3];
+      emp += h[8 * b + 4];
+      ed += h[8 * b + 5]; es += h[8 * b + 6]; ew += h[8 * b + 7];
+      ++n;
+    }
+    if (n)
+      std::fprintf(stderr, "[i8 profile] leaders %d: total %.3g cyc; MMA waits tempty %.1f%% full %.1f%% "
+                   "peer %.1f%%; producer waits empty %.1f%%; epilogue drains %.1f%% stream %.1f%% "
+                   "idle %.1f%%%s\n", n, tot / n, 100 * te / tot,
+                   100 * tf / tot, 100 * tp / tot, 100 * emp / tot, 100 * ed / tot, 100 * es / tot,
+                   100 * ew / tot, "");
+  }
   for (auto& ev : c->pending) {
     cudaEventDestroy(ev.first);
     cudaEventDestroy(ev.second);

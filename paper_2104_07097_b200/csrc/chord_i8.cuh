@@ -37,10 +37,6 @@
 // slack update and chord scan of chord2_kernel<INCREMENTAL> (fp64, exact
 // division filter) while the tensor cores work on.
 //
-// Warp roles (320 threads per CTA): warp 0 lane 0 = bulk-copy producer;
-// warp 1 = TMEM allocation, lane 0 = MMA issuer (even CTA) / stage relay (odd
-// CTA); warps 2..9 = epilogue (lane quarter = warp % 4, two warps per quarter
-// splitting the 128 rows).
 #pragma once
 
 #include "chord_tc32.cuh"
@@ -57,18 +53,34 @@ constexpr int I8_LEVELS = 8;    // slice-pair levels i + j = 0..7
 constexpr int I8_PASS_LEVELS = 4;  // level accumulators live per pass (4 x 128 TMEM columns)
 constexpr int I8_D_PIECE = I8_M * I8_BK;   // bytes per direction slice piece (4 KB)
 constexpr int I8_A_PIECE = I8_NH * I8_BK;  // bytes per A slice half piece (2 KB)
-constexpr int I8_D_STAGE = I8_SLICES * I8_D_PIECE;            // 28 KB
-constexpr int I8_STAGE = I8_SLICES * (I8_D_PIECE + I8_A_PIECE);  // 42 KB
-constexpr int I8_STAGES = 5;
-constexpr int I8_EPI_WARPS = 8;
-constexpr int I8_THREADS = 64 + 32 * I8_EPI_WARPS;
-constexpr size_t I8_SMEM = (size_t)I8_STAGES * I8_STAGE + 512;
+constexpr int I8_D_STAGE = I8_SLICES * I8_D_PIECE;  // 28 KB: one k step of direction slices
+// Ring slot: slices 0..3 of both operands (24 KB).  A pass-0 k step is one
+// slot ("a"); a pass-1 k step is slot "a" plus slot "b" holding slices 4..6.
+constexpr int I8_SLOT_SLICES = 4;
+constexpr int I8_SLOT = I8_SLOT_SLICES * (I8_D_PIECE + I8_A_PIECE);  // 24 KB
+constexpr int I8_SLOT_A = I8_SLOT_SLICES * I8_D_PIECE;               // A slices at +16 KB
+constexpr int I8_STAGES = 6;
+// Warp roles: warpgroup 0 = warp 0 bulk-copy producer, warp 1 TMEM allocation
+// + MMA issuer (even CTA) / stage relay (odd CTA), warp 2 slack/rate loader,
+// warp 3 idle -- they drop to 32 registers (setmaxnreg) so that the 16
+// epilogue warps (warpgroups 1..4) get 112: lane quarter = warp % 4, row
+// quarter = (warp - 4) / 4, so each thread owns one walk x 32 rows.
+constexpr int I8_EPI_WARPS = 16;
+constexpr int I8_ROWS_PER_WARP = I8_N / 4;
+constexpr int I8_THREADS = 128 + 32 * I8_EPI_WARPS;  // 640
+constexpr int I8_CTRL_REGS = 32, I8_EPI_REGS = 112;  // 128 x 32 + 512 x 112 = 640 x 96 (launch)
+// Slack/rate staging: the epilogue's stream of the cache is latency-bound with
+// plain loads, so the loader warp moves it HBM -> smem with bulk copies, 4 rows
+// (4 KB of S + 4 KB of R) per slot, two slots per row quarter.
+constexpr int I8_SR_ROWS = 4;
+constexpr int I8_SR_CHUNK = I8_SR_ROWS * I8_M * 8;  // bytes of S (or R) per slot
+constexpr int I8_SR_SLOTS = 8;
+constexpr size_t I8_SR_OFF = (size_t)I8_STAGES * I8_SLOT;
+constexpr size_t I8_RSC_OFF = I8_SR_OFF + (size_t)I8_SR_SLOTS * 2 * I8_SR_CHUNK;  // per-warp row scales
+constexpr size_t I8_BAR_OFF = I8_RSC_OFF + (size_t)I8_EPI_WARPS * I8_ROWS_PER_WARP * 8;
+constexpr size_t I8_SMEM = I8_BAR_OFF + 512;
 constexpr int64_t I8_MAX_K = 4608;  // keeps every level accumulator inside int32
-constexpr int I8_ROWS_PER_WARP = I8_N / 2;
 constexpr int I8_MMAS = 34;         // slice-pair products per k step (10 + 24)
-
-// slices a pass needs of each operand: pass 0 -> 0..3, pass 1 -> 0..6
-__host__ __device__ constexpr int i8_pass_slices(int pass) { return pass == 0 ? 4 : I8_SLICES; }
 
 // Interleaved K-major ("no swizzle") core-matrix layout of one (tile, k step)
 // slice piece of R rows, in bytes: [k_chunk(16 B)][row_group(8 rows)][row(8)][16].
@@ -126,6 +138,11 @@ __device__ inline void tc_ld4_issue(uint32_t addr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(addr));
 }
+// streaming store without a compiler memory barrier (the stream's addresses
+// are private to the thread, so later loads may be hoisted above it)
+__device__ inline void st_stream(double* p, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol));
+}
 __device__ inline void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // int32 -> fp64 through the exponent trick (one LOP + one DADD instead of the
@@ -152,6 +169,7 @@ struct I8Params {
   int64_t KS;          // k steps of 32
   int64_t z;           // live walks
   double eps_dir;
+  unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
 };
 
 // unit u -> (row tile, walk-tile pair): walk pairs inner, so the pairs in
@@ -167,12 +185,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
   if (*p.err != kNoError) return;  // read identically by both CTAs of the pair
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint8_t* ring = smem_raw;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)I8_STAGES * I8_STAGE);
+  const double* sr = reinterpret_cast<const double*>(smem_raw + I8_SR_OFF);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + I8_BAR_OFF);
   uint64_t* empty = full + I8_STAGES;
-  uint64_t* peer_full = empty + I8_STAGES;  // leader: the odd CTA's stage landed
+  uint64_t* peer_full = empty + I8_STAGES;  // leader: the odd CTA's slot landed
   uint64_t* tfull = peer_full + I8_STAGES;  // a pass's accumulators ready (both CTAs)
-  uint64_t* tempty = tfull + 1;             // a pass's accumulators drained (leader, 16 warps)
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 1);
+  uint64_t* tempty = tfull + 1;             // a pass's accumulators drained (leader, 32 warps)
+  uint64_t* sr_full = tempty + 1;           // [I8_SR_SLOTS] slack/rate chunk landed
+  uint64_t* sr_empty = sr_full + I8_SR_SLOTS;  // [I8_SR_SLOTS] chunk consumed (4 warps)
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(sr_empty + I8_SR_SLOTS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -189,6 +210,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, 2 * I8_EPI_WARPS);
+    for (int s = 0; s < I8_SR_SLOTS; ++s) {
+      mbar_init(&sr_full[s], 1);
+      mbar_init(&sr_empty[s], 4);
+    }
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -202,65 +227,88 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tptr;
 
-  if (warp == 0) {
-    // ---------------- producer: this CTA's direction slices + A half ----------------
-    if (lane == 0) {
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(I8_CTRL_REGS));
+    if (warp == 0 && lane == 0) {
+      // ---------------- producer: this CTA's direction slices + A half ----------------
       const uint64_t keep = policy_evict_last();  // direction slices: re-read by every row tile
       const uint64_t apol = policy_evict_normal();
       int stage = 0, round = 0;
+      long long w_empty = 0;
       for (int ui = 0; ui < my_units; ++ui) {
         int64_t rt, wp;
         i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
-        for (int pass = 0; pass < 2; ++pass) {
-          const int ns = i8_pass_slices(pass);
-          for (int ks = 0; ks < KS; ++ks) {
-            if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
-            uint8_t* st = ring + (size_t)stage * I8_STAGE;
-            mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * (I8_D_PIECE + I8_A_PIECE)));
-            const int64_t doff = (wt * p.KS + ks) * (int64_t)I8_D_STAGE;
-            const int64_t aoff =
-                ((rt * p.KS + ks) * 2 + rank) * (int64_t)(I8_SLICES * I8_A_PIECE);
-            bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
-            bulk_g2s_hint(st + I8_D_STAGE, p.A8 + aoff, ns * I8_A_PIECE, &full[stage], apol);
-            if (++stage == I8_STAGES) {
-              stage = 0;
-              ++round;
+        for (int pi = 0; pi < 2; ++pi)  // the long pass (levels 4..7) first
+          for (int ks = 0; ks < KS; ++ks)
+            for (int half = 0; half <= 1 - pi; ++half) {  // slot a: slices 0..3, b: 4..6
+              const int s0 = half * I8_SLOT_SLICES;
+              const int ns = half ? I8_SLICES - I8_SLOT_SLICES : I8_SLOT_SLICES;
+              const long long t0 = clock64();
+              if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
+              w_empty += clock64() - t0;
+              uint8_t* st = ring + (size_t)stage * I8_SLOT;
+              mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * (I8_D_PIECE + I8_A_PIECE)));
+              const int64_t doff = (wt * p.KS + ks) * (int64_t)I8_D_STAGE + s0 * I8_D_PIECE;
+              const int64_t aoff =
+                  ((rt * p.KS + ks) * 2 + rank) * (int64_t)(I8_SLICES * I8_A_PIECE) + s0 * I8_A_PIECE;
+              bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
+              bulk_g2s_hint(st + I8_SLOT_A, p.A8 + aoff, ns * I8_A_PIECE, &full[stage], apol);
+              if (++stage == I8_STAGES) {
+                stage = 0;
+                ++round;
+              }
             }
-          }
-        }
       }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && rank == 0) {
+      if (p.prof) p.prof[8 * blockIdx.x + 4] = (unsigned long long)w_empty;
+    } else if (warp == 1 && lane == 0 && rank == 0) {
       // ---------------- MMA issuer (leader CTA) ----------------
       int stage = 0, phase = 0;
+      long long w_tempty = 0, w_full = 0, w_peer = 0;
+      const long long t_start = clock64();
       for (int ui = 0; ui < my_units; ++ui) {
-        for (int pass = 0; pass < 2; ++pass) {
-          const int ph = 2 * ui + pass;  // accumulator phase
-          if (ph >= 1) mbar_wait_cluster(tempty, (uint32_t)((ph - 1) & 1));
+        for (int pi = 0; pi < 2; ++pi) {  // the long pass (levels 4..7) first
+          const int pass = 1 - pi;
+          const int ph = 2 * ui + pi;  // accumulator phase
+          long long t0 = clock64();
+          if (ph >= 1) mbar_wait_relaxed(tempty, (uint32_t)((ph - 1) & 1));
+          w_tempty += clock64() - t0;
           asm volatile("tcgen05.fence::after_thread_sync;");
           for (int ks = 0; ks < KS; ++ks) {
-            mbar_wait(&full[stage], (uint32_t)phase);
-            mbar_wait_cluster(&peer_full[stage], (uint32_t)phase);
-            asm volatile("tcgen05.fence::after_thread_sync;");
-            const uint8_t* sd = ring + (size_t)stage * I8_STAGE;
-            const uint8_t* sa = sd + I8_D_STAGE;
-            uint64_t dd[I8_SLICES], da[I8_SLICES];
-#pragma unroll
-            for (int s = 0; s < I8_SLICES; ++s) {
-              dd[s] = umma_desc(sd + s * I8_D_PIECE, I8_M * 16, 128);
-              da[s] = umma_desc(sa + s * I8_A_PIECE, I8_NH * 16, 128);
+            const uint8_t* sbase[2];
+            int slot[2];
+            for (int half = 0; half <= pass; ++half) {
+              long long t1 = clock64();
+              mbar_wait(&full[stage], (uint32_t)phase);
+              long long t2 = clock64();
+              mbar_wait_relaxed(&peer_full[stage], (uint32_t)phase);
+              w_full += t2 - t1;
+              w_peer += clock64() - t2;
+              sbase[half] = ring + (size_t)stage * I8_SLOT;
+              slot[half] = stage;
+              if (++stage == I8_STAGES) {
+                stage = 0;
+                phase ^= 1;
+              }
             }
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            // slice s of either operand lives in slot s / 4 at piece s % 4
+            auto ddesc = [&](int sl) {
+              return umma_desc(sbase[sl >> 2] + (sl & 3) * I8_D_PIECE, I8_M * 16, 128);
+            };
+            auto adesc = [&](int sl) {
+              return umma_desc(sbase[sl >> 2] + I8_SLOT_A + (sl & 3) * I8_A_PIECE, I8_NH * 16, 128);
+            };
             if (pass == 0) {
 #pragma unroll
               for (int l = 0; l < I8_PASS_LEVELS; ++l) {
                 const uint32_t acc = tmem + (uint32_t)(l * I8_N);
 #pragma unroll
                 for (int i = 0; i <= l; ++i)
-                  i8_mma2(acc, dd[l - i], da[i], i8_idesc(l - i == 0, i == 0),
+                  i8_mma2(acc, ddesc(l - i), adesc(i), i8_idesc(l - i == 0, i == 0),
                           (ks > 0 || i > 0) ? 1u : 0u);
               }
+              tc_commit2(&empty[slot[0]]);  // frees the slot in both CTAs when these MMAs finish
             } else {
 #pragma unroll
               for (int l = I8_PASS_LEVELS; l < I8_LEVELS; ++l) {
@@ -269,40 +317,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
                 const int i1 = l < I8_SLICES - 1 ? l : I8_SLICES - 1;
 #pragma unroll
                 for (int i = i0; i <= i1; ++i)
-                  i8_mma2(acc, dd[l - i], da[i], i8_idesc(l - i == 0, i == 0),
+                  i8_mma2(acc, ddesc(l - i), adesc(i), i8_idesc(l - i == 0, i == 0),
                           (ks > 0 || i > i0) ? 1u : 0u);
               }
-            }
-            tc_commit2(&empty[stage]);  // frees the slot in both CTAs when these MMAs finish
-            if (++stage == I8_STAGES) {
-              stage = 0;
-              phase ^= 1;
+              tc_commit2(&empty[slot[0]]);
+              tc_commit2(&empty[slot[1]]);
             }
           }
           tc_commit2(tfull);
         }
       }
-    } else if (lane == 0) {
-      // ---------------- relay (odd CTA): my stage landed -> leader ----------------
+      if (p.prof) {
+        unsigned long long* pr = p.prof + 8 * blockIdx.x;
+        pr[0] = (unsigned long long)(clock64() - t_start);
+        pr[1] = (unsigned long long)w_tempty;
+        pr[2] = (unsigned long long)w_full;
+        pr[3] = (unsigned long long)w_peer;
+      }
+    } else if (warp == 1 && lane == 0) {
+      // ---------------- relay (odd CTA): my slot landed -> leader ----------------
       int stage = 0, phase = 0;
-      for (int ui = 0; ui < my_units; ++ui)
-        for (int pass = 0; pass < 2; ++pass)
-          for (int ks = 0; ks < KS; ++ks) {
-            mbar_wait(&full[stage], (uint32_t)phase);
-            mbar_arrive_remote(&peer_full[stage], 0);
-            if (++stage == I8_STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
+      const int slots = my_units * 3 * KS;  // short pass: 1 slot per k step, long pass: 2
+      for (int i = 0; i < slots; ++i) {
+        mbar_wait(&full[stage], (uint32_t)phase);
+        mbar_arrive_remote(&peer_full[stage], 0);
+        if (++stage == I8_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    } else if (warp == 2 && lane == 0) {
+      // ---------------- loader: this CTA's slack/rate blocks -> smem ----------------
+      const uint64_t stream_policy = policy_evict_first();
+      for (int ui = 0; ui < my_units; ++ui) {
+        int64_t rt, wp;
+        i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+        const int64_t wt = 2 * wp + rank;
+        const int64_t cb = (rt * p.walk_tiles + wt) * (int64_t)(I8_N * I8_M);
+        for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j)
+          for (int g = 0; g < 4; ++g) {  // row quarter g's j-th chunk
+            const int slot = 2 * g + (j & 1);
+            const int use = (I8_ROWS_PER_WARP / I8_SR_ROWS / 2) * ui + j / 2;
+            if (use >= 1) mbar_wait(&sr_empty[slot], (uint32_t)((use - 1) & 1));
+            uint8_t* dst = smem_raw + I8_SR_OFF + (size_t)slot * 2 * I8_SR_CHUNK;
+            const int64_t off = cb + (int64_t)(g * I8_ROWS_PER_WARP + j * I8_SR_ROWS) * I8_M;
+            mbar_arrive_expect_tx(&sr_full[slot], 2 * I8_SR_CHUNK);
+            bulk_g2s_hint(dst, p.S + off, I8_SR_CHUNK, &sr_full[slot], stream_policy);
+            bulk_g2s_hint(dst + I8_SR_CHUNK, p.R + off, I8_SR_CHUNK, &sr_full[slot], stream_policy);
           }
+      }
     }
   } else {
-    // ---------------- epilogue: thread = walk, warp = (lane quarter, row half) ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(I8_EPI_REGS));
+    // ---------------- epilogue: thread = walk, warp = (lane quarter, row quarter) ----------------
     const int q = warp & 3;
-    const int rh = (warp - 2) / 4;
+    const int rq = (warp - 4) >> 2;
     const int wl = q * 32 + lane;
     const uint64_t stream_policy = policy_evict_first();  // the slack stream must not evict A
-    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(rh * I8_ROWS_PER_WARP);
+    const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(rq * I8_ROWS_PER_WARP);
+    double* wrsc = reinterpret_cast<double*>(smem_raw + I8_RSC_OFF) + (warp - 4) * I8_ROWS_PER_WARP;
     auto release = [&]() {
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
@@ -318,12 +391,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
       const int64_t wt = 2 * wp + rank;
       const int64_t c = wt * I8_M + wl;
-      const int64_t r0 = rt * I8_N + rh * I8_ROWS_PER_WARP;
+      const int64_t r0 = rt * I8_N + rq * I8_ROWS_PER_WARP;
       const double th = p.theta_prev[c];
       const double cs = p.csc[c];
+      __syncwarp();
+      wrsc[lane] = __ldg(p.rsc + r0 + lane);
+      __syncwarp();
       double ad[I8_ROWS_PER_WARP];
-      // pass 0: levels 0..3 -> ad = L0 + 2^-8 L1 + 2^-16 L2 + 2^-24 L3
+      // first pass: levels 4..7 -> ad = L4 + 2^-8 L5 + 2^-16 L6 + 2^-24 L7
+      long long e0 = clock64();
       mbar_wait(tfull, 0u);
+      long long e1 = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int g = 0; g < I8_ROWS_PER_WARP / 4; ++g) {
@@ -340,8 +418,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         }
       }
       release();
-      // pass 1: levels 4..7, weight 2^-32 relative to pass 0
+      long long e2 = clock64();
+      // second pass: levels 0..3; levels 4..7 weigh 2^-32 relative to them
       mbar_wait(tfull, 1u);
+      long long e3 = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;");
 #pragma unroll
       for (int g = 0; g < I8_ROWS_PER_WARP / 4; ++g) {
@@ -355,43 +435,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
           t = fma(t, 0.00390625, i8_i2d(lv[2][r]));
           t = fma(t, 0.00390625, i8_i2d(lv[1][r]));
           t = fma(t, 0.00390625, i8_i2d(lv[0][r]));
-          ad[g * 4 + r] = fma(t, 2.3283064365386963e-10, ad[g * 4 + r]) * cs;
+          ad[g * 4 + r] = fma(ad[g * 4 + r], 2.3283064365386963e-10, t) * cs;
         }
       }
       release();
-      // slack update + chord scan (as chord2_kernel<INCREMENTAL>), overlapping the
-      // next unit's MMAs
+      long long e4 = clock64();
+      // slack update + chord scan (as chord2_kernel<INCREMENTAL>) on the staged
+      // slack/rate chunks, overlapping the next unit's MMAs
       double hi = INFINITY, lo = -INFINITY, viol = -INFINITY;
       unsigned sd = 0u;
-      const int64_t sbase = ((rt * p.walk_tiles + wt) * I8_N + rh * I8_ROWS_PER_WARP) * I8_M + wl;
-      const double* __restrict__ Sin = p.S + sbase;
-      const double* __restrict__ Rin = p.R + sbase;
+      const int64_t sbase = ((rt * p.walk_tiles + wt) * I8_N + rq * I8_ROWS_PER_WARP) * I8_M + wl;
       double* __restrict__ Sout = p.S + sbase;
       double* __restrict__ Rout = p.R + sbase;
 #pragma unroll
-      for (int g = 0; g < I8_ROWS_PER_WARP / 4; ++g) {
-        double so[4], ro[4];
+      for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j) {
+        const int slot = 2 * rq + (j & 1);
+        mbar_wait(&sr_full[slot], (uint32_t)((j / 2) & 1));
+        const double* sS = sr + (size_t)slot * 2 * (I8_SR_CHUNK / 8) + wl;
+        const double* sR = sS + I8_SR_CHUNK / 8;
+        double sv[I8_SR_ROWS], av[I8_SR_ROWS];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          so[j] = ld_policy(Sin + (int64_t)(g * 4 + j) * I8_M, stream_policy);
-          ro[j] = ld_policy(Rin + (int64_t)(g * 4 + j) * I8_M, stream_policy);
+        for (int r = 0; r < I8_SR_ROWS; ++r) {
+          const int row = j * I8_SR_ROWS + r;
+          av[r] = ad[row] * wrsc[row];
+          sv[r] = fma(-th, sR[r * I8_M], sS[r * I8_M]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&sr_empty[slot]);
+#pragma unroll
+        for (int r = 0; r < I8_SR_ROWS; ++r) {
+          const int row = j * I8_SR_ROWS + r;
+          st_stream(Sout + (int64_t)row * I8_M, sv[r], stream_policy);
+          st_stream(Rout + (int64_t)row * I8_M, av[r], stream_policy);
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const double a = ad[g * 4 + j] * __ldg(p.rsc + r0 + g * 4 + j);
-          const double s = fma(-th, ro[j], so[j]);
-          st_policy(Sout + (int64_t)(g * 4 + j) * I8_M, s, stream_policy);
-          st_policy(Rout + (int64_t)(g * 4 + j) * I8_M, a, stream_policy);
-          viol = fmax(viol, -s);
-          scan_row(s, a, p.eps_dir, hi, lo, sd);
+        for (int r = 0; r < I8_SR_ROWS; ++r) {
+          viol = fmax(viol, -sv[r]);
+          scan_row(sv[r], av[r], p.eps_dir, hi, lo, sd);
         }
+      }
+      const long long e5 = clock64();
+      if (p.prof && warp == 4 && lane == 0) {
+        unsigned long long* pr = p.prof + 8 * blockIdx.x;
+        pr[5] += (unsigned long long)((e2 - e1) + (e4 - e3));  // drains
+        pr[6] += (unsigned long long)(e5 - e4);                 // stream + scan
+        pr[7] += (unsigned long long)((e1 - e0) + (e3 - e2));  // waiting for the MMAs
       }
       if (c < p.z) {
         const long long vk = dkey(viol), hk = dkey(hi), lk = dkey(lo);
-        if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
-        if (hk < *(volatile long long*)(p.hi_key + c)) atomicMin(p.hi_key + c, hk);
-        if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
-        if (sd & ~*(volatile unsigned*)(p.sides + c)) atomicOr(p.sides + c, sd);
+        // fire-and-forget reductions (no return value: RED, no round trip)
+        atomicMax(p.viol_key + c, vk);
+        atomicMin(p.hi_key + c, hk);
+        atomicMax(p.lo_key + c, lk);
+        if (sd) atomicOr(p.sides + c, sd);
       }
     }
   }

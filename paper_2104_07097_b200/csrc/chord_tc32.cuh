@@ -131,6 +131,20 @@ __device__ inline void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// relaxed cluster-scope wait: for barriers that only publish completions of
+// async-proxy work (a peer's bulk copies landed, a peer's TMEM loads waited
+// on); unlike the acquire form it does not invalidate L1 (CCTL.IVALL).
+__device__ inline void mbar_wait_relaxed(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ inline void tc_ld32(uint32_t addr, float (&v)[32]) {
   uint32_t r[32];
   asm volatile(

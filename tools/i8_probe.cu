@@ -136,6 +136,101 @@ void run(unsigned long long* sink, int sms) {
          MODE == 0 ? "cg1_SS" : MODE == 1 ? "cg1_TS" : "cg2_SS", N, cudaGetErrorString(e), ms, tops);
 }
 
+
+// The engine's pass-1 issue pattern (levels 4..7 of 7x7 slice pairs, N = 128,
+// cta_group::2): VAR = 0 exact sequence (signedness per pair, same-accumulator
+// runs), 1 constant idesc, 2 accumulator rotated every MMA.
+template <int VAR>
+__global__ void __launch_bounds__(128, 1) probe_seq(int iters, unsigned long long* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint8_t* sa = sm;                  // 7 direction slices x 4 KB
+  uint8_t* sb = sm + 7 * 4096;       // 7 A half slices x 2 KB
+  uint64_t* done = reinterpret_cast<uint64_t*>(sm + 7 * 4096 + 7 * 2048);
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(done + 1);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const uint32_t rank = ctarank();
+  for (int i = tid; i < (7 * 4096 + 7 * 2048) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
+  if (tid == 0) {
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tptr)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tptr;
+  if (tid == 0 && rank == 0) {
+    uint64_t dd[7], da[7];
+    for (int s = 0; s < 7; ++s) {
+      dd[s] = sdesc(sa + s * 4096, 128 * 16, 128);
+      da[s] = sdesc(sb + s * 2048, 64 * 16, 128);
+    }
+    int q = 0;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int l = 4; l < 8; ++l) {
+        const int i0 = l > 6 ? l - 6 : 0, i1 = l < 6 ? l : 6;
+#pragma unroll
+        for (int i = i0; i <= i1; ++i) {
+          const int j = l - i;
+          const uint32_t sa_ = VAR == 1 ? 1u : (j == 0 ? 1u : 0u), sb_ = VAR == 1 ? 1u : (i == 0 ? 1u : 0u);
+          const uint32_t idesc = (2u << 4) | (sa_ << 7) | (sb_ << 10) | ((uint32_t)(128 >> 3) << 17) | ((256u >> 4) << 24);
+          const uint32_t acc = tmem + (uint32_t)(((VAR == 2 ? (q++ & 3) : (l - 4))) * 128);
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                       ::"r"(acc), "l"(dd[j]), "l"(da[i]), "r"(idesc), "r"(1u));
+        }
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(s32(done)), "h"((unsigned short)3) : "memory");
+  }
+  __syncwarp();
+  mbar_wait(done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tmem + ((uint32_t)(warp * 32) << 16)));
+  asm volatile("tcgen05.wait::ld.sync.aligned;");
+  if (v == 0x12345678u) sink[0] = v;
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+}
+
+template <int VAR>
+void run_seq(unsigned long long* sink, int sms) {
+  const size_t smem = 7 * 4096 + 7 * 2048 + 64;
+  cudaFuncSetAttribute(probe_seq<VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int iters = 2000;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(sms);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, probe_seq<VAR>, iters, sink);
+  cudaDeviceSynchronize();
+  cudaEvent_t t0, t1;
+  cudaEventCreate(&t0);
+  cudaEventCreate(&t1);
+  cudaEventRecord(t0);
+  cudaLaunchKernelEx(&cfg, probe_seq<VAR>, iters, sink);
+  cudaEventRecord(t1);
+  cudaEventSynchronize(t1);
+  float ms;
+  cudaEventElapsedTime(&ms, t0, t1);
+  const double ops_per_sm = 2.0 * 128 * 128 * KB * (double)iters * 24;
+  printf("{\"mode\": \"engine_pass1_seq_var%d\", \"N\": 128, \"status\": \"%s\", \"ms\": %.3f, \"int8_tops\": %.1f}\n",
+         VAR, cudaGetErrorString(cudaGetLastError()), ms, ops_per_sm * sms / (ms * 1e-3) / 1e12);
+}
+
 int main() {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -150,5 +245,8 @@ int main() {
   run<2, 64>(sink, sms);
   run<2, 128>(sink, sms);
   run<2, 256>(sink, sms);
+  run_seq<0>(sink, sms);
+  run_seq<1>(sink, sms);
+  run_seq<2>(sink, sms);
   return 0;
 }
