@@ -68,25 +68,37 @@ def ncu_traffic(capture: str):
 I8_MMAS_PER_KSTEP = 34  # slice-pair products per k step (chord_i8.cuh)
 
 
-def int8_dense_peak():
-    """Dense int8 tensor-core peak on this pool's B200: the best tcgen05
-    kind::i8 rate of the MMA-only microbenchmark (tools/i8_probe.cu,
-    profiles/int8_probe_r01.jsonl); fallback 4500 TOPS (nominal)."""
+TENSOR_PROBE = os.path.join(ROOT, "profiles", "tensor_probe_r01.jsonl")
+
+
+def _probe_peak(key: str):
+    """Best rate of the MMA-only tcgen05 microbenchmark (tools/i8_probe.cu on
+    this pool's B200, profiles/tensor_probe_r01.jsonl) for `key`."""
     best = None
     try:
-        with open(os.path.join(ROOT, "profiles", "int8_probe_r01.jsonl")) as f:
+        with open(TENSOR_PROBE) as f:
             for line in f:
-                v = json.loads(line).get("int8_tops")
-                best = v if best is None else max(best, v)
+                v = json.loads(line).get(key)
+                if v is not None:
+                    best = v if best is None else max(best, v)
     except (OSError, ValueError):
         pass
-    return best or 4500.0
+    return best
+
+
+def int8_dense_peak():
+    """Dense int8 tensor-core peak (tcgen05 kind::i8 microbench); fallback
+    4500 TOPS (nominal)."""
+    return _probe_peak("int8_tops") or 4500.0
 
 
 def tf32_dense_peak():
-    """TF32 tensor-core peak: the driver-measured dense bf16 GEMM rate
-    (MEASURED_PEAKS.json) halved -- TF32 runs at half the bf16 rate on
-    Blackwell; fallback 1.59 PFLOP/s bf16 (B200_PROFILING.md)."""
+    """TF32 tensor-core peak: the tcgen05 kind::tf32 microbench (CTA pair,
+    N = 256, the fp32 variant's shape); fallback the driver-measured dense
+    bf16 GEMM rate halved (MEASURED_PEAKS.json), then 1590/2."""
+    v = _probe_peak("tf32_tflops")
+    if v:
+        return v
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             return json.load(f)["bf16_tflops"] / 2.0
@@ -413,7 +425,7 @@ def run_engine(args, world, rank, local):
               "roofline": {"bound": "tensor", "achieved": ops8, "peak": i8_peak,
                            "unit": "TOPS (int8 executed)", "frac": ops8 / i8_peak,
                            "traffic": ncu_traffic("i8_full"),
-                           "peak_source": "tcgen05 kind::i8 microbench, profiles/int8_probe_r01.jsonl"},
+                           "peak_source": "tcgen05 kind::i8 microbench, profiles/tensor_probe_r01.jsonl"},
               "all_inside_eps_feas": bool(bad8 == -1)}
 
     # the north star's fp32 variant on the same workload (A_I rounded to fp32,
@@ -442,7 +454,7 @@ def run_engine(args, world, rank, local):
                              "unit": "TFLOP/s (TF32 executed)", "frac": tf32_exec / tf32_peak,
                              "traffic": ncu_traffic("tc32_full"),
                              "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
-                             "peak_source": "MEASURED_PEAKS.json bf16 dense / 2"},
+                             "peak_source": "tcgen05 kind::tf32 microbench, profiles/tensor_probe_r01.jsonl"},
                 "all_inside_eps_feas": bool(bad32 == -1)}
 
     if rank != 0:
@@ -499,7 +511,7 @@ def run_engine(args, world, rank, local):
                                  "frac": 2.0 * achieved / tf32_dense_peak(),
                                  "kernel": "chord_tc32_kernel",
                                  "traffic": ncu_traffic("tc32_full"),
-                                 "peak_source": "MEASURED_PEAKS.json bf16 dense / 2"})
+                                 "peak_source": "tcgen05 kind::tf32 microbench"})
     print(json.dumps(line), flush=True)
 
 

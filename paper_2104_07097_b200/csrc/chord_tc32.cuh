@@ -273,12 +273,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int stage = 0, phase = 0;
       for (int ui = 0; ui < my_units; ++ui) {
         const int ab = ui & 1;
-        if (ui >= 2) mbar_wait_cluster(&tempty[ab], (uint32_t)(((ui >> 1) - 1) & 1));
+        if (ui >= 2) mbar_wait_relaxed(&tempty[ab], (uint32_t)(((ui >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t acc = tmem + (uint32_t)(ab * TC_N);
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], (uint32_t)phase);
-          mbar_wait_cluster(&peer_full[stage], (uint32_t)phase);
+          mbar_wait_relaxed(&peer_full[stage], (uint32_t)phase);
           asm volatile("tcgen05.fence::after_thread_sync;");
           const float* sd = ring + (size_t)stage * TC_STAGE_FLOATS;
           const float* sa_hi = sd + TC_D_PIECE;

@@ -29,7 +29,7 @@ __device__ inline uint32_t ctarank() {
 
 constexpr int KB = 32;  // bytes of K per MMA
 
-// MODE 0: cg1 SS, 1: cg1 TS (A in TMEM), 2: cg2 SS
+// MODE 0: cg1 SS, 1: cg1 TS (A in TMEM), 2: cg2 SS, 3: cg2 SS kind::tf32 (K = 8 per MMA)
 template <int MODE, int N>
 __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, unsigned long long* sink) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
   uint64_t* done = reinterpret_cast<uint64_t*>(sm + 8 * 4096 + 4 * 8192);
   uint32_t* tptr = reinterpret_cast<uint32_t*>(done + 1);
   const int tid = threadIdx.x, warp = tid >> 5;
-  const uint32_t rank = (MODE == 2) ? ctarank() : 0;
+  const uint32_t rank = (MODE >= 2) ? ctarank() : 0;
   for (int i = tid; i < (8 * 4096 + 4 * 8192) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01010101u * (i & 3);
   if (tid == 0) {
     mbar_init(done, 1);
@@ -46,7 +46,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) {
-    if (MODE == 2) {
+    if (MODE >= 2) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(s32(tptr)), "n"(512));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     } else {
@@ -55,13 +55,15 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
-  if (MODE == 2) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (MODE >= 2) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tptr;
-  const uint32_t M = (MODE == 2) ? 256 : 128;
-  const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((M >> 4) << 24);
-  const int nb = (MODE == 2) ? N / 2 : N;  // B rows staged per CTA
+  const uint32_t M = (MODE >= 2) ? 256 : 128;
+  const uint32_t idesc = MODE == 3
+      ? (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((M >> 4) << 24)
+      : (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((M >> 4) << 24);
+  const int nb = (MODE >= 2) ? N / 2 : N;  // B rows staged per CTA
   if (tid == 0 && rank == 0) {
     for (int it = 0; it < iters; ++it) {
       for (int q = 0; q < mmas_per_iter; ++q) {
@@ -75,13 +77,16 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
           const uint32_t ta = tmem + 256 + (uint32_t)((q & 7) * 8);  // A: 128 lanes x 8 columns
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n"
                        ::"r"(acc), "r"(ta), "l"(db), "r"(idesc), "r"(1u));
-        } else {
+        } else if (MODE == 2) {
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                       ::"r"(acc), "l"(da), "l"(db), "r"(idesc), "r"(1u));
+        } else {
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
                        ::"r"(acc), "l"(da), "l"(db), "r"(idesc), "r"(1u));
         }
       }
     }
-    if (MODE == 2)
+    if (MODE >= 2)
       asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(s32(done)), "h"((unsigned short)3) : "memory");
     else
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(s32(done)) : "memory");
@@ -94,10 +99,10 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
   asm volatile("tcgen05.wait::ld.sync.aligned;");
   if (v == 0x12345678u) sink[0] = v;
   asm volatile("tcgen05.fence::before_thread_sync;");
-  if (MODE == 2) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (MODE >= 2) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   else __syncthreads();
   if (warp == 0) {
-    if (MODE == 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+    if (MODE >= 2) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
     else asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
   }
 }
@@ -113,7 +118,7 @@ void run(unsigned long long* sink, int sms) {
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = (MODE == 2) ? 2 : 1;
+  at[0].val.clusterDim.x = (MODE >= 2) ? 2 : 1;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
@@ -130,10 +135,14 @@ void run(unsigned long long* sink, int sms) {
   float ms;
   cudaEventElapsedTime(&ms, t0, t1);
   cudaError_t e = cudaGetLastError();
-  const double ops_per_sm = 2.0 * 128 * N * KB * (double)iters * per;  // M per SM is 128
+  const double ops_per_sm = 2.0 * 128 * N * (MODE == 3 ? KB / 4 : KB) * (double)iters * per;  // M per SM is 128
   const double tops = ops_per_sm * sms / (ms * 1e-3) / 1e12;
-  printf("{\"mode\": \"%s\", \"N\": %d, \"status\": \"%s\", \"ms\": %.3f, \"int8_tops\": %.1f}\n",
-         MODE == 0 ? "cg1_SS" : MODE == 1 ? "cg1_TS" : "cg2_SS", N, cudaGetErrorString(e), ms, tops);
+  if (MODE == 3)
+    printf("{\"mode\": \"cg2_SS_tf32\", \"N\": %d, \"status\": \"%s\", \"ms\": %.3f, \"tf32_tflops\": %.1f}\n",
+           N, cudaGetErrorString(e), ms, tops);
+  else
+    printf("{\"mode\": \"%s\", \"N\": %d, \"status\": \"%s\", \"ms\": %.3f, \"int8_tops\": %.1f}\n",
+           MODE == 0 ? "cg1_SS" : MODE == 1 ? "cg1_TS" : "cg2_SS", N, cudaGetErrorString(e), ms, tops);
 }
 
 
@@ -245,6 +254,8 @@ int main() {
   run<2, 64>(sink, sms);
   run<2, 128>(sink, sms);
   run<2, 256>(sink, sms);
+  run<3, 128>(sink, sms);
+  run<3, 256>(sink, sms);
   run_seq<0>(sink, sms);
   run_seq<1>(sink, sms);
   run_seq<2>(sink, sms);
