@@ -946,7 +946,7 @@ int mhar_ctx_destroy(mhar_ctx* c) {
     double tot = 0, te = 0, tf = 0, tp = 0, emp = 0, ed = 0, es = 0, ew = 0;
     int n = 0;
     double atom = 0;
-    (void)atom;
+    for (int b = 1; b < c->num_sms; b += 2) atom += h[8 * b + 3];
     for (int b = 0; b < c->num_sms; b += 2) {
       if (!h[8 * b]) continue;
       tot += h[8 * b]; te += h[8 * b + 1]; tf += h[8 * b + 2]; tp += h[8 * b + 3];
@@ -957,9 +957,9 @@ int mhar_ctx_destroy(mhar_ctx* c) {
     if (n)
       std::fprintf(stderr, "[i8 profile] leaders %d: total %.3g cyc; MMA waits tempty %.1f%% full %.1f%% "
                    "peer %.1f%%; producer waits empty %.1f%%; epilogue drains %.1f%% stream %.1f%% "
-                   "idle %.1f%%%s\n", n, tot / n, 100 * te / tot,
+                   "idle %.1f%%; odd-CTA stream waits for staged chunks %.1f%%\n", n, tot / n, 100 * te / tot,
                    100 * tf / tot, 100 * tp / tot, 100 * emp / tot, 100 * ed / tot, 100 * es / tot,
-                   100 * ew / tot, "");
+                   100 * ew / tot, 100 * atom / tot);
   }
   for (auto& ev : c->pending) {
     cudaEventDestroy(ev.first);

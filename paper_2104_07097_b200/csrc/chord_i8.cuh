@@ -239,6 +239,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         int64_t rt, wp;
         i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
+        {
+          // stage this unit's slack/rate blocks (2 x 128 KB) in L2 two passes
+          // ahead of the loader's bulk copies to smem
+          const int64_t cb = (rt * p.walk_tiles + wt) * (int64_t)(I8_N * I8_M);
+          for (int q = 0; q < 8; ++q) {
+            bulk_prefetch_l2(p.S + cb + q * 2048, 2048 * 8);
+            bulk_prefetch_l2(p.R + cb + q * 2048, 2048 * 8);
+          }
+        }
         for (int pi = 0; pi < 2; ++pi)  // the long pass (levels 4..7) first
           for (int ks = 0; ks < KS; ++ks)
             for (int half = 0; half <= 1 - pi; ++half) {  // slot a: slices 0..3, b: 4..6
@@ -394,6 +403,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       const int64_t r0 = rt * I8_N + rq * I8_ROWS_PER_WARP;
       const double th = p.theta_prev[c];
       const double cs = p.csc[c];
+      // the bounds other units already reduced: the exact division filter
+      // then divides only for rows that can still move them (read now, used
+      // after the drains; a stale value is still a valid bound)
+      const long long hk0 = *(volatile long long*)(p.hi_key + c);
+      const long long lk0 = *(volatile long long*)(p.lo_key + c);
       __syncwarp();
       wrsc[lane] = __ldg(p.rsc + r0 + lane);
       __syncwarp();
@@ -442,15 +456,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       long long e4 = clock64();
       // slack update + chord scan (as chord2_kernel<INCREMENTAL>) on the staged
       // slack/rate chunks, overlapping the next unit's MMAs
-      double hi = INFINITY, lo = -INFINITY, viol = -INFINITY;
+      double hi = keyd(hk0), lo = keyd(lk0), viol = -INFINITY;
       unsigned sd = 0u;
+      long long wsr = 0;
       const int64_t sbase = ((rt * p.walk_tiles + wt) * I8_N + rq * I8_ROWS_PER_WARP) * I8_M + wl;
       double* __restrict__ Sout = p.S + sbase;
       double* __restrict__ Rout = p.R + sbase;
 #pragma unroll
       for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j) {
         const int slot = 2 * rq + (j & 1);
+        const long long w0 = clock64();
         mbar_wait(&sr_full[slot], (uint32_t)((j / 2) & 1));
+        wsr += clock64() - w0;
         const double* sS = sr + (size_t)slot * 2 * (I8_SR_CHUNK / 8) + wl;
         const double* sR = sS + I8_SR_CHUNK / 8;
         double sv[I8_SR_ROWS], av[I8_SR_ROWS];
@@ -480,6 +497,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         pr[5] += (unsigned long long)((e2 - e1) + (e4 - e3));  // drains
         pr[6] += (unsigned long long)(e5 - e4);                 // stream + scan
         pr[7] += (unsigned long long)((e1 - e0) + (e3 - e2));  // waiting for the MMAs
+        pr[3] += (unsigned long long)wsr;  // (odd CTAs) waiting for staged slack/rate chunks
       }
       if (c < p.z) {
         const long long vk = dkey(viol), hk = dkey(hi), lk = dkey(lo);
