@@ -284,6 +284,8 @@ int launch_tc32(mhar_ctx* c) {
   p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 2e-5;
   p.group_n = c->tc_group_n;
   p.a_policy = c->tc_a_policy;
+  p.prof = c->i8_prof;
+  if (c->i8_prof) cudaMemsetAsync(c->i8_prof, 0, 10 * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);  // (row tile, walk-tile pair)
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);  // CTA pairs
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
@@ -323,7 +325,7 @@ int launch_i8(mhar_ctx* c) {
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
   p.prof = c->i8_prof;
-  if (c->i8_prof) cudaMemsetAsync(c->i8_prof, 0, 8 * sizeof(unsigned long long) * c->num_sms, c->stream);
+  if (c->i8_prof) cudaMemsetAsync(c->i8_prof, 0, 10 * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
@@ -832,6 +834,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TC_SMEM);
+      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->i8_prof, 10 * (size_t)c->num_sms))) {
+        cudaFree(tmp);
+        return bail(st);
+      }
     }
     if (i8) {
       // A_I as 7 int8 slices of its per-row 53-bit fixed point
@@ -853,7 +859,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)I8_SMEM);
-      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->i8_prof, 8 * (size_t)c->num_sms))) {
+      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->i8_prof, 10 * (size_t)c->num_sms))) {
         cudaFree(tmp);
         return bail(st);
       }
@@ -940,9 +946,42 @@ int mhar_ctx_destroy(mhar_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->i8_prof) {  // debugging aid: cluster residency of the tcgen05 kernels
+    for (int which = 0; which < 2; ++which) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(148);
+      cfg.blockDim = dim3(which ? I8_THREADS : TC_THREADS);
+      cfg.dynamicSmemBytes = which ? I8_SMEM : TC_SMEM;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = -1;
+      cudaError_t e = which ? cudaOccupancyMaxActiveClusters(&ncl, chord_i8_kernel, &cfg)
+                            : cudaOccupancyMaxActiveClusters(&ncl, chord_tc32_kernel, &cfg);
+      std::fprintf(stderr, "[tcgen05 profile] %s: max active clusters of 2 = %d (%s)\n",
+                   which ? "chord_i8_kernel" : "chord_tc32_kernel", ncl, cudaGetErrorString(e));
+    }
+  }
   if (c->i8_prof) {  // debugging aid: where the int8 engine's MMA issuer and producer wait
-    std::vector<unsigned long long> h(8 * (size_t)c->num_sms);
+    std::vector<unsigned long long> h(10 * (size_t)c->num_sms);
     cudaMemcpy(h.data(), c->i8_prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    {
+      unsigned long long lo_in = ~0ull, hi_in = 0, lo_out = ~0ull, hi_out = 0;
+      for (int b = 0; b < c->num_sms; ++b) {
+        const unsigned long long gi = h[8 * c->num_sms + 2 * b], go = h[8 * c->num_sms + 2 * b + 1];
+        if (!gi) continue;
+        lo_in = std::min(lo_in, gi); hi_in = std::max(hi_in, gi);
+        lo_out = std::min(lo_out, go); hi_out = std::max(hi_out, go);
+      }
+      if (hi_out)
+        std::fprintf(stderr, "[tcgen05 profile] CTA entry spread %.3f ms, exit spread %.3f ms, "
+                     "first entry -> last exit %.3f ms\n", (hi_in - lo_in) * 1e-6,
+                     (hi_out - lo_out) * 1e-6, (hi_out - lo_in) * 1e-6);
+    }
     double tot = 0, te = 0, tf = 0, tp = 0, emp = 0, ed = 0, es = 0, ew = 0;
     int n = 0;
     double atom = 0;
@@ -955,7 +994,7 @@ int mhar_ctx_destroy(mhar_ctx* c) {
       ++n;
     }
     if (n)
-      std::fprintf(stderr, "[i8 profile] leaders %d: total %.3g cyc; MMA waits tempty %.1f%% full %.1f%% "
+      std::fprintf(stderr, "[tcgen05 profile] leaders %d: total %.3g cyc; MMA waits tempty %.1f%% full %.1f%% "
                    "peer %.1f%%; producer waits empty %.1f%%; epilogue drains %.1f%% stream %.1f%% "
                    "idle %.1f%%; odd-CTA stream waits for staged chunks %.1f%%\n", n, tot / n, 100 * te / tot,
                    100 * tf / tot, 100 * tp / tot, 100 * emp / tot, 100 * ed / tot, 100 * es / tot,

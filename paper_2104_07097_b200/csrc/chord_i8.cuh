@@ -44,6 +44,9 @@
 
 namespace mhar_dev {
 
+#ifndef MHAR_I8_PREFETCH
+#define MHAR_I8_PREFETCH 0
+#endif
 constexpr int I8_M = 128;       // walks per CTA (unit: 2 x 128)
 constexpr int I8_N = 128;       // rows per unit
 constexpr int I8_NH = 64;       // rows staged by each CTA of the pair
@@ -59,7 +62,7 @@ constexpr int I8_D_STAGE = I8_SLICES * I8_D_PIECE;  // 28 KB: one k step of dire
 constexpr int I8_SLOT_SLICES = 4;
 constexpr int I8_SLOT = I8_SLOT_SLICES * (I8_D_PIECE + I8_A_PIECE);  // 24 KB
 constexpr int I8_SLOT_A = I8_SLOT_SLICES * I8_D_PIECE;               // A slices at +16 KB
-constexpr int I8_STAGES = 6;
+constexpr int I8_STAGES = 7;
 // Warp roles: warpgroup 0 = warp 0 bulk-copy producer, warp 1 TMEM allocation
 // + MMA issuer (even CTA) / stage relay (odd CTA), warp 2 slack/rate loader,
 // warp 3 idle -- they drop to 32 registers (setmaxnreg) so that the 16
@@ -74,7 +77,8 @@ constexpr int I8_CTRL_REGS = 32, I8_EPI_REGS = 112;  // 128 x 32 + 512 x 112 = 6
 // (4 KB of S + 4 KB of R) per slot, two slots per row quarter.
 constexpr int I8_SR_ROWS = 4;
 constexpr int I8_SR_CHUNK = I8_SR_ROWS * I8_M * 8;  // bytes of S (or R) per slot
-constexpr int I8_SR_SLOTS = 8;
+constexpr int I8_SR_PER_GROUP = 1;  // staging slots per row quarter
+constexpr int I8_SR_SLOTS = 4 * I8_SR_PER_GROUP;
 constexpr size_t I8_SR_OFF = (size_t)I8_STAGES * I8_SLOT;
 constexpr size_t I8_RSC_OFF = I8_SR_OFF + (size_t)I8_SR_SLOTS * 2 * I8_SR_CHUNK;  // per-warp row scales
 constexpr size_t I8_BAR_OFF = I8_RSC_OFF + (size_t)I8_EPI_WARPS * I8_ROWS_PER_WARP * 8;
@@ -239,6 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         int64_t rt, wp;
         i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
+#if MHAR_I8_PREFETCH
         {
           // stage this unit's slack/rate blocks (2 x 128 KB) in L2 two passes
           // ahead of the loader's bulk copies to smem
@@ -248,6 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
             bulk_prefetch_l2(p.R + cb + q * 2048, 2048 * 8);
           }
         }
+#endif
         for (int pi = 0; pi < 2; ++pi)  // the long pass (levels 4..7) first
           for (int ks = 0; ks < KS; ++ks)
             for (int half = 0; half <= 1 - pi; ++half) {  // slot a: slices 0..3, b: 4..6
@@ -365,8 +371,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         const int64_t cb = (rt * p.walk_tiles + wt) * (int64_t)(I8_N * I8_M);
         for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j)
           for (int g = 0; g < 4; ++g) {  // row quarter g's j-th chunk
-            const int slot = 2 * g + (j & 1);
-            const int use = (I8_ROWS_PER_WARP / I8_SR_ROWS / 2) * ui + j / 2;
+            const int slot = I8_SR_PER_GROUP * g + j % I8_SR_PER_GROUP;
+            const int use = (I8_ROWS_PER_WARP / I8_SR_ROWS / I8_SR_PER_GROUP) * ui + j / I8_SR_PER_GROUP;
             if (use >= 1) mbar_wait(&sr_empty[slot], (uint32_t)((use - 1) & 1));
             uint8_t* dst = smem_raw + I8_SR_OFF + (size_t)slot * 2 * I8_SR_CHUNK;
             const int64_t off = cb + (int64_t)(g * I8_ROWS_PER_WARP + j * I8_SR_ROWS) * I8_M;
@@ -464,9 +470,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       double* __restrict__ Rout = p.R + sbase;
 #pragma unroll
       for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j) {
-        const int slot = 2 * rq + (j & 1);
+        const int slot = I8_SR_PER_GROUP * rq + j % I8_SR_PER_GROUP;
         const long long w0 = clock64();
-        mbar_wait(&sr_full[slot], (uint32_t)((j / 2) & 1));
+        mbar_wait(&sr_full[slot],
+                  (uint32_t)(((I8_ROWS_PER_WARP / I8_SR_ROWS / I8_SR_PER_GROUP) * ui +
+                              j / I8_SR_PER_GROUP) & 1));
         wsr += clock64() - w0;
         const double* sS = sr + (size_t)slot * 2 * (I8_SR_CHUNK / 8) + wl;
         const double* sR = sS + I8_SR_CHUNK / 8;

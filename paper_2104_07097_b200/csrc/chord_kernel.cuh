@@ -282,11 +282,18 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
           scan_row(sl, ad, p.eps_dir, hi[j][e], lo[j][e], sd[j][e]);
           if (MODE == FUSED_STORE) {
             const int64_t si = cache_index(r, c0[j] + 2 * (lane & 3) + e, p);
-            p.S[si] = sl;
-            if (p.rate_f32)  // the fp32 variant keeps its rates in fp32
+            if (p.rate_f32) {
+              // the fp32 variant keeps its rates in fp32 and its slack as a
+              // double-float pair (chord_tc32.cuh); +inf padding rows stay +inf
+              const float h = (float)sl;
+              const float l = isfinite(sl) ? (float)(sl - (double)h) : 0.0f;
+              const float2 v = make_float2(h, l);
+              p.S[si] = *reinterpret_cast<const double*>(&v);
               reinterpret_cast<float*>(p.R)[si] = (float)ad;
-            else
+            } else {
+              p.S[si] = sl;
               p.R[si] = ad;
+            }
           }
         }
     }

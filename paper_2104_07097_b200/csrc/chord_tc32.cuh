@@ -46,6 +46,13 @@ constexpr int TC_A_PIECE = TC_NH * TC_BK;  // floats per A_hi (or A_lo) half pie
 constexpr int TC_STAGE_FLOATS = TC_D_PIECE + 2 * TC_A_PIECE;  // 24 KB
 constexpr int TC_EPI_WARPS = 8;       // two per TMEM lane quarter, each owns half the rows
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
+#ifndef MHAR_TC_GROUP
+#define MHAR_TC_GROUP 16
+#endif
+#ifndef MHAR_TC_PREFETCH
+#define MHAR_TC_PREFETCH 0
+#endif
+constexpr int TC_GROUP = MHAR_TC_GROUP;  // epilogue rows per load group
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 512;
 
 // Interleaved K-major ("no swizzle") core-matrix layout of one (tile, k_tile)
@@ -161,6 +168,14 @@ __device__ inline void tc_ld32(uint32_t addr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// The fp32 variant's slack cache holds double-float pairs (hi, lo) in the
+// 8-byte slots: s = hi + lo with |lo| <= ulp(hi) / 2.
+__host__ __device__ inline double df_pack(float hi, float lo) {
+  const float2 v = make_float2(hi, lo);
+  return *reinterpret_cast<const double*>(&v);
+}
+__host__ __device__ inline float2 df_unpack(double d) { return *reinterpret_cast<const float2*>(&d); }
+
 struct TcParams {
   const float* Ahi;  // tc_a_index layout
   const float* Alo;
@@ -182,6 +197,7 @@ struct TcParams {
   double margin;       // mu: chords of {A x <= b - mu}
   int group_n;         // rasterisation band (row tiles)
   int a_policy;        // L2 policy of the A_hi/A_lo stream: 0 normal, 1 evict_last, 2 evict_first
+  unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
 };
 
 // unit u -> (row tile, walk-tile pair), banded over group_n row tiles
@@ -198,6 +214,8 @@ __device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     chord_tc32_kernel(const TcParams p) {
+  unsigned long long g_entry = 0;
+  if (p.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   if (*p.err != kNoError) return;  // read identically by both CTAs of the pair
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   float* ring = reinterpret_cast<float*>(smem_raw);
@@ -246,12 +264,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                             : p.a_policy == 2 ? policy_evict_first()
                                               : policy_evict_normal();
       int stage = 0, round = 0;
+      long long w_empty = 0;
       for (int ui = 0; ui < my_units; ++ui) {
         int64_t rt, wp;
         tc_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
+#if MHAR_TC_PREFETCH
+        {
+          // stage this unit's slack (256 KB) and rate (128 KB) blocks in L2 about
+          // one unit ahead of the epilogue
+          const int64_t cb = (rt * p.walk_tiles + wt) * (int64_t)(TC_N * TC_M);
+          for (int q = 0; q < 16; ++q) bulk_prefetch_l2(p.S + cb + q * 2048, 2048 * 8);
+          for (int q = 0; q < 8; ++q) bulk_prefetch_l2(p.R + cb + q * 4096, 4096 * 4);
+        }
+#endif
         for (int kt = 0; kt < KT; ++kt) {
+          const long long t0 = clock64();
           if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
+          w_empty += clock64() - t0;
           float* st = ring + (size_t)stage * TC_STAGE_FLOATS;
           mbar_arrive_expect_tx(&full[stage], TC_STAGE_FLOATS * 4);
           const int64_t doff = (wt * p.KT + kt) * TC_D_PIECE;
@@ -266,19 +296,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
         }
       }
+      if (p.prof) p.prof[8 * blockIdx.x + 4] = (unsigned long long)w_empty;
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
       // ---------------- MMA issuer (leader CTA) ----------------
       int stage = 0, phase = 0;
+      long long w_tempty = 0, w_full = 0, w_peer = 0;
+      const long long t_start = clock64();
       for (int ui = 0; ui < my_units; ++ui) {
         const int ab = ui & 1;
+        const long long t0 = clock64();
         if (ui >= 2) mbar_wait_relaxed(&tempty[ab], (uint32_t)(((ui >> 1) - 1) & 1));
+        w_tempty += clock64() - t0;
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t acc = tmem + (uint32_t)(ab * TC_N);
         for (int kt = 0; kt < KT; ++kt) {
+          const long long t1 = clock64();
           mbar_wait(&full[stage], (uint32_t)phase);
+          const long long t2 = clock64();
           mbar_wait_relaxed(&peer_full[stage], (uint32_t)phase);
+          w_full += t2 - t1;
+          w_peer += clock64() - t2;
           asm volatile("tcgen05.fence::after_thread_sync;");
           const float* sd = ring + (size_t)stage * TC_STAGE_FLOATS;
           const float* sa_hi = sd + TC_D_PIECE;
@@ -300,6 +339,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           }
         }
         tc_commit2(&tfull[ab]);
+      }
+      if (p.prof) {
+        unsigned long long* pr = p.prof + 8 * blockIdx.x;
+        pr[0] = (unsigned long long)(clock64() - t_start);
+        pr[1] = (unsigned long long)w_tempty;
+        pr[2] = (unsigned long long)w_full;
+        pr[3] = (unsigned long long)w_peer;
       }
     } else if (lane == 0) {
       // ---------------- relay (odd CTA): my stage landed -> leader ----------------
@@ -326,10 +372,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       tc_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
       const int64_t wt = 2 * wp + rank;
       const int ab = ui & 1;
+      const long long e0 = clock64();
       mbar_wait(&tfull[ab], (uint32_t)((ui >> 1) & 1));
+      const long long e1 = clock64();
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int64_t c = wt * TC_M + wl;
-      const double th = p.theta_prev[c];
+      // theta as a float pair: the slack update below runs in double-float
+      // (hi + lo, ~48 bits) on the fp32 pipes -- fp64 SIMT instructions issue
+      // on the pipe the tensor cores keep busy and stalled this epilogue
+      const double thd = p.theta_prev[c];
+      const float th_hi = (float)thd, th_lo = (float)(thd - (double)th_hi);
       float hi = __int_as_float(0x7F800000), lo = -hi, viol = -hi;
       unsigned sd = 0u;
       const int64_t sbase = (rt * p.walk_tiles + wt) * TC_N * TC_M + wl;
@@ -338,24 +390,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const float* __restrict__ Rin = p.R + sbase;
       double* __restrict__ Sout = p.S + sbase;
       float* __restrict__ Rout = p.R + sbase;
-      // 16 rows at a time: all loads of the group in flight before any store
-      // (the cache is read and rewritten in place).  Only the slack update is
-      // fp64; the ratio test runs on the fp32 pipes, branch-free -- the chord
-      // is already that of the body shrunk by mu >> fp32 rounding of s / ad.
-      auto rows16 = [&](int r0, const float* vv) {
-        double so[16];
-        float ro[16];
+      // 8 rows at a time: all loads of the group in flight before any store
+      // (the cache is read and rewritten in place).  The ratio test runs on
+      // the fp32 pipes, branch-free -- the chord is already that of the body
+      // shrunk by mu >> fp32 rounding of s / ad.
+      auto rows8 = [&](int r0, const float* vv) {
+        double so[TC_GROUP];
+        float ro[TC_GROUP];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
+        for (int j = 0; j < TC_GROUP; ++j) {
           so[j] = ld_policy(Sin + (int64_t)(r0 + j) * TC_M, stream_policy);
           ro[j] = ld_policy(Rin + (int64_t)(r0 + j) * TC_M, stream_policy);
         }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const double s = fma(-th, (double)ro[j], so[j]);
-          st_policy(Sout + (int64_t)(r0 + j) * TC_M, s, stream_policy);
+        for (int j = 0; j < TC_GROUP; ++j) {
+          // s = S - theta r in double-float: exact product error by FMA, TwoSum
+          const float2 sp = df_unpack(so[j]);
+          const float r = ro[j];
+          const float ph = __fmul_rn(th_hi, r);
+          const float pl = fmaf(th_lo, r, fmaf(th_hi, r, -ph));
+          const float a = __fsub_rn(sp.x, ph);
+          const float bb = __fsub_rn(a, sp.x);
+          const float er = __fadd_rn(__fsub_rn(sp.x, __fsub_rn(a, bb)), __fsub_rn(-ph, bb));
+          const float l = __fadd_rn(__fsub_rn(sp.y, pl), er);
+          const bool fin = fabsf(sp.x) < __int_as_float(0x7F800000);  // +inf: padding row
+          const float sh = fin ? __fadd_rn(a, l) : sp.x;
+          const float sl = fin ? __fsub_rn(l, __fsub_rn(sh, a)) : 0.0f;
+          st_policy(Sout + (int64_t)(r0 + j) * TC_M, df_pack(sh, sl), stream_policy);
           st_policy(Rout + (int64_t)(r0 + j) * TC_M, vv[j], stream_policy);
-          const float sf = (float)s, ad = vv[j];
+          const float sf = sh, ad = vv[j];
           viol = fmaxf(viol, -sf);
           const float qt = __fdividef(sf - mu, ad);
           const bool up = ad > eps, dn = ad < -eps;
@@ -367,8 +430,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       for (int c0 = rh * (TC_N / 2); c0 < (rh + 1) * (TC_N / 2); c0 += 32) {
         float v[32];
         tc_ld32(taddr + (uint32_t)c0, v);
-        rows16(c0, v);
-        rows16(c0 + 16, v + 16);
+#pragma unroll
+        for (int g = 0; g < 32; g += TC_GROUP) rows8(c0 + g, v + g);
       }
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
@@ -377,6 +440,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           mbar_arrive(&tempty[ab]);
         else
           mbar_arrive_remote(&tempty[ab], 0);
+      }
+      if (p.prof && warp == 2 && lane == 0) {
+        unsigned long long* pr = p.prof + 8 * blockIdx.x;
+        pr[6] += (unsigned long long)(clock64() - e1);  // drain + stream + scan
+        pr[7] += (unsigned long long)(e1 - e0);         // waiting for the MMAs
       }
       if (c < p.z) {
         const long long vk = dkey((double)viol), hk = dkey((double)hi), lk = dkey((double)lo);
@@ -391,6 +459,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync_all();  // all MMAs done and consumed in both CTAs before TMEM is freed
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(512));
+  if (p.prof && tid == 0) {
+    unsigned long long g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    p.prof[8 * gridDim.x + 2 * blockIdx.x] = g_entry;
+    p.prof[8 * gridDim.x + 2 * blockIdx.x + 1] = g_exit;
+  }
 }
 
 // fp64 polytope rows -> (A_hi, A_lo) with A_used = A_hi + A_lo written back

@@ -1,0 +1,6 @@
+libs=${LIBS:-"tools/ab_i8p1.so paper_2104_07097_b200/lib/libmhar_b200.so"}
+for i in 1 2 3; do
+  for lib in $libs; do
+    MHAR_LIB=$lib timeout 120 python bench.py --f64-engine int8 --no-i8 --no-fp32 --no-cpu --e2e-steps 1 --steps 10 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().splitlines()[-1]);print('$lib', round(d['roofline']['avg_launch_ms'],3), d['clocks']['sm_mhz'])"
+  done
+done
