@@ -37,21 +37,50 @@ constexpr int kThreads = 1024;
 // Single CTA: entering column (Dantzig: largest reduced cost > tol; Bland:
 // first such column), then the leaving row by the minimum-ratio test with
 // ties (within 1e-15) broken by the smallest basic column.
+// Pivot-loop control, resident on the device so a phase runs without host
+// round trips: the host enqueues batches of select+pivot launches and reads
+// `done` once per batch.
+struct Ctl {
+  int done;          // 1: the phase has ended; every queued launch returns at once
+  int status;        // 0 optimal, 7 unbounded ray, 10 pivot budget
+  int stall;         // consecutive degenerate pivots
+  int bland;         // Bland's rule after a degenerate stall (lp.cpp:47-98)
+  long long npiv;    // pivots of this solve
+  long long budget;  // 10^4 + 200 (rows + cols)
+  int stall_limit;   // rows + priced columns
+  int pad;
+};
+
 __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restrict__ T,
                                                           const double* __restrict__ b,
                                                           const double* __restrict__ cost,
                                                           const int* __restrict__ basis, int rows,
-                                                          int cols, int limit_col, int bland,
+                                                          int cols, int limit_col, Ctl* ctl,
                                                           int* out /* entering, leaving */,
-                                                          double* out_ratio) {
+                                                          double* prow, double* fcol,
+                                                          double* pb /* [b_row/piv, cost_col] */) {
   __shared__ double sv[kThreads / 32];
   __shared__ int si[kThreads / 32];
   __shared__ int s_enter;
   __shared__ double s_min;
+  __shared__ int s_go;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_go = !ctl->done && ctl->npiv < ctl->budget;
+  __syncthreads();
+  if (!s_go) {
+    if (tid == 0 && !ctl->done) {  // pivot budget exhausted
+      ctl->done = 1;
+      ctl->status = 10;
+    }
+    return;
+  }
+  const int bland = ctl->bland;
   // pricing
   double bv = bland ? 0.0 : kReducedCostTol;
   int bi = 0x7FFFFFFF;
+  // (loops unrolled so each thread has its loads in flight together: this
+  // single-CTA kernel is latency-bound)
+#pragma unroll 8
   for (int j = tid; j < limit_col; j += kThreads) {
     const double c = cost[j];
     if (bland) {
@@ -82,14 +111,21 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
       }
     s_enter = (bi == 0x7FFFFFFF) ? -1 : bi;
     out[0] = s_enter;
+    if (s_enter < 0) {  // optimal
+      ctl->done = 1;
+      ctl->status = 0;
+    }
   }
   __syncthreads();
   const int e = s_enter;
   if (e < 0) return;
-  // ratio test, pass 1: minimum ratio
+  // ratio test, pass 1: minimum ratio; the entering column (one strided
+  // sector per row) is cached in fcol for pass 2 and the rank-1 update
   double mr = __longlong_as_double(0x7FF0000000000000LL);
+#pragma unroll 4
   for (int i = tid; i < rows; i += kThreads) {
     const double a = T[(size_t)i * cols + e];
+    fcol[i] = a;
     if (a > kPivotTol) mr = fmin(mr, b[i] / a);
   }
   for (int o = 16; o > 0; o >>= 1) mr = fmin(mr, __shfl_xor_sync(0xFFFFFFFFu, mr, o));
@@ -104,8 +140,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
   const double lim = s_min + 1e-15;
   int best_basic = 0x7FFFFFFF, best_row = -1;
   if (s_min < __longlong_as_double(0x7FF0000000000000LL)) {
+#pragma unroll 4
     for (int i = tid; i < rows; i += kThreads) {
-      const double a = T[(size_t)i * cols + e];
+      const double a = fcol[i];
       if (a > kPivotTol && b[i] / a <= lim && basis[i] < best_basic) {
         best_basic = basis[i];
         best_row = i;
@@ -132,8 +169,40 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
         best_row = si[w];
       }
     out[1] = best_row;
-    *out_ratio = s_min;
+    if (best_row < 0) {  // unbounded ray
+      ctl->done = 1;
+      ctl->status = 7;
+    } else {
+      if (s_min < kDegenerateStep) {
+        if (++ctl->stall > ctl->stall_limit) ctl->bland = 1;
+      } else {
+        ctl->stall = 0;
+      }
+      ++ctl->npiv;
+    }
+    si[0] = best_row;
   }
+  __syncthreads();
+  const int row = si[0];
+  if (row < 0) return;
+  // capture for the rank-1 update (fcol = T[:,e] is cached above; the pivot
+  // row is divided out by prow_kernel on the whole grid)
+  if (tid == 0) {
+    const double piv = fcol[row];
+    pb[0] = b[row] / piv;
+    pb[1] = cost[e];
+  }
+}
+
+// prow = T[row,:] / T[row,col] for the pivot the select kernel chose
+__global__ void prow_kernel(const double* __restrict__ T, int cols, const int* __restrict__ sel,
+                            const int* __restrict__ done, const double* __restrict__ fcol,
+                            double* __restrict__ prow) {
+  if (*done) return;
+  const int row = sel[1];
+  const double piv = fcol[row];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+    prow[j] = T[(size_t)row * cols + j] / piv;
 }
 
 // pivot on (row, col): prow = T[row,:]/piv, fcol = T[:,col] captured first
@@ -145,45 +214,61 @@ __global__ void capture_kernel(const double* __restrict__ T, const double* __res
     prow[j] = T[(size_t)row * cols + j] / piv;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
     fcol[i] = T[(size_t)i * cols + col];
-  if (blockIdx.x == 0 && threadIdx.x == 0) *pb = b[row] / piv;
-}
-
-__global__ void pivot_kernel(double* __restrict__ T, double* __restrict__ b,
-                             double* __restrict__ cost, int* basis, int rows, int cols, int row,
-                             int col, const double* __restrict__ prow,
-                             const double* __restrict__ fcol, const double* pb) {
-  // blockIdx.y walks tableau rows (rows == the cost row), x-threads columns
-  const double brow = *pb;
-  const double cf = cost[col];  // nobody writes cost[col] in this launch
-  for (int i = blockIdx.y; i <= rows; i += gridDim.y) {
-    if (i == rows) {
-      if (cf != 0.0)
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
-          if (j != col) cost[j] -= cf * prow[j];
-      continue;
-    }
-    double* Ti = T + (size_t)i * cols;
-    if (i == row) {
-      for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
-        Ti[j] = prow[j];
-    } else {
-      const double f = fcol[i];
-      if (f != 0.0)
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
-          Ti[j] -= f * prow[j];
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-      if (i == row) {
-        b[i] = brow;
-        basis[i] = col;
-      } else if (fcol[i] != 0.0) {
-        b[i] -= fcol[i] * brow;
-      }
-    }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    pb[0] = b[row] / piv;
+    pb[1] = 0.0;  // drive-out pivots run without a cost row
   }
 }
 
-__global__ void zero_cost_col_kernel(double* cost, int col) { cost[col] = 0.0; }
+// sel <- (col, row) for a host-chosen pivot
+__global__ void set_sel_kernel(int* sel, int row, int col) {
+  sel[0] = col;
+  sel[1] = row;
+}
+
+__global__ void __launch_bounds__(256) pivot_kernel(double* __restrict__ T, double* __restrict__ b,
+                                                    double* __restrict__ cost, int* basis, int rows,
+                                                    int cols, const int* __restrict__ sel,
+                                                    const int* __restrict__ done,
+                                                    const double* __restrict__ prow,
+                                                    const double* __restrict__ fcol,
+                                                    const double* pb) {
+  // one block per tableau row (blockIdx.x == rows: the cost row); rows are
+  // 16-byte aligned (even column stride), updated as double2
+  if (*done) return;
+  const int col = sel[0], row = sel[1];
+  const double brow = pb[0];
+  const double cf = pb[1];  // cost[col] before this pivot (captured)
+  const int i = blockIdx.x;
+  const int c2 = cols >> 1;
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(prow);
+  if (i == rows) {
+    if (cf != 0.0)
+      for (int j = threadIdx.x; j < cols; j += blockDim.x)
+        cost[j] = (j == col) ? 0.0 : cost[j] - cf * prow[j];
+    return;
+  }
+  double2* __restrict__ Ti = reinterpret_cast<double2*>(T + (size_t)i * cols);
+  if (i == row) {
+    for (int j = threadIdx.x; j < c2; j += blockDim.x) Ti[j] = __ldg(p2 + j);
+    if (threadIdx.x == 0) {
+      b[i] = brow;
+      basis[i] = col;
+    }
+    return;
+  }
+  const double f = fcol[i];
+  if (f == 0.0) return;
+#pragma unroll 4
+  for (int j = threadIdx.x; j < c2; j += blockDim.x) {
+    double2 t = Ti[j];
+    const double2 q = __ldg(p2 + j);
+    t.x = fma(-f, q.x, t.x);
+    t.y = fma(-f, q.y, t.y);
+    Ti[j] = t;
+  }
+  if (threadIdx.x == 0) b[i] -= f * brow;
+}
 
 // v_i = a_i x + |a_i| r - b_i over all rows (A column-major m x n)
 __global__ void violation_kernel(const double* __restrict__ A, const double* __restrict__ norms,
@@ -202,7 +287,8 @@ __global__ void violation_kernel(const double* __restrict__ A, const double* __r
 struct Dev {
   double *T = nullptr, *b = nullptr, *cost = nullptr, *prow = nullptr, *fcol = nullptr;
   double *pb = nullptr, *ratio = nullptr;
-  int *basis = nullptr, *sel = nullptr;
+  int *basis = nullptr, *sel = nullptr, *zero = nullptr;
+  Ctl* ctl = nullptr;
   cudaStream_t s = nullptr;
   ~Dev() {
     cudaFree(T);
@@ -214,6 +300,8 @@ struct Dev {
     cudaFree(ratio);
     cudaFree(basis);
     cudaFree(sel);
+    cudaFree(zero);
+    cudaFree(ctl);
     if (s) cudaStreamDestroy(s);
   }
 };
@@ -253,7 +341,7 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
     if (is_eq[i] || sgn[i] < 0) ++nart;
   }
   const int total = structural + nart;  // priced columns
-  const int W = total + 1;              // + the unperturbed rhs column
+  const int W = (total + 2) & ~1;       // + the unperturbed rhs column, even (16-byte rows)
   std::vector<double> T((size_t)m * W, 0.0), b(m);
   std::vector<int> basis(m, -1);
   int slack = ncols, art = structural;
@@ -287,47 +375,53 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
       !ok(cudaMalloc(&d.T, sizeof(double) * T.size())) ||
       !ok(cudaMalloc(&d.b, sizeof(double) * m)) || !ok(cudaMalloc(&d.cost, sizeof(double) * W)) ||
       !ok(cudaMalloc(&d.prow, sizeof(double) * W)) ||
-      !ok(cudaMalloc(&d.fcol, sizeof(double) * m)) || !ok(cudaMalloc(&d.pb, sizeof(double))) ||
+      !ok(cudaMalloc(&d.fcol, sizeof(double) * m)) || !ok(cudaMalloc(&d.pb, 2 * sizeof(double))) ||
+      !ok(cudaMalloc(&d.zero, sizeof(int))) || !ok(cudaMalloc(&d.ctl, sizeof(Ctl))) ||
       !ok(cudaMalloc(&d.ratio, sizeof(double))) || !ok(cudaMalloc(&d.basis, sizeof(int) * m)) ||
       !ok(cudaMalloc(&d.sel, sizeof(int) * 2)))
     return err(msg, 100, "simplex: device allocation failed");
   cudaMemcpyAsync(d.T, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice, d.s);
   cudaMemcpyAsync(d.b, b.data(), sizeof(double) * m, cudaMemcpyHostToDevice, d.s);
   cudaMemcpyAsync(d.basis, basis.data(), sizeof(int) * m, cudaMemcpyHostToDevice, d.s);
+  cudaMemsetAsync(d.zero, 0, sizeof(int), d.s);
 
   const long budget = 10000 + 200L * (m + total);
   long npiv = 0;
   int rows = m;
+  auto pivot_launch = [&](const int* done) {
+    pivot_kernel<<<rows + 1, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, d.sel, done,
+                                             d.prow, d.fcol, d.pb);
+  };
+  // a host-chosen pivot (artificials driven out after phase one)
   auto pivot = [&](int row, int col) {
+    set_sel_kernel<<<1, 1, 0, d.s>>>(d.sel, row, col);
     capture_kernel<<<std::max(1, std::min(1024, (std::max(rows, W) + 255) / 256)), 256, 0, d.s>>>(
         d.T, d.b, rows, W, row, col, d.prow, d.fcol, d.pb);
-    const dim3 g((unsigned)std::min(8, (W + 255) / 256), (unsigned)std::min(rows + 1, 65535));
-    pivot_kernel<<<g, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, row, col, d.prow, d.fcol,
-                                     d.pb);
-    zero_cost_col_kernel<<<1, 1, 0, d.s>>>(d.cost, col);
+    pivot_launch(d.zero);
     ++npiv;
   };
-  // one phase: 0 optimal, 7 unbounded ray, 10 budget, 100 CUDA
+  // one phase, driven on the device: 0 optimal, 7 unbounded ray, 10 budget, 100 CUDA
   auto run_phase = [&](int limit_col) -> int {
-    int stall = 0;
-    bool bland = false;
+    Ctl h{};
+    h.budget = budget - npiv;
+    h.stall_limit = rows + total;
+    cudaMemcpyAsync(d.ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, d.s);
+    int batch = 8;
     for (;;) {
-      select_kernel<<<1, kThreads, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, limit_col,
-                                             bland ? 1 : 0, d.sel, d.ratio);
-      int sel[2];
-      double ratio;
-      cudaMemcpyAsync(sel, d.sel, sizeof(sel), cudaMemcpyDeviceToHost, d.s);
-      cudaMemcpyAsync(&ratio, d.ratio, sizeof(double), cudaMemcpyDeviceToHost, d.s);
-      if (cudaStreamSynchronize(d.s) != cudaSuccess) return 100;
-      if (sel[0] < 0) return 0;
-      if (sel[1] < 0) return 7;
-      if (ratio < kDegenerateStep) {
-        if (++stall > rows + total) bland = true;
-      } else {
-        stall = 0;
+      for (int k = 0; k < batch; ++k) {
+        select_kernel<<<1, kThreads, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, limit_col,
+                                               d.ctl, d.sel, d.prow, d.fcol, d.pb);
+        prow_kernel<<<std::max(1, std::min(64, (W + 255) / 256)), 256, 0, d.s>>>(
+            d.T, W, d.sel, &d.ctl->done, d.fcol, d.prow);
+        pivot_launch(&d.ctl->done);
       }
-      pivot(sel[1], sel[0]);
-      if (npiv > budget) return 10;
+      cudaMemcpyAsync(&h, d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, d.s);
+      if (cudaStreamSynchronize(d.s) != cudaSuccess) return 100;
+      if (h.done) {
+        npiv += h.npiv;
+        return h.status;
+      }
+      batch = std::min(batch * 2, 256);
     }
   };
   auto fetch_row = [&](int i, double* dst) {

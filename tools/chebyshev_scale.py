@@ -4,7 +4,9 @@ import json
 import sys
 import time
 
+import os
 import numpy as np
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import paper_2104_07097_b200 as mh
 from paper_2104_07097_b200 import workloads
