@@ -44,7 +44,10 @@ constexpr int STAGE_DOUBLES = A_PIECE + 2 * B_PIECE;
 constexpr size_t CHORD_SMEM = (size_t)CHORD_STAGES * STAGE_DOUBLES * sizeof(double) + 1024;
 // INCREMENTAL / CHECK kernel (2 CTAs / SM)
 constexpr int CHORD2_STAGES = 4;  // 4 x 24 KB ring per CTA
-constexpr int CHORD2_LAG = 1;
+#ifndef MHAR_CHORD2_LAG
+#define MHAR_CHORD2_LAG 1
+#endif
+constexpr int CHORD2_LAG = MHAR_CHORD2_LAG;
 constexpr int STAGE2_DOUBLES = A_PIECE + B_PIECE;
 constexpr size_t CHORD2_SMEM = (size_t)CHORD2_STAGES * STAGE2_DOUBLES * sizeof(double) + 256;
 
