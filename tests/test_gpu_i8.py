@@ -164,3 +164,59 @@ def test_contexts_alive_together_do_not_interfere():
     his = {round(h, 9) for _, h in seen}
     los = {l for l, _ in seen if l is not None}
     assert len(his) == 1 and len(los) == 1
+
+
+def test_i8_injected_step_with_equalities(orc):
+    # config 4 shape (n = 1000, m_I = 52000 with the box rows, m_E = 100):
+    # D = P H is projected, then quantised; one step vs the oracle at 1e-9
+    from paper_2104_07097_b200 import workloads as wl
+    w = wl.config(4)
+    p = w.polytope
+    z = 128
+    rng = np.random.default_rng(44)
+    op = mh.compute_projection(p.a_eq)
+    X = np.asfortranarray(op.p @ rng.uniform(-0.02, 0.02, (p.dim(), z)))
+    H = np.asfortranarray(rng.standard_normal((p.dim(), z)))
+    U = rng.uniform(0, 1, z)
+    with mh.Engine(p, z, projector=op, f64_engine="int8") as eng:
+        eng.set_state(X)
+        lo, hi, th, fl = eng.step_injected(H, U)
+        Xg = eng.get_state()
+    st, Xr, lor, hir, thr, flr, _ = orc.step_injected(p.a_in, p.b_in, op.p, EPS_DIR, X, H, U)
+    assert st == 0
+    np.testing.assert_array_equal(fl, flr)
+    ok = (flr & mh.FLAG_DEGENERATE) == 0
+    w_ = np.where(ok, hir - lor, 1.0)
+    assert np.all(np.abs(lo - lor)[ok] <= RTOL * w_[ok])
+    assert np.all(np.abs(hi - hir)[ok] <= RTOL * w_[ok])
+    assert np.abs(Xg - Xr).max() <= RTOL * np.abs(Xr).max()
+
+
+def test_i8_run_simplex_moments_and_drift():
+    # simplex(6) with the equality sum x = 1: reprojection cadence, moments
+    p = mh.make_simplex(6)
+    op = mh.compute_projection(p.a_eq)
+    with mh.Engine(p, 256, seed=21, projector=op, f64_engine="int8") as eng:
+        S, st = eng.run(np.full(6, 1.0 / 6), phi=30, windows=20, burn_in=60, reproject_every=30)
+    assert np.abs(S.sum(1) - 1.0).max() <= 1e-9
+    assert (S @ p.a_in.T - p.b_in).max() <= 1e-9
+    assert np.abs(S.mean(0) - 1.0 / 6).max() <= 0.02
+
+
+def test_i8_redraw_keeps_the_rate_cache_consistent():
+    # eps_dir 0.6 on box(8): directions with every |d_i| <= 0.6 are degenerate
+    # and redrawn from the walk's own stream; the redrawn walk's rates go into
+    # the tile-layout fp64 cache.  The incremental int8 engine must follow the
+    # DMMA engine that recomputes the slack every iterate (with eps this large
+    # walks may leave the box -- the reference skips rows with |a d| <= eps --
+    # so the check is trajectory agreement, over a few iterates).
+    p = mh.make_hypercube(8)
+    out = {}
+    for name, kw in [("int8", dict(f64_engine="int8", refresh_every=1000)),
+                     ("dmma", dict(slack="recompute"))]:
+        with mh.Engine(p, 256, seed=3, eps_dir=0.6, **kw) as eng:
+            eng.set_state(np.zeros((8, 256)))
+            eng.step(4)
+            out[name] = (eng.get_state(), eng.stats()["redraw_count"])
+    assert out["int8"][1] > 0 and out["int8"][1] == out["dmma"][1]
+    assert np.abs(out["int8"][0] - out["dmma"][0]).max() <= 1e-9
