@@ -44,6 +44,9 @@
 
 namespace mhar_dev {
 
+#ifndef MHAR_I8_EXPERIMENT
+#define MHAR_I8_EXPERIMENT 0
+#endif
 #ifndef MHAR_I8_PREFETCH
 #define MHAR_I8_PREFETCH 0
 #endif
@@ -263,12 +266,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
               if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
               w_empty += clock64() - t0;
               uint8_t* st = ring + (size_t)stage * I8_SLOT;
+#if MHAR_I8_EXPERIMENT == 1  // timing experiment only: skip the D slices (wrong results)
+              mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * I8_A_PIECE));
+#elif MHAR_I8_EXPERIMENT == 2  // timing experiment only: skip the A slices (wrong results)
+              mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * I8_D_PIECE));
+#else
               mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * (I8_D_PIECE + I8_A_PIECE)));
+#endif
               const int64_t doff = (wt * p.KS + ks) * (int64_t)I8_D_STAGE + s0 * I8_D_PIECE;
               const int64_t aoff =
                   ((rt * p.KS + ks) * 2 + rank) * (int64_t)(I8_SLICES * I8_A_PIECE) + s0 * I8_A_PIECE;
+#if MHAR_I8_EXPERIMENT != 1
               bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
+#endif
+#if MHAR_I8_EXPERIMENT != 2
               bulk_g2s_hint(st + I8_SLOT_A, p.A8 + aoff, ns * I8_A_PIECE, &full[stage], apol);
+#endif
               if (++stage == I8_STAGES) {
                 stage = 0;
                 ++round;
