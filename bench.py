@@ -469,6 +469,14 @@ def run_engine(args, world, rank, local):
                "sample": f"{args.cpu_walks} walks x {args.cpu_iters} iterates of the same polytope "
                          f"({dt:.1f} s; oracle/mhar_oracle.c restating proj/src/sampler.cpp, "
                          f"OpenMP AVX-512 GEMM)"}
+        if args.cpu_walks_1core > 0:
+            # the reference itself is single-threaded (no OpenMP):
+            # the same port on one core, smaller sample
+            v1, dt1 = cpu_sample(w, args.cpu_walks_1core, args.cpu_iters_1core, 1)
+            cpu["single_core"] = {
+                "value": v1, "cores": 1,
+                "sample": f"{args.cpu_walks_1core} walks x {args.cpu_iters_1core} iterates "
+                          f"({dt1:.1f} s)"}
     line = {
         "metric": METRIC, "value": value, "unit": "chain-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -532,6 +540,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-walks", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=24)
+    ap.add_argument("--cpu-walks-1core", type=int, default=32)
+    ap.add_argument("--cpu-iters-1core", type=int, default=4)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-variant measurement")
     ap.add_argument("--no-i8", action="store_true", help="skip the int8-slice fp64 engine")
