@@ -220,3 +220,21 @@ def test_i8_redraw_keeps_the_rate_cache_consistent():
             out[name] = (eng.get_state(), eng.stats()["redraw_count"])
     assert out["int8"][1] > 0 and out["int8"][1] == out["dmma"][1]
     assert np.abs(out["int8"][0] - out["dmma"][0]).max() <= 1e-9
+
+
+def test_i8_uniformity_screening_against_direct_draws():
+    # acceptance #3's screen (proj/tests/acceptance_main.cpp:160-203) on the
+    # int8 engine: box(8) samples vs direct uniform draws, 10 seeds, at least
+    # 9 runs with Friedman-Rafsky z >= -1.64
+    from paper_2104_07097_b200 import stats
+    n = 8
+    p = mh.make_hypercube(n)
+    ok = 0
+    for rep in range(10):
+        with mh.Engine(p, 256, seed=500 + rep, f64_engine="int8") as eng:
+            S, _ = eng.run(np.zeros(n), phi=64, windows=8, burn_in=64)
+        S = S[:2000]
+        ref = stats.sample_uniform_hypercube(np.random.default_rng(rep), n, 2000)
+        if stats.friedman_rafsky(S, ref).z_value >= stats.kUniformityZThreshold:
+            ok += 1
+    assert ok >= 9, f"{ok}/10"
