@@ -62,6 +62,8 @@ const char* code_name(int st) {
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
 
+constexpr int kProfWords = 10;  // per-CTA profile words (MHAR_I8_PROFILE)
+
 }  // namespace
 
 struct mhar_ctx {
@@ -102,7 +104,7 @@ struct mhar_ctx {
   double *rsc = nullptr, *csc = nullptr;
   int* rexp = nullptr;
   int64_t KS = 0, i8_row_tiles = 0;
-  unsigned long long* i8_prof = nullptr;  // MHAR_I8_PROFILE: per-CTA wait cycles of the last launch
+  unsigned long long* tc_prof = nullptr;  // MHAR_I8_PROFILE: tcgen05 kernels' per-CTA counters
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
   double* rows2 = nullptr;
   double* pinned[2] = {nullptr, nullptr};
@@ -284,8 +286,8 @@ int launch_tc32(mhar_ctx* c) {
   p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 2e-5;
   p.group_n = c->tc_group_n;
   p.a_policy = c->tc_a_policy;
-  p.prof = c->i8_prof;
-  if (c->i8_prof) cudaMemsetAsync(c->i8_prof, 0, 10 * sizeof(unsigned long long) * c->num_sms, c->stream);
+  p.prof = c->tc_prof;
+  if (c->tc_prof) cudaMemsetAsync(c->tc_prof, 0, kProfWords * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);  // (row tile, walk-tile pair)
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);  // CTA pairs
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
@@ -324,8 +326,8 @@ int launch_i8(mhar_ctx* c) {
   p.KS = c->KS;
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
-  p.prof = c->i8_prof;
-  if (c->i8_prof) cudaMemsetAsync(c->i8_prof, 0, 10 * sizeof(unsigned long long) * c->num_sms, c->stream);
+  p.prof = c->tc_prof;
+  if (c->tc_prof) cudaMemsetAsync(c->tc_prof, 0, kProfWords * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
@@ -668,6 +670,46 @@ int reset_streams(mhar_ctx* c) {
   return 0;
 }
 
+// MHAR_I8_PROFILE=1 debugging aid: the last tcgen05 chord launch's per-CTA
+// counters (chord_tc32.cuh / chord_i8.cuh `prof`), printed at ctx_destroy.
+// Per CTA b: [8b+0] MMA-issuer cycles, [8b+1..3] its waits on TMEM drain /
+// own slot / peer slot, [8b+4] producer waits on free slots, [8b+5..7]
+// epilogue drain / stream / idle cycles; [8N + 2b, +1] %globaltimer at entry
+// and exit (chord_tc32 only).
+void report_tc_profile(mhar_ctx* c) {
+  const int N = c->num_sms;
+  std::vector<unsigned long long> h(kProfWords * (size_t)N);
+  if (cudaMemcpy(h.data(), c->tc_prof, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  unsigned long long in_lo = ~0ull, in_hi = 0, out_lo = ~0ull, out_hi = 0;
+  for (int b = 0; b < N; ++b) {
+    const unsigned long long gi = h[8 * N + 2 * b], go = h[8 * N + 2 * b + 1];
+    if (!gi) continue;
+    in_lo = std::min(in_lo, gi);
+    in_hi = std::max(in_hi, gi);
+    out_lo = std::min(out_lo, go);
+    out_hi = std::max(out_hi, go);
+  }
+  if (out_hi)
+    std::fprintf(stderr, "[tcgen05 profile] CTA entry spread %.3f ms, exit spread %.3f ms, "
+                 "first entry -> last exit %.3f ms\n", (in_hi - in_lo) * 1e-6,
+                 (out_hi - out_lo) * 1e-6, (out_hi - in_lo) * 1e-6);
+  double w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int leaders = 0;
+  for (int b = 0; b < N; b += 2) {
+    if (!h[8 * b]) continue;
+    for (int k = 0; k < 8; ++k) w[k] += (double)h[8 * b + k];
+    ++leaders;
+  }
+  if (!leaders) return;
+  const double t = w[0];
+  std::fprintf(stderr,
+               "[tcgen05 profile] leaders %d: %.3g cycles each; MMA issuer waits: TMEM drain %.1f%%, "
+               "own slot %.1f%%, peer slot %.1f%%; producer waits for free slots %.1f%%; "
+               "epilogue: drain %.1f%%, stream %.1f%%, idle %.1f%%\n",
+               leaders, t / leaders, 100 * w[1] / t, 100 * w[2] / t, 100 * w[3] / t, 100 * w[4] / t,
+               100 * w[5] / t, 100 * w[6] / t, 100 * w[7] / t);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -834,7 +876,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TC_SMEM);
-      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->i8_prof, 10 * (size_t)c->num_sms))) {
+      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->tc_prof, kProfWords * (size_t)c->num_sms))) {
         cudaFree(tmp);
         return bail(st);
       }
@@ -859,7 +901,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)I8_SMEM);
-      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->i8_prof, 10 * (size_t)c->num_sms))) {
+      if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->tc_prof, kProfWords * (size_t)c->num_sms))) {
         cudaFree(tmp);
         return bail(st);
       }
@@ -946,60 +988,7 @@ int mhar_ctx_destroy(mhar_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  if (c->i8_prof) {  // debugging aid: cluster residency of the tcgen05 kernels
-    for (int which = 0; which < 2; ++which) {
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(148);
-      cfg.blockDim = dim3(which ? I8_THREADS : TC_THREADS);
-      cfg.dynamicSmemBytes = which ? I8_SMEM : TC_SMEM;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = 2;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      int ncl = -1;
-      cudaError_t e = which ? cudaOccupancyMaxActiveClusters(&ncl, chord_i8_kernel, &cfg)
-                            : cudaOccupancyMaxActiveClusters(&ncl, chord_tc32_kernel, &cfg);
-      std::fprintf(stderr, "[tcgen05 profile] %s: max active clusters of 2 = %d (%s)\n",
-                   which ? "chord_i8_kernel" : "chord_tc32_kernel", ncl, cudaGetErrorString(e));
-    }
-  }
-  if (c->i8_prof) {  // debugging aid: where the int8 engine's MMA issuer and producer wait
-    std::vector<unsigned long long> h(10 * (size_t)c->num_sms);
-    cudaMemcpy(h.data(), c->i8_prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    {
-      unsigned long long lo_in = ~0ull, hi_in = 0, lo_out = ~0ull, hi_out = 0;
-      for (int b = 0; b < c->num_sms; ++b) {
-        const unsigned long long gi = h[8 * c->num_sms + 2 * b], go = h[8 * c->num_sms + 2 * b + 1];
-        if (!gi) continue;
-        lo_in = std::min(lo_in, gi); hi_in = std::max(hi_in, gi);
-        lo_out = std::min(lo_out, go); hi_out = std::max(hi_out, go);
-      }
-      if (hi_out)
-        std::fprintf(stderr, "[tcgen05 profile] CTA entry spread %.3f ms, exit spread %.3f ms, "
-                     "first entry -> last exit %.3f ms\n", (hi_in - lo_in) * 1e-6,
-                     (hi_out - lo_out) * 1e-6, (hi_out - lo_in) * 1e-6);
-    }
-    double tot = 0, te = 0, tf = 0, tp = 0, emp = 0, ed = 0, es = 0, ew = 0;
-    int n = 0;
-    double atom = 0;
-    for (int b = 1; b < c->num_sms; b += 2) atom += h[8 * b + 3];
-    for (int b = 0; b < c->num_sms; b += 2) {
-      if (!h[8 * b]) continue;
-      tot += h[8 * b]; te += h[8 * b + 1]; tf += h[8 * b + 2]; tp += h[8 * b + 3];
-      emp += h[8 * b + 4];
-      ed += h[8 * b + 5]; es += h[8 * b + 6]; ew += h[8 * b + 7];
-      ++n;
-    }
-    if (n)
-      std::fprintf(stderr, "[tcgen05 profile] leaders %d: total %.3g cyc; MMA waits tempty %.1f%% full %.1f%% "
-                   "peer %.1f%%; producer waits empty %.1f%%; epilogue drains %.1f%% stream %.1f%% "
-                   "idle %.1f%%; odd-CTA stream waits for staged chunks %.1f%%\n", n, tot / n, 100 * te / tot,
-                   100 * tf / tot, 100 * tp / tot, 100 * emp / tot, 100 * ed / tot, 100 * es / tot,
-                   100 * ew / tot, 100 * atom / tot);
-  }
+  if (c->tc_prof) report_tc_profile(c);
   for (auto& ev : c->pending) {
     cudaEventDestroy(ev.first);
     cudaEventDestroy(ev.second);

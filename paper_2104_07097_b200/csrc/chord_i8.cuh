@@ -44,9 +44,6 @@
 
 namespace mhar_dev {
 
-#ifndef MHAR_I8_EXPERIMENT
-#define MHAR_I8_EXPERIMENT 0
-#endif
 #ifndef MHAR_I8_PREFETCH
 #define MHAR_I8_PREFETCH 0
 #endif
@@ -266,22 +263,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
               if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
               w_empty += clock64() - t0;
               uint8_t* st = ring + (size_t)stage * I8_SLOT;
-#if MHAR_I8_EXPERIMENT == 1  // timing experiment only: skip the D slices (wrong results)
-              mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * I8_A_PIECE));
-#elif MHAR_I8_EXPERIMENT == 2  // timing experiment only: skip the A slices (wrong results)
-              mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * I8_D_PIECE));
-#else
               mbar_arrive_expect_tx(&full[stage], (uint32_t)(ns * (I8_D_PIECE + I8_A_PIECE)));
-#endif
               const int64_t doff = (wt * p.KS + ks) * (int64_t)I8_D_STAGE + s0 * I8_D_PIECE;
               const int64_t aoff =
                   ((rt * p.KS + ks) * 2 + rank) * (int64_t)(I8_SLICES * I8_A_PIECE) + s0 * I8_A_PIECE;
-#if MHAR_I8_EXPERIMENT != 1
               bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
-#endif
-#if MHAR_I8_EXPERIMENT != 2
               bulk_g2s_hint(st + I8_SLOT_A, p.A8 + aoff, ns * I8_A_PIECE, &full[stage], apol);
-#endif
               if (++stage == I8_STAGES) {
                 stage = 0;
                 ++round;
@@ -477,18 +464,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       // slack/rate chunks, overlapping the next unit's MMAs
       double hi = keyd(hk0), lo = keyd(lk0), viol = -INFINITY;
       unsigned sd = 0u;
-      long long wsr = 0;
       const int64_t sbase = ((rt * p.walk_tiles + wt) * I8_N + rq * I8_ROWS_PER_WARP) * I8_M + wl;
       double* __restrict__ Sout = p.S + sbase;
       double* __restrict__ Rout = p.R + sbase;
 #pragma unroll
       for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j) {
         const int slot = I8_SR_PER_GROUP * rq + j % I8_SR_PER_GROUP;
-        const long long w0 = clock64();
         mbar_wait(&sr_full[slot],
                   (uint32_t)(((I8_ROWS_PER_WARP / I8_SR_ROWS / I8_SR_PER_GROUP) * ui +
                               j / I8_SR_PER_GROUP) & 1));
-        wsr += clock64() - w0;
         const double* sS = sr + (size_t)slot * 2 * (I8_SR_CHUNK / 8) + wl;
         const double* sR = sS + I8_SR_CHUNK / 8;
         double sv[I8_SR_ROWS], av[I8_SR_ROWS];
@@ -518,7 +502,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         pr[5] += (unsigned long long)((e2 - e1) + (e4 - e3));  // drains
         pr[6] += (unsigned long long)(e5 - e4);                 // stream + scan
         pr[7] += (unsigned long long)((e1 - e0) + (e3 - e2));  // waiting for the MMAs
-        pr[3] += (unsigned long long)wsr;  // (odd CTAs) waiting for staged slack/rate chunks
       }
       if (c < p.z) {
         const long long vk = dkey(viol), hk = dkey(hi), lk = dkey(lo);
