@@ -43,7 +43,13 @@ constexpr int CHORD_LAG = 2;     // refill the slot consumed two stages ago
 constexpr int STAGE_DOUBLES = A_PIECE + 2 * B_PIECE;
 constexpr size_t CHORD_SMEM = (size_t)CHORD_STAGES * STAGE_DOUBLES * sizeof(double) + 1024;
 // INCREMENTAL / CHECK kernel (2 CTAs / SM)
-constexpr int CHORD2_STAGES = 4;  // 4 x 24 KB ring per CTA
+#ifndef MHAR_CHORD2_STAGES
+#define MHAR_CHORD2_STAGES 4
+#endif
+#ifndef MHAR_CHORD2_PREFETCH
+#define MHAR_CHORD2_PREFETCH 0  // L2 bulk prefetch of the slack block: measured 2 % slower
+#endif
+constexpr int CHORD2_STAGES = MHAR_CHORD2_STAGES;  // 4 x 24 KB ring per CTA
 #ifndef MHAR_CHORD2_LAG
 #define MHAR_CHORD2_LAG 1
 #endif
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordPar
 
     for (int kt = 0; kt < KT; ++kt) {
       if (tid == 0) producer_issue();
-      if (MODE == INCREMENTAL && kt == (KT > 8 ? KT - 8 : 0) && lane == 0) {
+      if (MHAR_CHORD2_PREFETCH && MODE == INCREMENTAL && kt == (KT > 8 ? KT - 8 : 0) && lane == 0) {
         // stage this warp's slack/rate block (2 x 8 KB) into L2 ahead of the epilogue
         bulk_prefetch_l2(p.S + cache_base, S_WARP_BLOCK * 8);
         bulk_prefetch_l2(p.R + cache_base, S_WARP_BLOCK * 8);
