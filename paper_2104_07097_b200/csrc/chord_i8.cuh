@@ -363,7 +363,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       }
     } else if (warp == 2 && lane == 0) {
       // ---------------- loader: this CTA's slack/rate blocks -> smem ----------------
-      const uint64_t stream_policy = policy_evict_first();
+      const uint64_t stream_policy = MHAR_STREAM_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
       for (int ui = 0; ui < my_units; ++ui) {
         int64_t rt, wp;
         i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
@@ -388,7 +388,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
     const int q = warp & 3;
     const int rq = (warp - 4) >> 2;
     const int wl = q * 32 + lane;
-    const uint64_t stream_policy = policy_evict_first();  // the slack stream must not evict A
+    const uint64_t stream_policy = MHAR_STREAM_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();  // the slack stream must not evict A
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(rq * I8_ROWS_PER_WARP);
     double* wrsc = reinterpret_cast<double*>(smem_raw + I8_RSC_OFF) + (warp - 4) * I8_ROWS_PER_WARP;
     auto release = [&]() {

@@ -46,6 +46,12 @@ constexpr size_t CHORD_SMEM = (size_t)CHORD_STAGES * STAGE_DOUBLES * sizeof(doub
 #ifndef MHAR_CHORD2_STAGES
 #define MHAR_CHORD2_STAGES 4
 #endif
+#ifndef MHAR_CHORD2_KEEP
+#define MHAR_CHORD2_KEEP 1
+#endif
+#ifndef MHAR_CHORD2_STREAMING
+#define MHAR_CHORD2_STREAMING 1
+#endif
 #ifndef MHAR_CHORD2_PREFETCH
 #define MHAR_CHORD2_PREFETCH 0  // L2 bulk prefetch of the slack block: measured 2 % slower
 #endif
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordPar
     }
   };
   if (tid == 0) {
-    keep_policy = policy_evict_last();
+    keep_policy = MHAR_CHORD2_KEEP ? policy_evict_last() : policy_evict_normal();
     if (my_units > 0) unit_coords(blockIdx.x, p, &l_mt, &l_ct);
     for (int q = 0; q < CHORD2_STAGES - CHORD2_LAG; ++q) producer_issue();
   }
@@ -438,8 +444,13 @@ __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordPar
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int64_t base = cache_base + ((i * 4 + j) * 32 + lane) * 2;
+#if MHAR_CHORD2_STREAMING
           so[i] = __ldcs(reinterpret_cast<const double2*>(p.S + base));
           ro[i] = __ldcs(reinterpret_cast<const double2*>(p.R + base));
+#else
+          so[i] = __ldcg(reinterpret_cast<const double2*>(p.S + base));
+          ro[i] = __ldcg(reinterpret_cast<const double2*>(p.R + base));
+#endif
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {

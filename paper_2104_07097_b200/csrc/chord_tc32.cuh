@@ -365,7 +365,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int q = warp & 3;                      // TMEM lane quarter this warp may access
     const int rh = (warp - 2) / 4;               // which 128 of the unit's 256 rows
     const int wl = q * 32 + lane;                // walk within this CTA's tile
-    const uint64_t stream_policy = policy_evict_first();  // the slack stream must not evict A
+    const uint64_t stream_policy = MHAR_STREAM_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();  // the slack stream must not evict A
     const float eps = (float)p.eps_dir, mu = (float)p.margin;
     for (int ui = 0; ui < my_units; ++ui) {
       int64_t rt, wp;

@@ -23,6 +23,9 @@ namespace mhar_dev {
 // k = l%4) for the first k4 step and k+4 for the second -- the mma.m8n8k4
 // fragment maps (A: row = l>>2, k = l&3; B: k = l&3, col = l>>2).
 // ---------------------------------------------------------------------------
+#ifndef MHAR_STREAM_EVICT_FIRST
+#define MHAR_STREAM_EVICT_FIRST 1  // L2 policy of the tcgen05 kernels' slack/rate stream
+#endif
 constexpr int BM = 128;        // rows of A_I per tile
 constexpr int BK = 16;         // k per pipeline stage
 constexpr int BC = 64;         // walks per B piece
