@@ -91,6 +91,7 @@ struct mhar_ctx {
   uint64_t *col_state = nullptr, *theta_state = nullptr;
   int redraw_grid = 1;
   int group_m = 4;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
+  int walk_band = 0;  // > 0: walk-tile bands (MHAR_WALK_BAND overrides)
   // walk-resident small-body path (small_kernel.cuh); Acm != null enables it
   double* Acm = nullptr;
   // fp32 variant (chord_tc32.cuh)
@@ -221,6 +222,7 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
   p.group_m = c->group_m;
+  p.walk_band = c->walk_band;
   p.tc_walk_tiles = c->tc_walk_tiles;
   p.cache_rows = c->cache_rows;
   p.rate_f32 = c->Ahi != nullptr;
@@ -831,6 +833,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     return bail(st);
   c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
   if (const char* g = std::getenv("MHAR_GROUP_M")) c->group_m = std::max(1, std::atoi(g));
+  if (const char* g = std::getenv("MHAR_WALK_BAND")) c->walk_band = std::max(0, std::atoi(g));
   if (const char* g = std::getenv("MHAR_TC_GROUP")) c->tc_group_n = std::max(1, std::atoi(g));
   if (const char* g = std::getenv("MHAR_TC_APOL")) c->tc_a_policy = std::atoi(g) % 3;
   if ((st = dalloc(c, &c->redraw_scratch, (size_t)c->redraw_grid * 3 * c->n))) return bail(st);

@@ -82,6 +82,7 @@ struct ChordParams {
   int64_t z;          // live walks
   double eps_dir;
   int group_m;        // rasterisation band height (m tiles)
+  int walk_band;      // > 0: walk-tile bands instead (see unit_coords)
   int64_t tc_walk_tiles;  // > 0: the slack cache uses a tcgen05 tile layout (tile_cache_index)
   int64_t cache_rows;     // its row tile: 256 (fp32 variant, fp32 rates) or 64 (int8 slices)
   int rate_f32;           // 1: the rate cache holds fp32 (fp32 variant)
@@ -93,10 +94,23 @@ __device__ inline int64_t cache_index(int64_t r, int64_t c, const ChordParams& p
   return s_index(r, c, p.col_tiles);
 }
 
-// Unit u -> (row tile, walk tile): bands of group_m row tiles, walk tiles
-// inner, so the CTAs in flight share few A tiles and the walk operand stays
-// L2-resident.
+// Unit u -> (row tile, walk tile).  walk_band > 0: bands of walk_band walk
+// tiles, the row tiles inner -- the band's direction tiles stay L2-resident
+// and each A_I tile is read once per band while the units in flight share it
+// (A_I streamed col_tiles / walk_band times).  Otherwise bands of group_m row
+// tiles with the walk tiles inner (A_I read once, every direction tile
+// re-read per row band).
 __device__ inline void unit_coords(int64_t u, const ChordParams& p, int64_t* mt, int64_t* ct) {
+  if (p.walk_band > 0) {
+    const int64_t band_units = (int64_t)p.walk_band * p.m_tiles;
+    const int64_t band = u / band_units;
+    const int64_t in_band = u - band * band_units;
+    const int64_t start = band * p.walk_band;
+    const int64_t w = (p.col_tiles - start < p.walk_band) ? p.col_tiles - start : p.walk_band;
+    *ct = start + in_band % w;
+    *mt = in_band / w;
+    return;
+  }
   const int64_t band_units = (int64_t)p.group_m * p.col_tiles;
   const int64_t band = u / band_units;
   const int64_t in_band = u - band * band_units;
