@@ -146,6 +146,13 @@ int mhar_debug_last_iterate(mhar_ctx* ctx, double* d, double* lower, double* upp
 int mhar_step(mhar_ctx* ctx, int64_t iters, int64_t reproject_every);
 /* Waits for queued work and reports a pending device-side error. */
 int mhar_sync(mhar_ctx* ctx);
+/* Checkpoint / resume: with Philox directions the walk state is
+ * X (mhar_get_state) plus this iterate counter, which keys every draw of
+ * the next iterate; a fresh context given the same options, X
+ * (mhar_set_state) and the counter continues the same chain.  Reference
+ * streams carry per-walk state instead: INVALID_ARGUMENT there. */
+int mhar_get_iteration(mhar_ctx* ctx, int64_t* iteration);
+int mhar_set_iteration(mhar_ctx* ctx, int64_t iteration);
 /* mhar_step bracketed by CUDA events on the context's stream; *device_ms is
  * the device time of the `iters` iterates (synchronises). */
 int mhar_step_timed(mhar_ctx* ctx, int64_t iters, int64_t reproject_every, double* device_ms);

@@ -134,6 +134,7 @@ EXPORTED_SYMBOLS = [
     "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
     "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
     "mhar_select_points", "mhar_chebyshev_center", "mhar_debug_last_iterate",
+    "mhar_get_iteration", "mhar_set_iteration",
 ]
 
 
@@ -171,6 +172,10 @@ def lib():
     L.mhar_set_state.argtypes = [C.c_void_p, _dp]
     L.mhar_get_state.argtypes = [C.c_void_p, _dp]
     L.mhar_get_state_rows_device.argtypes = [C.c_void_p, C.c_void_p]
+    L.mhar_get_iteration.argtypes = [C.c_void_p, _i64p]
+    L.mhar_get_iteration.restype = C.c_int
+    L.mhar_set_iteration.argtypes = [C.c_void_p, C.c_int64]
+    L.mhar_set_iteration.restype = C.c_int
     L.mhar_debug_last_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
     L.mhar_debug_last_iterate.restype = C.c_int
     L.mhar_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -506,6 +511,26 @@ class Engine:
         _check(lib().mhar_lambda_intervals(self._h, _d(X), _d(D), _d(lo), _d(hi),
                                            fl.ctypes.data_as(_u8p)))
         return LambdaIntervals(lo, hi, (fl & FLAG_DEGENERATE).astype(np.uint8), fl)
+
+    @property
+    def iteration(self) -> int:
+        """Iterates executed (the Philox counter of the next iterate)."""
+        v = C.c_int64(0)
+        _check(lib().mhar_get_iteration(self._h, C.byref(v)))
+        return v.value
+
+    @iteration.setter
+    def iteration(self, value: int):
+        _check(lib().mhar_set_iteration(self._h, int(value)))
+
+    def checkpoint(self):
+        """(X, iteration): everything a Philox walk needs to resume."""
+        return self.get_state(), self.iteration
+
+    def restore(self, checkpoint):
+        X, it = checkpoint
+        self.set_state(X)
+        self.iteration = it
 
     def debug_last_iterate(self):
         """Test hook: (D n x z, lower, upper, theta) of the last iterate."""

@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/mhar_b200.h"
 #include "chord_kernel.cuh"
 #include "host_linalg.h"
@@ -61,6 +63,13 @@ const char* code_name(int st) {
   } while (0)
 
 int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+// NVTX range for the host-side phases (iterate, run window, LP, MST):
+// visible in Nsight Systems, a few ns when no tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr int kProfWords = 10;  // per-CTA profile words (MHAR_I8_PROFILE)
 
@@ -494,6 +503,7 @@ int launch_reproject(mhar_ctx* c) {
 // One iterate of every walk.  injected_h (device, packed) / injected_u
 // (device) replace the RNG for the test hook.
 int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
+  NvtxRange range(injected ? "mhar.iterate.injected" : "mhar.iterate");
   CK(cudaMemsetAsync(c->redraw_count, 0, sizeof(int), c->stream));
   if (!injected) {
     int s = launch_normals(c, c->me > 0 ? c->H : c->D);
@@ -1083,6 +1093,23 @@ int mhar_step(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   return advance(c, iters, reproject_every);
 }
 
+int mhar_get_iteration(mhar_ctx* c, int64_t* iteration) {
+  if (!c || !iteration) return fail(MHAR_ERR_INVALID_ARGUMENT, "get_iteration: null argument");
+  *iteration = c->iterations;
+  return 0;
+}
+
+int mhar_set_iteration(mhar_ctx* c, int64_t iteration) {
+  if (!c || iteration < 0) return fail(MHAR_ERR_INVALID_ARGUMENT, "set_iteration: bad argument");
+  if (c->opt.rng != MHAR_RNG_PHILOX)
+    return fail(MHAR_ERR_INVALID_ARGUMENT,
+                "set_iteration: reference streams carry per-walk state; checkpoint needs Philox");
+  CK(cudaSetDevice(c->device));
+  CK(cudaStreamSynchronize(c->stream));
+  c->iterations = iteration;
+  return 0;
+}
+
 int mhar_sync(mhar_ctx* c) {
   if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "sync: null context");
   CK(cudaSetDevice(c->device));
@@ -1281,6 +1308,7 @@ int mhar_check_state(mhar_ctx* c, double eps, int64_t* first_bad, double* max_vi
 
 int mhar_run(mhar_ctx* c, const mhar_run_config* cfg, const double* x0, double* samples,
              mhar_run_stats* stats) {
+  NvtxRange range("mhar.run");
   if (!c || !cfg || !x0) return fail(MHAR_ERR_INVALID_ARGUMENT, "run: null argument");
   if (cfg->phi < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: phi must be >= 1");
   if (cfg->windows < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "config: windows must be >= 1");
@@ -1462,6 +1490,7 @@ int mhar_minimum_spanning_tree(const double* points, int64_t N, int64_t n, int d
 
 int mhar_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t nb, int64_t n,
                          int device, mhar_fr_result* out) {
+  NvtxRange range("mhar.friedman_rafsky");
   if (!out) return fail(MHAR_ERR_INVALID_ARGUMENT, "friedman_rafsky: null result");
   if (!a || !b || na < 2 || nb < 2)
     return fail(MHAR_ERR_DEGENERATE_TEST,
@@ -1503,6 +1532,7 @@ int mhar_friedman_rafsky(const double* a, int64_t na, const double* b, int64_t n
 
 int mhar_chebyshev_center(const mhar_polytope* p, int device, double* x_out, double* radius,
                           mhar_lp_stats* stats) {
+  NvtxRange range("mhar.chebyshev_center");
   if (!p || !x_out || !radius) return fail(MHAR_ERR_INVALID_ARGUMENT, "chebyshev_center: null argument");
   if (p->n < 1) return fail(MHAR_ERR_INVALID_ARGUMENT, "chebyshev_center: dimension must be positive");
   if (p->m_in < 0 || p->m_eq < 0 || (p->m_in > 0 && (!p->a_in || !p->b_in)) ||

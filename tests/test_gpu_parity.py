@@ -365,3 +365,31 @@ def test_state_rows_to_device_and_gather_layout():
         rows = torch.empty((70, 6), dtype=torch.float64, device="cuda:0")
         eng.state_rows_to_device(rows.data_ptr())
     assert np.array_equal(rows.cpu().numpy(), X.T)
+
+
+@pytest.mark.parametrize("slack,tol", [("recompute", 0.0), ("incremental", 1e-9)])
+def test_checkpoint_resume_continues_the_chain(slack, tol):
+    # with Philox, X plus the iterate counter is the whole state;
+    # 10 iterates == 6 iterates, checkpoint, a fresh context restored, 4 more
+    # (bit-exact when the slack is recomputed; the incremental cache is
+    # refreshed on restore, so that run agrees to rounding)
+    p = workloads.random_polytope(40, 900, seed=12)
+    z = 96
+    X0 = np.zeros((40, z), order="F")
+    with mh.Engine(p, z, seed=77, slack=slack) as eng:
+        eng.set_state(X0)
+        eng.step(10)
+        ref = eng.get_state()
+        assert eng.iteration == 10
+    with mh.Engine(p, z, seed=77, slack=slack) as eng:
+        eng.set_state(X0)
+        eng.step(6)
+        ck = eng.checkpoint()
+    with mh.Engine(p, z, seed=77, slack=slack) as eng:
+        eng.restore(ck)
+        eng.step(4)
+        out = eng.get_state()
+    assert np.abs(out - ref).max() <= tol
+    with mh.Engine(p, z, seed=77, rng="reference") as eng:
+        with pytest.raises(mh.MharError):
+            eng.iteration = 3
