@@ -28,6 +28,7 @@
 #include "small_kernel.cuh"
 #include "chord_tc32.cuh"
 #include "chord_i8.cuh"
+#include "fastpath.cuh"
 #include "stats_kernels.cuh"
 
 using namespace mhar_dev;
@@ -115,6 +116,10 @@ struct mhar_ctx {
   int* rexp = nullptr;
   int64_t KS = 0, i8_row_tiles = 0;
   unsigned long long* tc_prof = nullptr;  // MHAR_I8_PROFILE: tcgen05 kernels' per-CTA counters
+  // structure-aware paths (fastpath.cuh)
+  double* diag_coef = nullptr;  // stacked diagonal blocks: per-row coefficient (m)
+  int64_t diag_blocks = 0;
+  double* proj_g = nullptr;     // factored projection: G A_E H per walk (m_E x z_pad)
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
   double* rows2 = nullptr;
   double* pinned[2] = {nullptr, nullptr};
@@ -238,7 +243,46 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   return p;
 }
 
+// compute_lambda_intervals' stacked-diagonal fast path (fastpath.cuh)
+int launch_diag(mhar_ctx* c, int mode, const double* X) {
+  DiagParams p;
+  p.coef = c->diag_coef;
+  p.b = c->b;
+  p.X = X;
+  p.D = c->D;
+  p.hi_key = c->hi_key;
+  p.lo_key = c->lo_key;
+  p.viol_key = c->viol_key;
+  p.sides = c->sides;
+  p.err = c->err;
+  p.n = c->n;
+  p.blocks = c->diag_blocks;
+  p.KT = c->KT;
+  p.z = c->z;
+  p.eps_dir = c->opt.eps_dir;
+  p.bounds = mode == CHECK ? 0 : 1;
+  const int64_t splits = std::max<int64_t>(
+      1, std::min<int64_t>(c->KT, (4 * (int64_t)c->num_sms + c->ct64 - 1) / c->ct64));
+  p.kt_per_cta = (c->KT + splits - 1) / splits;
+  const dim3 grid((unsigned)c->ct64, (unsigned)((c->KT + p.kt_per_cta - 1) / p.kt_per_cta));
+  std::pair<cudaEvent_t, cudaEvent_t> ev{};
+  if (c->timing) {
+    ev = take_events(c);
+    cudaEventRecord(ev.first, c->stream);
+  }
+  diag_chord_kernel<<<grid, kDiagThreads, 0, c->stream>>>(p);
+  LAUNCH_OK(c, "diag_chord_kernel");
+  ++c->chord_launches;
+  if (c->timing) {
+    cudaEventRecord(ev.second, c->stream);
+    c->pending.push_back(ev);
+    c->pending_flops.push_back(4.0 * (double)c->m * (double)c->z);  // slack + rate per row
+  }
+  return 0;
+}
+
 int launch_chord(mhar_ctx* c, int mode, const double* X) {
+  if (c->diag_coef) return launch_diag(c, mode, X);
   ChordParams p = chord_params(c, X);
   const bool fused = (mode == FUSED || mode == FUSED_STORE);
   const int64_t units = p.m_tiles * p.col_tiles;
@@ -407,9 +451,20 @@ int launch_normals(mhar_ctx* c, double* out) {
 
 // D = P H and collapse flags (sampler.cpp:244-250).
 int launch_projection(mhar_ctx* c) {
-  dim3 grid((unsigned)(c->p_rows_pad / BM), (unsigned)c->ct64);
-  project_kernel<<<grid, 256, 0, c->stream>>>(c->Ppk, c->H, c->D, c->n, c->KT, c->err);
-  LAUNCH_OK(c, "project_kernel");
+  if (c->proj_g) {
+    // factored: D = H - A_E' (G (A_E H)), O(m_E n z)
+    proj_factor_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
+        c->AE, c->G, c->H, c->me, c->n, c->z, c->KT, c->proj_g, c->err);
+    LAUNCH_OK(c, "proj_factor_kernel");
+    const int64_t total = c->z_pad * c->KT * BK;
+    proj_correct_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->AE, c->proj_g, c->H, c->D, c->me, c->n, c->z, total, c->KT, c->err);
+    LAUNCH_OK(c, "proj_correct_kernel");
+  } else {
+    dim3 grid((unsigned)(c->p_rows_pad / BM), (unsigned)c->ct64);
+    project_kernel<<<grid, 256, 0, c->stream>>>(c->Ppk, c->H, c->D, c->n, c->KT, c->err);
+    LAUNCH_OK(c, "project_kernel");
+  }
   collapse_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
       c->D, c->n, c->z, c->KT, c->collapsed, c->err);
   LAUNCH_OK(c, "collapse_kernel");
@@ -786,6 +841,31 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     c->opt.slack_mode = MHAR_SLACK_INCREMENTAL;
     c->opt.small_path = 0;
   }
+  // stacked diagonal blocks (sampler.cpp:47-71): every row's single nonzero at
+  // column row % n -> the elementwise chord path, no slack cache needed
+  std::vector<double> diag_coef;
+  if (!tiles && p->m_in % p->n == 0) {
+    diag_coef.resize(p->m_in);
+    bool ok = true;
+    for (int64_t col = 0; col < p->n && ok; ++col)
+      for (int64_t i = 0; i < p->m_in; ++i) {
+        const double v = p->a_in[i + col * p->m_in];
+        if (i % p->n == col) {
+          if (v == 0.0) {
+            ok = false;
+            break;
+          }
+          diag_coef[i] = v;
+        } else if (v != 0.0) {
+          ok = false;
+          break;
+        }
+      }
+    if (ok && std::getenv("MHAR_NO_FASTPATH") == nullptr)
+      c->opt.slack_mode = MHAR_SLACK_RECOMPUTE;  // one elementwise pass is cheaper than a cache
+    else
+      diag_coef.clear();
+  }
   c->device = opt->device;
   c->n = p->n;
   c->m = p->m_in;
@@ -933,7 +1013,13 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     std::vector<double> bp(c->m_pad, __builtin_huge_val());
     std::memcpy(bp.data(), p->b_in, sizeof(double) * c->m);
     cudaMemcpyAsync(c->b, bp.data(), sizeof(double) * c->m_pad, cudaMemcpyHostToDevice, c->stream);
-    cudaStreamSynchronize(c->stream);  // bp is a local
+    if (!diag_coef.empty()) {
+      if ((st = dalloc(c, &c->diag_coef, diag_coef.size()))) return bail(st);
+      c->diag_blocks = c->m / c->n;
+      cudaMemcpyAsync(c->diag_coef, diag_coef.data(), sizeof(double) * diag_coef.size(),
+                      cudaMemcpyHostToDevice, c->stream);
+    }
+    cudaStreamSynchronize(c->stream);  // bp, diag_coef are locals
   }
   if (c->me > 0) {
     std::vector<double> P((size_t)c->n * c->n), G((size_t)c->me * c->me);
@@ -950,7 +1036,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         (st = dalloc(c, &c->AE, (size_t)c->me * c->n)) || (st = dalloc(c, &c->bE, c->me)) ||
         (st = dalloc(c, &c->G, (size_t)c->me * c->me)) ||
         (st = dalloc(c, &c->eqres, (size_t)c->me * c->z)) ||
-        (st = dalloc(c, &c->eqg, (size_t)c->me * c->z)))
+        (st = dalloc(c, &c->eqg, (size_t)c->me * c->z)) ||
+        // factored projection when m_E is small against n (fastpath.cuh)
+        (c->me <= kMaxFactorEq && c->n >= 256 && std::getenv("MHAR_NO_FASTPATH") == nullptr &&
+         (st = dalloc(c, &c->proj_g, (size_t)c->me * c->z_pad))))
       return bail(st);
     cudaMemcpyAsync(c->Pcm, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->AE, p->a_eq, sizeof(double) * c->me * c->n, cudaMemcpyHostToDevice,
