@@ -672,6 +672,9 @@ int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   sp.err = c->err;
   sp.walk_err = c->walk_err;
   sp.ns = c->small_ns;
+  sp.coef = c->diag_coef;
+  sp.diag_blocks = c->diag_blocks;
+  sp.factored = c->proj_g != nullptr ? 1 : 0;
   small_kernel<<<c->small_grid, 32 * SMALL_WARPS, c->small_smem, c->stream>>>(sp);
   LAUNCH_OK(c, "small_kernel");
   small_error_kernel<<<1, 256, 0, c->stream>>>(c->walk_err, c->z, c->err);
@@ -866,6 +869,11 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     else
       diag_coef.clear();
   }
+  // factored projection H - A_E' G A_E H for few equalities (fastpath.cuh); the
+  // reference-stream mode at small n keeps the dense P H of the oracle
+  const bool factored = p->m_eq >= 1 && p->m_eq <= kMaxFactorEq &&
+                        (p->n >= 256 || opt->rng == MHAR_RNG_PHILOX) &&
+                        std::getenv("MHAR_NO_FASTPATH") == nullptr;
   c->device = opt->device;
   c->n = p->n;
   c->m = p->m_in;
@@ -1002,7 +1010,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     // small bodies: keep the column-major copy for the walk-resident kernel
     c->small_ns = (int)(c->n | 1);
     const size_t small_bytes =
-        sizeof(double) * small_smem_doubles(c->n, c->m, c->me, c->me > 0, c->small_ns);
+        sizeof(double) * small_smem_doubles(c->n, c->m, c->me, c->me > 0, c->small_ns,
+                                            !diag_coef.empty(), factored);
     if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_bytes <= 200 * 1024) {
       c->Acm = tmp;
       c->allocs.push_back(tmp);
@@ -1038,8 +1047,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         (st = dalloc(c, &c->eqres, (size_t)c->me * c->z)) ||
         (st = dalloc(c, &c->eqg, (size_t)c->me * c->z)) ||
         // factored projection when m_E is small against n (fastpath.cuh)
-        (c->me <= kMaxFactorEq && c->n >= 256 && std::getenv("MHAR_NO_FASTPATH") == nullptr &&
-         (st = dalloc(c, &c->proj_g, (size_t)c->me * c->z_pad))))
+        (factored && (st = dalloc(c, &c->proj_g, (size_t)c->me * c->z_pad))))
       return bail(st);
     cudaMemcpyAsync(c->Pcm, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->AE, p->a_eq, sizeof(double) * c->me * c->n, cudaMemcpyHostToDevice,

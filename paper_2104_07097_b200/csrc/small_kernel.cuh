@@ -38,12 +38,16 @@ struct SmallParams {
   const unsigned long long* err;
   unsigned long long* walk_err;  // per walk: (iterate << 24) | (phase << 8) | status
   int ns;                        // smem row stride (odd)
+  const double* coef;            // stacked diagonal blocks (fastpath.cuh): per-row coefficient, or null
+  int64_t diag_blocks;
+  int factored;                  // 1: D = H - A_E' G A_E H instead of P H (P not staged)
 };
 
 __host__ __device__ inline size_t small_smem_doubles(int64_t n, int64_t m, int64_t me, bool proj,
-                                                     int ns) {
-  size_t s = (size_t)m * ns + (size_t)m;           // A rows, b
-  if (proj) s += (size_t)n * ns;                   // P rows
+                                                     int ns, bool diag = false,
+                                                     bool factored = false) {
+  size_t s = diag ? 2 * (size_t)m : (size_t)m * ns + (size_t)m;  // A rows (or coefficients), b
+  if (proj && !factored) s += (size_t)n * ns;      // P rows
   s += (size_t)me * ns + (size_t)me + (size_t)me * me;  // A_E, b_E, G
   s += (size_t)SMALL_WARPS * (3 * (size_t)n + 2 * (size_t)me);  // per warp x, h, d, res, g
   return s;
@@ -100,24 +104,62 @@ __device__ inline SmallChord small_chord(const double* As, const double* bs, con
   return c;
 }
 
+// Chord of (x, d) against stacked diagonal blocks (sampler.cpp:166-172):
+// lanes own coordinates; row blk n + k has coefficient cs[blk n + k].
+__device__ inline SmallChord small_chord_diag(const double* cs, const double* bs, const double* xs,
+                                              const double* ds, int64_t n, int64_t blocks,
+                                              double eps, int lane) {
+  double hi = __longlong_as_double(0x7FF0000000000000LL);
+  double lo = -hi;
+  unsigned sd = 0;
+  for (int64_t k = lane; k < n; k += 32) {
+    const double x = xs[k], d = ds[k];
+    for (int64_t blk = 0; blk < blocks; ++blk) {
+      const int64_t r = blk * n + k;
+      const double sl = __dsub_rn(bs[r], __dmul_rn(x, cs[r]));  // one rounding each
+      const double ad = __dmul_rn(d, cs[r]);
+      if (ad > eps) {
+        sd |= 1u;
+        const double q = sl / ad;
+        hi = q < hi ? q : hi;
+      } else if (ad < -eps) {
+        sd |= 2u;
+        const double q = sl / ad;
+        lo = q > lo ? q : lo;
+      }
+    }
+  }
+  SmallChord c;
+  c.hi = warp_min(hi);
+  c.lo = warp_max(lo);
+  for (int o = 16; o > 0; o >>= 1) sd |= __shfl_xor_sync(0xFFFFFFFFu, sd, o);
+  c.sides = sd;
+  return c;
+}
+
 __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallParams p) {
   if (*p.err != kNoError) return;
   extern __shared__ __align__(16) double sm[];
   const int ns = p.ns;
   const int64_t n = p.n, m = p.m, me = p.me;
-  double* As = sm;
-  double* bs = As + m * ns;
+  const bool diag = p.coef != nullptr;
+  double* As = sm;  // A rows, or the diagonal coefficients
+  double* bs = As + (diag ? m : m * ns);
   double* Ps = bs + m;
-  double* AEs = Ps + (p.P ? n * ns : 0);
+  double* AEs = Ps + (p.P && !p.factored ? n * ns : 0);
   double* bEs = AEs + me * ns;
   double* Gs = bEs + me;
   double* wbase = Gs + me * me;
-  for (int64_t i = threadIdx.x; i < m * n; i += blockDim.x) {
-    const int64_t r = i % m, k = i / m;
-    As[r * ns + k] = p.A[i];
+  if (diag) {
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) As[i] = p.coef[i];
+  } else {
+    for (int64_t i = threadIdx.x; i < m * n; i += blockDim.x) {
+      const int64_t r = i % m, k = i / m;
+      As[r * ns + k] = p.A[i];
+    }
   }
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) bs[i] = p.b[i];
-  if (p.P)
+  if (p.P && !p.factored)
     for (int64_t i = threadIdx.x; i < n * n; i += blockDim.x) Ps[(i % n) * ns + i / n] = p.P[i];
   for (int64_t i = threadIdx.x; i < me * n; i += blockDim.x) AEs[(i % me) * ns + i / me] = p.AE[i];
   for (int64_t i = threadIdx.x; i < me; i += blockDim.x) bEs[i] = p.bE[i];
@@ -157,7 +199,35 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
         }
         __syncwarp();
         bool collapsed = false;
-        if (p.P) {
+        if (p.P && p.factored) {
+          // d = h - A_E' G (A_E h), the reduction order of proj_factor_kernel /
+          // proj_correct_kernel / collapse_kernel (fastpath.cuh)
+          for (int64_t i = 0; i < me; ++i) {
+            double r = 0.0;
+            for (int64_t k = lane; k < n; k += 32) r = fma(AEs[i * ns + k], hs[k], r);
+            r = warp_sum(r);
+            if (lane == 0) res[i] = r;
+          }
+          __syncwarp();
+          for (int64_t i = lane; i < me; i += 32) {
+            double s = 0.0;
+            for (int64_t j = 0; j < me; ++j) s = fma(Gs[i + j * me], res[j], s);
+            gv[i] = s;
+          }
+          __syncwarp();
+          double sq = 0.0;
+          for (int64_t k = lane; k < n; k += 32) {
+            double s = 0.0;
+            for (int64_t i = 0; i < me; ++i) s = fma(AEs[i * ns + k], gv[i], s);
+            const double dk = hs[k] - s;
+            dsb[k] = dk;
+            sq = fma(dk, dk, sq);
+          }
+          __syncwarp();
+          collapsed = sqrt(warp_sum(sq)) <= kNearZeroDirection;
+          d = dsb;
+          if (attempt > 0 && collapsed) continue;
+        } else if (p.P) {
           double sq = 0.0;
           for (int64_t i = lane; i < n; i += 32) {
             const double* pr = Ps + i * ns;
@@ -173,7 +243,8 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
         } else {
           d = hs;
         }
-        const SmallChord c = small_chord(As, bs, xs, d, m, n, ns, p.eps_dir, lane);
+        const SmallChord c = diag ? small_chord_diag(As, bs, xs, d, n, p.diag_blocks, p.eps_dir, lane)
+                                  : small_chord(As, bs, xs, d, m, n, ns, p.eps_dir, lane);
         if (c.sides == 0u) continue;  // no usable side: degenerate, redraw
         if (c.sides != 3u) {          // one-sided: the body is unbounded
           werr = ((unsigned long long)t << 24) |
