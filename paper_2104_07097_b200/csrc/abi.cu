@@ -127,7 +127,7 @@ struct mhar_ctx {
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   unsigned long long* walk_err = nullptr;
   size_t small_smem = 0;
-  int small_ns = 1, small_grid = 0;
+  int small_ns = 1, small_grid = 0, small_warps = SMALL_WARPS;
 
   // host bookkeeping
   int64_t iterations = 0;
@@ -675,7 +675,7 @@ int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   sp.coef = c->diag_coef;
   sp.diag_blocks = c->diag_blocks;
   sp.factored = c->proj_g != nullptr ? 1 : 0;
-  small_kernel<<<c->small_grid, 32 * SMALL_WARPS, c->small_smem, c->stream>>>(sp);
+  small_kernel<<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp);
   LAUNCH_OK(c, "small_kernel");
   small_error_kernel<<<1, 256, 0, c->stream>>>(c->walk_err, c->z, c->err);
   LAUNCH_OK(c, "small_error_kernel");
@@ -1008,14 +1008,26 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       }
     }
     // small bodies: keep the column-major copy for the walk-resident kernel
+    // (warps per CTA: the most that fit next to the body; the path is taken
+    // when at least 4 walks per SM are resident)
     c->small_ns = (int)(c->n | 1);
-    const size_t small_bytes =
-        sizeof(double) * small_smem_doubles(c->n, c->m, c->me, c->me > 0, c->small_ns,
-                                            !diag_coef.empty(), factored);
-    if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_bytes <= 200 * 1024) {
+    size_t small_bytes = 0;
+    int small_warps = 0;
+    for (int w = SMALL_WARPS; w >= 1 && !small_warps; --w) {
+      const size_t bytes = sizeof(double) * small_smem_doubles(c->n, c->m, c->me, c->me > 0,
+                                                               c->small_ns, !diag_coef.empty(),
+                                                               factored, w);
+      const size_t per_sm = (227 * 1024) / (bytes + 1024);
+      if (bytes <= 220 * 1024 && (size_t)w * per_sm >= 4) {
+        small_warps = w;
+        small_bytes = bytes;
+      }
+    }
+    if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_warps > 0) {
       c->Acm = tmp;
       c->allocs.push_back(tmp);
       c->small_smem = small_bytes;
+      c->small_warps = small_warps;
     } else {
       cudaFree(tmp);
     }
@@ -1080,10 +1092,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)c->small_smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_kernel, 32 * SMALL_WARPS,
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_kernel, 32 * c->small_warps,
                                                   c->small_smem);
     if (per_sm < 1) per_sm = 1;
-    const int64_t need = (c->z + SMALL_WARPS - 1) / SMALL_WARPS;
+    const int64_t need = (c->z + c->small_warps - 1) / c->small_warps;
     c->small_grid = (int)std::min<int64_t>(need, (int64_t)per_sm * c->num_sms);
   }
   if ((st = reset_streams(c))) return bail(st);

@@ -43,13 +43,19 @@ struct SmallParams {
   int factored;                  // 1: D = H - A_E' G A_E H instead of P H (P not staged)
 };
 
+// Per-warp scratch: x, h (and d when a dense P is applied; otherwise d is
+// formed in place of h), res, g.
+__host__ __device__ inline size_t small_warp_doubles(int64_t n, int64_t me, bool dense_proj) {
+  return (dense_proj ? 3 : 2) * (size_t)n + 2 * (size_t)me;
+}
 __host__ __device__ inline size_t small_smem_doubles(int64_t n, int64_t m, int64_t me, bool proj,
                                                      int ns, bool diag = false,
-                                                     bool factored = false) {
+                                                     bool factored = false,
+                                                     int warps = SMALL_WARPS) {
   size_t s = diag ? 2 * (size_t)m : (size_t)m * ns + (size_t)m;  // A rows (or coefficients), b
   if (proj && !factored) s += (size_t)n * ns;      // P rows
   s += (size_t)me * ns + (size_t)me + (size_t)me * me;  // A_E, b_E, G
-  s += (size_t)SMALL_WARPS * (3 * (size_t)n + 2 * (size_t)me);  // per warp x, h, d, res, g
+  s += (size_t)warps * small_warp_doubles(n, me, proj && !factored);
   return s;
 }
 
@@ -167,16 +173,18 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
   __syncthreads();
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* xs = wbase + (size_t)warp * (3 * n + 2 * me);
+  const int nwarps = blockDim.x >> 5;
+  const bool dense_proj = p.P && !p.factored;
+  double* xs = wbase + (size_t)warp * small_warp_doubles(n, me, dense_proj);
   double* hs = xs + n;
-  double* dsb = hs + n;
-  double* res = dsb + n;
+  double* dsb = dense_proj ? hs + n : hs;  // factored / no projection: d replaces h
+  double* res = hs + (dense_proj ? 2 * n : n);
   double* gv = res + me;
   const int64_t ppc = (n + 1) / 2;
   unsigned long long redraws = 0;
 
-  for (int64_t w = (int64_t)blockIdx.x * SMALL_WARPS + warp; w < p.z;
-       w += (int64_t)gridDim.x * SMALL_WARPS) {
+  for (int64_t w = (int64_t)blockIdx.x * nwarps + warp; w < p.z;
+       w += (int64_t)gridDim.x * nwarps) {
     const uint64_t gw = (uint64_t)(p.chain_offset + w);
     for (int64_t k = lane; k < n; k += 32) xs[k] = p.X[b_index(w, k, p.KT)];
     __syncwarp();
@@ -220,7 +228,7 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
             double s = 0.0;
             for (int64_t i = 0; i < me; ++i) s = fma(AEs[i * ns + k], gv[i], s);
             const double dk = hs[k] - s;
-            dsb[k] = dk;
+            dsb[k] = dk;  // dsb == hs: each lane rewrites only its own coordinates
             sq = fma(dk, dk, sq);
           }
           __syncwarp();
