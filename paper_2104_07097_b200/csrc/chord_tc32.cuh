@@ -46,13 +46,13 @@ constexpr int TC_A_PIECE = TC_NH * TC_BK;  // floats per A_hi (or A_lo) half pie
 constexpr int TC_STAGE_FLOATS = TC_D_PIECE + 2 * TC_A_PIECE;  // 24 KB
 constexpr int TC_EPI_WARPS = 8;       // two per TMEM lane quarter, each owns half the rows
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
-#ifndef MHAR_TC_GROUP
-#define MHAR_TC_GROUP 16
+#ifndef MHAR_TC_EPI_ROWS
+#define MHAR_TC_EPI_ROWS 16
 #endif
 #ifndef MHAR_TC_PREFETCH
 #define MHAR_TC_PREFETCH 0
 #endif
-constexpr int TC_GROUP = MHAR_TC_GROUP;  // epilogue rows per load group
+constexpr int TC_GROUP = MHAR_TC_EPI_ROWS;  // epilogue rows per load group
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 512;
 
 // Interleaved K-major ("no swizzle") core-matrix layout of one (tile, k_tile)
