@@ -46,6 +46,9 @@ constexpr size_t CHORD_SMEM = (size_t)CHORD_STAGES * STAGE_DOUBLES * sizeof(doub
 #ifndef MHAR_CHORD2_STAGES
 #define MHAR_CHORD2_STAGES 4
 #endif
+#ifndef MHAR_CHORD_RED
+#define MHAR_CHORD_RED 1  // RED reductions; the volatile pre-check loads were measured 1-3 % slower
+#endif
 #ifndef MHAR_CHORD2_KEEP
 #define MHAR_CHORD2_KEEP 1
 #endif
@@ -171,6 +174,15 @@ __device__ __forceinline__ void reduce_and_publish(double (&hi)[NCH][2], double 
         const int64_t c = c0[j] + 2 * lane + e;
         if (c >= p.z) continue;
         const long long vk = dkey(viol[j][e]);
+#if MHAR_CHORD_RED
+        // fire-and-forget reductions (RED): no round trip in the epilogue
+        atomicMax(p.viol_key + c, vk);
+        if (BOUNDS) {
+          atomicMin(p.hi_key + c, dkey(hi[j][e]));
+          atomicMax(p.lo_key + c, dkey(lo[j][e]));
+          if (sd[j][e]) atomicOr(p.sides + c, sd[j][e]);
+        }
+#else
         if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
         if (BOUNDS) {
           const long long hk = dkey(hi[j][e]), lk = dkey(lo[j][e]);
@@ -178,6 +190,7 @@ __device__ __forceinline__ void reduce_and_publish(double (&hi)[NCH][2], double 
           if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
           if (sd[j][e] & ~*(volatile unsigned*)(p.sides + c)) atomicOr(p.sides + c, sd[j][e]);
         }
+#endif
       }
   }
 }
