@@ -448,10 +448,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       }
       if (c < p.z) {
         const long long vk = dkey((double)viol), hk = dkey((double)hi), lk = dkey((double)lo);
+#if MHAR_CHORD_RED
+        // fire-and-forget reductions (RED): no round trip in the epilogue
+        atomicMax(p.viol_key + c, vk);
+        atomicMin(p.hi_key + c, hk);
+        atomicMax(p.lo_key + c, lk);
+        if (sd) atomicOr(p.sides + c, sd);
+#else
         if (vk > *(volatile long long*)(p.viol_key + c)) atomicMax(p.viol_key + c, vk);
         if (hk < *(volatile long long*)(p.hi_key + c)) atomicMin(p.hi_key + c, hk);
         if (lk > *(volatile long long*)(p.lo_key + c)) atomicMax(p.lo_key + c, lk);
         if (sd & ~*(volatile unsigned*)(p.sides + c)) atomicOr(p.sides + c, sd);
+#endif
       }
     }
   }
