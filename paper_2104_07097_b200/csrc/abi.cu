@@ -831,9 +831,15 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
 
   if (opt->f64_engine != MHAR_F64_DMMA && opt->f64_engine != MHAR_F64_INT8)
     return fail(MHAR_ERR_INVALID_ARGUMENT, "options: unknown f64_engine");
-  const bool i8 = opt->f64_engine == MHAR_F64_INT8 && opt->precision != 32;
-  if (i8 && round_up(p->n, I8_BK) > I8_MAX_K)
+  if (opt->f64_engine == MHAR_F64_INT8 && opt->precision != 32 && round_up(p->n, I8_BK) > I8_MAX_K)
     return fail(MHAR_ERR_INVALID_ARGUMENT, "options: the int8-slice engine needs n <= 4608");
+  // MHAR_F64_ENGINE=int8 selects the int8-slice engine for every eligible
+  // context (n <= 4608, fp64) without code changes -- e.g. for the C++ drop-in
+  const char* env_engine = std::getenv("MHAR_F64_ENGINE");
+  const bool i8 = opt->precision != 32 &&
+                  (opt->f64_engine == MHAR_F64_INT8 ||
+                   (env_engine && std::strcmp(env_engine, "int8") == 0 &&
+                    round_up(p->n, I8_BK) <= I8_MAX_K));
 
   mhar_ctx* c = new mhar_ctx();
   c->opt = *opt;

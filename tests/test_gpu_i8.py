@@ -238,3 +238,21 @@ def test_i8_uniformity_screening_against_direct_draws():
         if stats.friedman_rafsky(S, ref).z_value >= stats.kUniformityZThreshold:
             ok += 1
     assert ok >= 9, f"{ok}/10"
+
+
+def test_env_switch_selects_the_int8_engine(monkeypatch):
+    # MHAR_F64_ENGINE=int8: every eligible fp64 context uses the int8 engine
+    # (the C++ drop-in needs no code change); walk tiles of the tcgen05 pair
+    # pad z to 256 instead of 64
+    p = workloads.random_polytope(50, 600, seed=2)
+    with mh.Engine(p, 100) as eng:
+        assert eng.stats()["z_padded"] == 128
+    monkeypatch.setenv("MHAR_F64_ENGINE", "int8")
+    with mh.Engine(p, 100) as eng:
+        assert eng.stats()["z_padded"] == 256
+        eng.set_state(np.zeros((50, 100)))
+        eng.step(5)
+        assert eng.check_state(1e-9)[0] == -1
+    big = workloads.random_polytope(4700, 4, seed=1)  # beyond n <= 4608: stays on DMMA
+    with mh.Engine(big, 8) as eng:
+        assert eng.stats()["z_padded"] == 64
