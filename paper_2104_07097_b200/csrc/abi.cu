@@ -105,7 +105,7 @@ struct mhar_ctx {
   // walk-resident small-body path (small_kernel.cuh); Acm != null enables it
   double* Acm = nullptr;
   // fp32 variant (chord_tc32.cuh)
-  float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr;
+  float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr, *Dlo = nullptr;
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
   int tc_group_n = 1;   // tc32 rasterisation band (row tiles); MHAR_TC_GROUP overrides
   int tc_a_policy = 0;  // L2 policy of the tc32 A stream (evict_normal); MHAR_TC_APOL overrides
@@ -324,6 +324,7 @@ int launch_tc32(mhar_ctx* c) {
   p.Ahi = c->Ahi;
   p.Alo = c->Alo;
   p.Dhi = c->Dhi;
+  p.Dlo = c->Dlo;
   p.S = c->S;
   p.R = reinterpret_cast<float*>(c->R);
   p.theta_prev = c->theta;
@@ -350,7 +351,10 @@ int launch_tc32(mhar_ctx* c) {
     ev = take_events(c);
     cudaEventRecord(ev.first, c->stream);
   }
-  chord_tc32_kernel<<<grid, TC_THREADS, TC_SMEM, c->stream>>>(p);
+  if (c->Dlo)
+    chord_tc32_kernel<true><<<grid, TC_THREADS, TcCfg<true>::smem, c->stream>>>(p);
+  else
+    chord_tc32_kernel<false><<<grid, TC_THREADS, TcCfg<false>::smem, c->stream>>>(p);
   LAUNCH_OK(c, "chord_tc32_kernel");
   ++c->chord_launches;
   if (c->timing) {
@@ -588,7 +592,7 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
     // fp32 variant: the tensor cores see D_hi + D_lo; D becomes that direction
     const int64_t total = c->z_pad * c->KT * BK;
     tc_split_d_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        c->D, c->n, c->z_pad, c->KT, c->Dhi, c->err);
+        c->D, c->n, c->z_pad, c->KT, c->Dhi, c->Dlo, c->err);
     LAUNCH_OK(c, "tc_split_d_kernel");
   }
   if (c->A8) {
@@ -972,7 +976,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       // A_I rounded to fp32 and split for 3xTF32; the fp64 copy becomes A_hi + A_lo
       const size_t an = (size_t)c->m_pad * c->n_pad, dn = (size_t)c->z_pad * c->n_pad;
       if ((st = dalloc(c, &c->Ahi, an)) || (st = dalloc(c, &c->Alo, an)) ||
-          (st = dalloc(c, &c->Dhi, dn))) {
+          (st = dalloc(c, &c->Dhi, dn)) || (p->m_eq > 0 && (st = dalloc(c, &c->Dlo, dn)))) {
         cudaFree(tmp);
         return bail(st);
       }
@@ -981,8 +985,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       ++c->launches;
       cudaMemsetAsync(c->Dhi, 0, dn * sizeof(float), c->stream);
       cudaStreamSynchronize(c->stream);
-      cudaFuncSetAttribute(chord_tc32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TC_SMEM);
+      cudaFuncSetAttribute(chord_tc32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcCfg<false>::smem);
+      cudaFuncSetAttribute(chord_tc32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcCfg<true>::smem);
       if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->tc_prof, kProfWords * (size_t)c->num_sms))) {
         cudaFree(tmp);
         return bail(st);

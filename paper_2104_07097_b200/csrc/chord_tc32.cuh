@@ -54,6 +54,15 @@ constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 #endif
 constexpr int TC_GROUP = MHAR_TC_EPI_ROWS;  // epilogue rows per load group
 constexpr size_t TC_SMEM = (size_t)TC_STAGES * TC_STAGE_FLOATS * 4 + 512;
+// Bodies with equalities: the direction P h must stay in the null space of
+// A_E, so it is not rounded to TF32; it is split d = d_hi + d_lo instead and
+// the rates take three MMAs (A_hi d_hi + A_lo d_hi + A_hi d_lo).  A stage then
+// also carries d_lo (32 KB), six stages.
+template <bool SPLIT_D> struct TcCfg {
+  static constexpr int stages = SPLIT_D ? 6 : TC_STAGES;
+  static constexpr int stage_floats = TC_STAGE_FLOATS + (SPLIT_D ? TC_D_PIECE : 0);
+  static constexpr size_t smem = (size_t)stages * stage_floats * 4 + 512;
+};
 
 // Interleaved K-major ("no swizzle") core-matrix layout of one (tile, k_tile)
 // piece of R rows: [k_chunk(4 floats)][row_group(8 rows)][row(8)][4].
@@ -179,7 +188,8 @@ __host__ __device__ inline float2 df_unpack(double d) { return *reinterpret_cast
 struct TcParams {
   const float* Ahi;  // tc_a_index layout
   const float* Alo;
-  const float* Dhi;  // tc_d_index layout, TF32-exact directions
+  const float* Dhi;  // tc_d_index layout, TF32-exact directions (or their TF32 high part)
+  const float* Dlo;  // split directions (bodies with equalities): d - d_hi in TF32, else null
   double* S;         // tc_s_index layout, fp64 slack
   float* R;          // rates of the previous iterate (fp32: what the MMA produced)
   const double* theta_prev;
@@ -212,17 +222,20 @@ __device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_
   *wp = in_band / h;
 }
 
+template <bool SPLIT_D>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     chord_tc32_kernel(const TcParams p) {
+  constexpr int kStages = TcCfg<SPLIT_D>::stages;
+  constexpr int kStageFloats = TcCfg<SPLIT_D>::stage_floats;
   unsigned long long g_entry = 0;
   if (p.prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
   if (*p.err != kNoError) return;  // read identically by both CTAs of the pair
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   float* ring = reinterpret_cast<float*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)TC_STAGES * TC_STAGE_FLOATS * 4);
-  uint64_t* empty = full + TC_STAGES;
-  uint64_t* peer_full = empty + TC_STAGES;  // leader: the odd CTA's stage landed
-  uint64_t* tfull = peer_full + TC_STAGES;  // [2] accumulator ready (both CTAs)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)kStages * kStageFloats * 4);
+  uint64_t* empty = full + kStages;
+  uint64_t* peer_full = empty + kStages;  // leader: the odd CTA's stage landed
+  uint64_t* tfull = peer_full + kStages;  // [2] accumulator ready (both CTAs)
   uint64_t* tempty = tfull + 2;             // [2] accumulator drained (leader, 8 warps)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -234,7 +247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   const int KT = (int)p.KT;
 
   if (tid == 0) {
-    for (int s = 0; s < TC_STAGES; ++s) {
+    for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
       mbar_init(&peer_full[s], 1);
@@ -282,15 +295,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const long long t0 = clock64();
           if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
           w_empty += clock64() - t0;
-          float* st = ring + (size_t)stage * TC_STAGE_FLOATS;
-          mbar_arrive_expect_tx(&full[stage], TC_STAGE_FLOATS * 4);
+          float* st = ring + (size_t)stage * kStageFloats;
+          mbar_arrive_expect_tx(&full[stage], kStageFloats * 4);
           const int64_t doff = (wt * p.KT + kt) * TC_D_PIECE;
           const int64_t aoff = ((rt * p.KT + kt) * 2 + rank) * TC_A_PIECE;
           bulk_g2s_hint(st, p.Dhi + doff, TC_D_PIECE * 4, &full[stage], keep);
           bulk_g2s_hint(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage], apol);
           bulk_g2s_hint(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage],
                         apol);
-          if (++stage == TC_STAGES) {
+          if (SPLIT_D)
+            bulk_g2s_hint(st + TC_D_PIECE + 2 * TC_A_PIECE, p.Dlo + doff, TC_D_PIECE * 4,
+                          &full[stage], keep);
+          if (++stage == kStages) {
             stage = 0;
             ++round;
           }
@@ -319,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           w_full += t2 - t1;
           w_peer += clock64() - t2;
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const float* sd = ring + (size_t)stage * TC_STAGE_FLOATS;
+          const float* sd = ring + (size_t)stage * kStageFloats;
           const float* sa_hi = sd + TC_D_PIECE;
           const float* sa_lo = sa_hi + TC_A_PIECE;
 #pragma unroll
@@ -331,9 +347,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             const uint64_t al = umma_desc(sa_lo + aofs, TC_NH * 16, 128);
             tc_mma2(acc, dd, ah, (kt | k) ? 1u : 0u);
             tc_mma2(acc, dd, al, 1u);
+            if (SPLIT_D) {
+              const uint64_t dl = umma_desc(sa_lo + TC_A_PIECE + dofs, TC_M * 16, 128);
+              tc_mma2(acc, dl, ah, 1u);
+            }
           }
           tc_commit2(&empty[stage]);  // frees the slot in both CTAs when these MMAs finish
-          if (++stage == TC_STAGES) {
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -354,7 +374,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], (uint32_t)phase);
           mbar_arrive_remote(&peer_full[stage], 0);
-          if (++stage == TC_STAGES) {
+          if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
@@ -497,17 +517,24 @@ __global__ void tc_split_a_kernel(const double* __restrict__ Acm, int64_t m, int
 
 // fp64 directions (packed b_index) -> TF32-exact directions; D is replaced
 // by them so the walk moves along exactly the direction the tensor cores see.
+// Split mode (bodies with equalities): D keeps the fp64 direction (it stays in
+// the null space of A_E) and d = d_hi + d_lo is handed to the tensor cores.
 __global__ void tc_split_d_kernel(double* __restrict__ D, int64_t n, int64_t z_pad, int64_t KT,
-                                  float* __restrict__ Dhi, const unsigned long long* err) {
+                                  float* __restrict__ Dhi, float* __restrict__ Dlo,
+                                  const unsigned long long* err) {
   if (*err != kNoError) return;
   const int64_t total = z_pad * KT * BK;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c, k;
     b_coords(i, KT, &c, &k);
-    const float h = tf32_trunc((float)D[i]);
+    const double d = D[i];
+    const float h = tf32_trunc((float)d);
     Dhi[tc_d_index(c, k, KT)] = h;
-    D[i] = (double)h;
+    if (Dlo)
+      Dlo[tc_d_index(c, k, KT)] = tf32_trunc((float)(d - (double)h));
+    else
+      D[i] = (double)h;
   }
 }
 

@@ -101,3 +101,24 @@ def test_fp32_config5_full_width_feasible():
         eng.step(10)
         bad, viol, _ = eng.check_state(1e-9)
     assert bad == -1 and viol.max() <= 0.0
+
+
+def test_fp32_with_equalities_stays_on_the_slice_and_inside():
+    # bodies with equalities: the projected direction is split (d_hi + d_lo)
+    # rather than rounded to TF32, so it stays in the null space of A_E and
+    # the reprojection cadence only removes rounding drift
+    n, me = 120, 6
+    rng = np.random.default_rng(12)
+    a_eq = rng.standard_normal((me, n))
+    base = workloads.random_polytope(n, 3000, seed=13)
+    p = mh.Polytope(base.a_in, base.b_in, a_eq, np.zeros(me))
+    op = mh.compute_projection(p.a_eq)
+    with mh.Engine(p, 256, seed=4, projector=op, precision=32, refresh_every=64) as eng:
+        eng.set_state(np.zeros((n, 256)))
+        for _ in range(4):
+            eng.step(75, 25)
+            bad, viol, eqv = eng.check_state(1e-9)
+            assert bad == -1 and viol.max() <= 0.0 and eqv.max() <= 1e-9
+        X = eng.get_state()
+    assert np.abs(a_eq @ X).max() <= 1e-9
+    assert np.abs(X).max() > 0.05
