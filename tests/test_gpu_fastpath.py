@@ -99,3 +99,20 @@ def test_factored_projection_run_stays_on_the_slice():
     assert np.abs(S.sum(1) - 1.0).max() <= 1e-9
     assert (S @ p.a_in.T - p.b_in).max() <= 1e-9
     assert abs(S.mean() - 1.0 / n) <= 0.1 / n
+
+
+def test_multi_kernel_structured_run_large_simplex():
+    # n = 3000 does not fit the walk-resident kernel: the multi-kernel path
+    # with the diagonal chord and the factored projection, run() with
+    # reprojection; against the general path (dense P H, DMMA chord)
+    n = 3000
+    p = mh.make_simplex(n)
+    op = mh.compute_projection(p.a_eq)
+    out = {}
+    for fast in (True, False):
+        with _engine(p, 256, seed=9, projector=op, fastpath=fast, slack="recompute") as eng:
+            S, _ = eng.run(np.full(n, 1.0 / n), phi=10, windows=2, burn_in=10, reproject_every=10)
+        assert np.abs(S.sum(1) - 1.0).max() <= 1e-9
+        assert (S @ p.a_in.T - p.b_in).max() <= 1e-9
+        out[fast] = S
+    assert np.abs(out[True] - out[False]).max() <= 1e-9
