@@ -562,13 +562,17 @@ def main():
                     help="run the paper's hypercube/simplex table (PAPER.md:845-887) instead")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.impl == "reference" and not (args.paper or args.sweep_z):
+        # CPU-only arm: rank 0 times the reference restatement, the other
+        # ranks exit 0 without work; no process group, no device touched
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")),
+                      int(os.environ.get("RANK", "0")))
+        return
     world, rank, local = dist_setup(args)
     if args.paper:
         run_paper(args)
     elif args.sweep_z:
         run_sweep(args)
-    elif args.impl == "reference":
-        run_reference(args, world, rank)
     else:
         run_engine(args, world, rank, local)
     if world > 1:

@@ -36,3 +36,19 @@ def test_roofline_peaks_and_traffic_are_committed():
     for cap in ("chord2_full", "tc32_full", "i8_full"):
         t = bench.ncu_traffic(cap)
         assert t is not None and t > 1.0
+
+
+def test_reference_arm_under_torchrun_two_ranks():
+    # the driver launches the reference arm like the engine arm: rank 0
+    # prints the one line, rank 1 exits 0 without work or a device
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"),
+         "--impl", "reference", "--gpus", "2", "--config", "3", "--steps", "1", "--warmup", "3",
+         "--cpu-walks", "8"],
+        cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
