@@ -334,15 +334,27 @@ def run_engine(args, world, rank, local):
     import paper_2104_07097_b200 as mh
     from paper_2104_07097_b200 import workloads
 
-    w = workloads.config(args.config, z=args.z)
+    offset = None
+    if args.strong:
+        # strong scaling: a fixed job of --strong walks split
+        # into contiguous per-rank ranges keyed on the global chain id
+        base, extra = divmod(args.strong, world)
+        z_local = base + (1 if rank < extra else 0)
+        offset = rank * base + min(rank, extra)
+        w = workloads.config(args.config, z=z_local)
+    else:
+        w = workloads.config(args.config, z=args.z)
     p = w.polytope
     z = w.z
+    total_walks = args.strong if args.strong else z * world
+    if offset is None:
+        offset = rank * z
     # the committed ncu captures (profiles/ncu_full_r01.json) are of this workload
     captured = args.config == 5 and z == 4096
     projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
     reproject = args.reproject if p.num_equalities() else 0
     eng = mh.Engine(p, z, seed=args.seed, projector=projector, slack=args.slack,
-                    refresh_every=args.refresh, device=local, chain_offset=rank * z,
+                    refresh_every=args.refresh, device=local, chain_offset=offset,
                     precision=args.precision, f64_engine=args.f64_engine)
     X0 = np.zeros((p.dim(), z), order="F")
     X0[:] = w.x0[:, None]
@@ -362,7 +374,7 @@ def run_engine(args, world, rank, local):
     eng.set_timing(False)
     st = eng.stats()
     ms = max_over_ranks(ms, world)
-    value = z * world * args.steps / (ms * 1e-3)
+    value = total_walks * args.steps / (ms * 1e-3)
 
     # e2e: the reference-facing call with HOST buffers every step, as the
     # reference's own loop `step(p, op, cfg, rng, state)` does: the walk state
@@ -380,7 +392,7 @@ def run_engine(args, world, rank, local):
         eng.get_state(out=Xh)
         t_e2e.append(time.perf_counter() - t0)
     e2e_s = max_over_ranks(sum(t_e2e), world)
-    e2e_value = z * world * args.e2e_steps / e2e_s
+    e2e_value = total_walks * args.e2e_steps / e2e_s
     bytes_state = p.dim() * z * 8
 
     # one collection window (outside the timed region): containment of every
@@ -420,7 +432,7 @@ def run_engine(args, world, rank, local):
         alg8 = s8["chord_flops"] / max(s8["chord_ms"] * 1e-3, 1e-30) / 1e12
         ops8 = I8_MMAS_PER_KSTEP * alg8  # int8 tensor ops executed (34 slice-pair products)
         i8_peak = int8_dense_peak()
-        i8 = {"value": z * world * args.steps / (ms8 * 1e-3), "unit": "chain-steps/s",
+        i8 = {"value": total_walks * args.steps / (ms8 * 1e-3), "unit": "chain-steps/s",
               "ms_per_step": ms8 / args.steps,
               "dtype": "f64 results: A_I and d as 53-bit fixed point in 7 int8 slices, exact "
                        "int32 slice products (levels 0..7), fp64 combine; slack and walks f64",
@@ -449,7 +461,7 @@ def run_engine(args, world, rank, local):
         e32.close()
         tf32_exec = 2.0 * s32["chord_flops"] / max(s32["chord_ms"] * 1e-3, 1e-30) / 1e12
         tf32_peak = tf32_dense_peak()
-        fp32 = {"value": z * world * args.steps / (ms32 * 1e-3), "unit": "chain-steps/s",
+        fp32 = {"value": total_walks * args.steps / (ms32 * 1e-3), "unit": "chain-steps/s",
                 "ms_per_step": ms32 / args.steps,
                 "dtype": "A_I rounded to f32; rates f32-accurate on tcgen05 (TF32 hi/lo split); "
                          "slack and walks f64",
@@ -482,10 +494,11 @@ def run_engine(args, world, rank, local):
     line = {
         "metric": METRIC, "value": value, "unit": "chain-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded unit-norm Gaussian rows, BASELINE config %d)" % args.config,
         "config": {"workload": w.name, "n": p.dim(), "m_I": p.num_inequalities(),
-                   "m_E": p.num_equalities(), "walks_per_gpu": z, "walks_total": z * world,
+                   "m_E": p.num_equalities(), "walks_per_gpu": z, "walks_total": total_walks,
                    "slack_mode": args.slack, "refresh_every": args.refresh, "rng": "philox",
                    "parallelism": f"walk-sharded x{world}",
                    "l2": "inputs larger than L2 (A_I is %.1f GB)" % (p.a_in.nbytes / 1e9)},
@@ -501,7 +514,7 @@ def run_engine(args, world, rank, local):
                      "peak_source": "fp64 DMMA microbench, profiles/fp64_peaks_r01.json"},
         "reference_equivalent_tflops": value * fpi / z / 1e12 / world,
         "refresh": {"every": args.refresh, "ms": ms_refresh,
-                    "amortized_value": z * world * args.refresh /
+                    "amortized_value": total_walks * args.refresh /
                     ((ms / args.steps * (args.refresh - 1) + ms_refresh) * 1e-3),
                     "note": "value is the steady incremental iterate; amortized_value adds one "
                             "fused refresh pass per `every` iterates"},
@@ -540,6 +553,8 @@ def main():
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--z", type=int, default=None)
+    ap.add_argument("--strong", type=int, default=0,
+                    help="strong scaling: a fixed total of this many walks split over the ranks")
     ap.add_argument("--seed", type=int, default=2021)
     ap.add_argument("--slack", default="incremental", choices=["incremental", "recompute"])
     ap.add_argument("--refresh", type=int, default=128)

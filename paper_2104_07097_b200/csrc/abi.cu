@@ -1596,16 +1596,53 @@ int mhar_minimum_spanning_tree(const double* points, int64_t N, int64_t n, int d
     return fail(MHAR_ERR_CUDA, "minimum_spanning_tree: cudaMalloc failed");
   }
   cudaMemcpyAsync(dP, pt.data(), sizeof(double) * pt.size(), cudaMemcpyHostToDevice, s);
-  prim_kernel<<<1, PRIM_THREADS, 0, s>>>(dP, N, n, dbest, dpar, dint, dea, deb, dew);
-  cudaError_t e = cudaGetLastError();
+  // pools past a few thousand points spread over every SM (cooperative grid,
+  // one barrier per added vertex); MHAR_PRIM=cta|grid forces one form
+  const char* prim_env = std::getenv("MHAR_PRIM");
+  bool grid_form = N > 2048;
+  if (prim_env && !std::strcmp(prim_env, "cta")) grid_form = false;
+  if (prim_env && !std::strncmp(prim_env, "grid", 4)) grid_form = true;  // grid | grid_l2
+  cudaError_t e = cudaSuccess;
+  PrimCand* dcand = nullptr;
+  if (grid_form) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    int64_t G = (N + PRIM_GRID_THREADS - 1) / PRIM_GRID_THREADS;
+    if (G > sms) G = sms;
+    if (G < 1) G = 1;
+    int64_t chunk = (N + G - 1) / G;
+    G = (N + chunk - 1) / chunk;
+    // the CTA's own points go to shared memory too when they fit (L2
+    // latency otherwise bounds the sequential distance sums)
+    const int64_t nst = std::min<int64_t>(n, PRIM_GRID_SMEM_COORDS);
+    int stage_own = n <= PRIM_GRID_SMEM_COORDS && sizeof(double) * (nst + chunk * n) <= 200 * 1024;
+    if (prim_env && !std::strcmp(prim_env, "grid_l2")) stage_own = 0;
+    const size_t smem = sizeof(double) * (size_t)(nst + (stage_own ? chunk * n : 0));
+    e = cudaMalloc(&dcand, sizeof(PrimCand) * 2 * G);
+    if (e == cudaSuccess && smem > 48 * 1024)
+      e = cudaFuncSetAttribute(prim_grid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem);
+    if (e == cudaSuccess) {
+      void* args[] = {&dP, (void*)&N, (void*)&n, &chunk, &dbest, &dpar, &dint,
+                      &dcand, &dea, &deb, &dew, &stage_own};
+      e = cudaLaunchCooperativeKernel((const void*)prim_grid_kernel, dim3((unsigned)G),
+                                      dim3(PRIM_GRID_THREADS), args, smem, s);
+    }
+  } else {
+    prim_kernel<<<1, PRIM_THREADS, 0, s>>>(dP, N, n, dbest, dpar, dint, dea, deb, dew);
+    e = cudaGetLastError();
+  }
   if (e == cudaSuccess) {
     cudaMemcpyAsync(edge_a, dea, sizeof(int) * (N - 1), cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(edge_b, deb, sizeof(int) * (N - 1), cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(edge_w, dew, sizeof(double) * (N - 1), cudaMemcpyDeviceToHost, s);
     e = cudaStreamSynchronize(s);
   }
+  cudaFree(dcand);
   cleanup();
-  if (e != cudaSuccess) return fail(MHAR_ERR_CUDA, std::string("prim_kernel: ") + cudaGetErrorString(e));
+  if (e != cudaSuccess)
+    return fail(MHAR_ERR_CUDA, std::string(grid_form ? "prim_grid_kernel: " : "prim_kernel: ") +
+                                   cudaGetErrorString(e));
   return 0;
 }
 

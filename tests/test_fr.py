@@ -87,6 +87,27 @@ def test_gpu_mst_equals_oracle(orc, N, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("form", ["cta", "grid", "grid_l2"])
+@pytest.mark.parametrize("case", ["lattice_ties", "wide", "ragged"])
+def test_gpu_mst_forms_equal_oracle(orc, monkeypatch, form, case):
+    # both Prim forms (one CTA; cooperative grid over every SM) edge for edge
+    # against the oracle: an integer lattice with many equal distances (the
+    # tie rule), n beyond the staged-coordinate limit, a ragged pool size
+    from paper_2104_07097_b200 import stats
+    rng = np.random.default_rng(len(case))
+    if case == "lattice_ties":
+        P = rng.integers(0, 12, (4000, 2)).astype(np.float64)
+    elif case == "wide":
+        P = rng.uniform(-1, 1, (300, 4500))
+    else:
+        P = rng.standard_normal((5003, 7))
+    monkeypatch.setenv("MHAR_PRIM", form)
+    ga, gb, gw = stats.minimum_spanning_tree(P)
+    oa, ob, ow = orc.minimum_spanning_tree(P)
+    assert np.array_equal(ga, oa) and np.array_equal(gb, ob) and np.array_equal(gw, ow)
+
+
+@pytest.mark.gpu
 def test_gpu_fr_kats_and_oracle(orc):
     import paper_2104_07097_b200 as mh
     from paper_2104_07097_b200 import stats
