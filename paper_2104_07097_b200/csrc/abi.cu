@@ -115,6 +115,7 @@ struct mhar_ctx {
   double *rsc = nullptr, *csc = nullptr;
   int* rexp = nullptr;
   int64_t KS = 0, i8_row_tiles = 0;
+  int i8_clusters = 0;  // co-resident clusters of the int8 kernel
   unsigned long long* tc_prof = nullptr;  // MHAR_I8_PROFILE: tcgen05 kernels' per-CTA counters
   // structure-aware paths (fastpath.cuh)
   double* diag_coef = nullptr;  // stacked diagonal blocks: per-row coefficient (m)
@@ -387,8 +388,8 @@ int launch_i8(mhar_ctx* c) {
   p.eps_dir = c->opt.eps_dir;
   p.prof = c->tc_prof;
   if (c->tc_prof) cudaMemsetAsync(c->tc_prof, 0, kProfWords * sizeof(unsigned long long) * c->num_sms, c->stream);
-  const int64_t units = p.row_tiles * (p.walk_tiles / 2);
-  const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);
+  const int64_t units = p.row_tiles / I8_PAIRS * (p.walk_tiles / 2);
+  const int grid = I8_CL * (int)std::min<int64_t>(units, c->i8_clusters);
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
   if (c->timing) {
     ev = take_events(c);
@@ -906,7 +907,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
 
   c->n_pad = round_up(c->n, BK);
   c->KT = c->n_pad / BK;
-  c->m_pad = round_up(c->m, fp32 ? TC_N : BM);
+  c->m_pad = round_up(c->m, fp32 ? TC_N : i8 ? (int64_t)I8_N * I8_PAIRS : BM);
   c->m_tiles = c->m_pad / BM;
   c->z_pad = round_up(c->z, tiles ? 2 * TC_M : 64);  // tcgen05: whole CTA-pair walk tiles
   c->ct64 = c->z_pad / 64;
@@ -1014,6 +1015,19 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       cudaStreamSynchronize(c->stream);
       cudaFuncSetAttribute(chord_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)I8_SMEM);
+      {
+        // persistent grid: as many clusters as can be co-resident (a cluster
+        // of 4 needs 4 free SMs in one GPC)
+        cudaLaunchConfig_t lc{};
+        lc.gridDim = dim3((unsigned)(I8_CL * (c->num_sms / I8_CL)));
+        lc.blockDim = dim3(I8_THREADS);
+        lc.dynamicSmemBytes = I8_SMEM;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, chord_i8_kernel, &lc) != cudaSuccess || ncl < 1)
+          ncl = c->num_sms / I8_CL;
+        cudaGetLastError();
+        c->i8_clusters = ncl;
+      }
       if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->tc_prof, kProfWords * (size_t)c->num_sms))) {
         cudaFree(tmp);
         return bail(st);

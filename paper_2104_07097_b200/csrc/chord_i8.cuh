@@ -47,6 +47,18 @@ namespace mhar_dev {
 #ifndef MHAR_I8_PREFETCH
 #define MHAR_I8_PREFETCH 0
 #endif
+// CTAs per cluster: 2 = one CTA pair; 4 = two pairs on adjacent row tiles of
+// the same walk pair, each direction slice fetched once from L2 and
+// multicast into both pairs (each CTA copies half, cp.async.bulk .multicast).
+// Measured (tools/ab_i8.sh, ab_i8_prof.sh): only 33 clusters of 4 are
+// co-resident (132 of 148 SMs), and per SM-clock the multicast run is no
+// faster, so the default stays 2 (40.5 vs 42.0 ms per launch at config 5).
+#ifndef MHAR_I8_CLUSTER
+#define MHAR_I8_CLUSTER 2
+#endif
+constexpr int I8_CL = MHAR_I8_CLUSTER;
+constexpr int I8_PAIRS = I8_CL / 2;  // CTA pairs per cluster = row tiles per cluster unit
+static_assert(I8_CL == 2 || I8_CL == 4, "cluster of one or two CTA pairs");
 constexpr int I8_M = 128;       // walks per CTA (unit: 2 x 128)
 constexpr int I8_N = 128;       // rows per unit
 constexpr int I8_NH = 64;       // rows staged by each CTA of the pair
@@ -176,15 +188,17 @@ struct I8Params {
   unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
 };
 
-// unit u -> (row tile, walk-tile pair): walk pairs inner, so the pairs in
-// flight share a few A tiles and every direction tile stays L2-resident
-__device__ inline void i8_unit(int64_t u, const I8Params& p, int64_t* rt, int64_t* wp) {
+// cluster unit u -> (row tile of pair pp, walk-tile pair): walk pairs inner,
+// so the clusters in flight share a few A tiles and every direction tile stays
+// L2-resident; the pairs of a cluster take adjacent row tiles
+__device__ inline void i8_unit(int64_t u, int pp, const I8Params& p, int64_t* rt, int64_t* wp) {
   const int64_t pairs = p.walk_tiles / 2;
-  *rt = u / pairs;
-  *wp = u - *rt * pairs;
+  const int64_t rg = u / pairs;
+  *rt = rg * I8_PAIRS + pp;
+  *wp = u - rg * pairs;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
+__global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
     chord_i8_kernel(const I8Params p) {
   if (*p.err != kNoError) return;  // read identically by both CTAs of the pair
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -200,16 +214,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
   uint32_t* tptr = reinterpret_cast<uint32_t*>(sr_empty + I8_SR_SLOTS);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t rank = cluster_rank();
-  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  const int64_t n_units = p.row_tiles * (p.walk_tiles / 2);
-  const int my_units = (pair < n_units) ? (int)((n_units - 1 - pair) / npairs + 1) : 0;
+  const uint32_t crank = cluster_rank();
+  const uint32_t rank = crank & 1;          // CTA within its pair (walk tile half)
+  const int pp = (int)(crank >> 1);         // pair within the cluster (row tile)
+  const uint32_t lead = crank & ~1u;        // the pair's MMA-issuing CTA
+  const unsigned short pair_mask = (unsigned short)(3u << (2 * pp));
+  const unsigned short all_mask = (unsigned short)((1u << I8_CL) - 1);
+  const int64_t cl = blockIdx.x / I8_CL, ncl = gridDim.x / I8_CL;
+  const int64_t n_units = p.row_tiles / I8_PAIRS * (p.walk_tiles / 2);
+  const int my_units = (cl < n_units) ? (int)((n_units - 1 - cl) / ncl + 1) : 0;
   const int KS = (int)p.KS;
 
   if (tid == 0) {
     for (int s = 0; s < I8_STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], I8_PAIRS);  // a commit from every pair reading the multicast
       mbar_init(&peer_full[s], 1);
     }
     mbar_init(tfull, 1);
@@ -241,7 +260,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       long long w_empty = 0;
       for (int ui = 0; ui < my_units; ++ui) {
         int64_t rt, wp;
-        i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+        i8_unit(cl + (int64_t)ui * ncl, pp, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
 #if MHAR_I8_PREFETCH
         {
@@ -267,7 +286,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
               const int64_t doff = (wt * p.KS + ks) * (int64_t)I8_D_STAGE + s0 * I8_D_PIECE;
               const int64_t aoff =
                   ((rt * p.KS + ks) * 2 + rank) * (int64_t)(I8_SLICES * I8_A_PIECE) + s0 * I8_A_PIECE;
-              bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
+              if (I8_CL == 4) {
+                // half of the direction bytes each, into this CTA and its
+                // counterpart in the other pair (same walk tile)
+                const uint32_t hb = (uint32_t)(ns * I8_D_PIECE / 2);
+                bulk_g2s_mc(st + pp * hb, p.D8 + doff + pp * hb, hb, &full[stage],
+                            (unsigned short)((1u << rank) | (1u << (rank + 2))), keep);
+              } else {
+                bulk_g2s_hint(st, p.D8 + doff, ns * I8_D_PIECE, &full[stage], keep);
+              }
               bulk_g2s_hint(st + I8_SLOT_A, p.A8 + aoff, ns * I8_A_PIECE, &full[stage], apol);
               if (++stage == I8_STAGES) {
                 stage = 0;
@@ -323,7 +350,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
                   i8_mma2(acc, ddesc(l - i), adesc(i), i8_idesc(l - i == 0, i == 0),
                           (ks > 0 || i > 0) ? 1u : 0u);
               }
-              tc_commit2(&empty[slot[0]]);  // frees the slot in both CTAs when these MMAs finish
+              tc_commit2(&empty[slot[0]], all_mask);  // frees the slot when these MMAs finish
             } else {
 #pragma unroll
               for (int l = I8_PASS_LEVELS; l < I8_LEVELS; ++l) {
@@ -335,11 +362,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
                   i8_mma2(acc, ddesc(l - i), adesc(i), i8_idesc(l - i == 0, i == 0),
                           (ks > 0 || i > i0) ? 1u : 0u);
               }
-              tc_commit2(&empty[slot[0]]);
-              tc_commit2(&empty[slot[1]]);
+              tc_commit2(&empty[slot[0]], all_mask);
+              tc_commit2(&empty[slot[1]], all_mask);
             }
           }
-          tc_commit2(tfull);
+          tc_commit2(tfull, pair_mask);
         }
       }
       if (p.prof) {
@@ -355,7 +382,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       const int slots = my_units * 3 * KS;  // short pass: 1 slot per k step, long pass: 2
       for (int i = 0; i < slots; ++i) {
         mbar_wait(&full[stage], (uint32_t)phase);
-        mbar_arrive_remote(&peer_full[stage], 0);
+        mbar_arrive_remote(&peer_full[stage], lead);
         if (++stage == I8_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -366,7 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
       const uint64_t stream_policy = MHAR_STREAM_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
       for (int ui = 0; ui < my_units; ++ui) {
         int64_t rt, wp;
-        i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+        i8_unit(cl + (int64_t)ui * ncl, pp, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
         const int64_t cb = (rt * p.walk_tiles + wt) * (int64_t)(I8_N * I8_M);
         for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j)
@@ -398,12 +425,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(I8_THREADS, 1)
         if (rank == 0)
           mbar_arrive(tempty);
         else
-          mbar_arrive_remote(tempty, 0);
+          mbar_arrive_remote(tempty, lead);
       }
     };
     for (int ui = 0; ui < my_units; ++ui) {
       int64_t rt, wp;
-      i8_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+      i8_unit(cl + (int64_t)ui * ncl, pp, p, &rt, &wp);
       const int64_t wt = 2 * wp + rank;
       const int64_t c = wt * I8_M + wl;
       const int64_t r0 = rt * I8_N + rq * I8_ROWS_PER_WARP;

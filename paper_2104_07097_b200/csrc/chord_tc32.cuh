@@ -109,11 +109,11 @@ __device__ inline void tc_mma2(uint32_t tmem, uint64_t da, uint64_t db, uint32_t
 }
 // arrive on the barrier at the same smem offset in both CTAs of the pair
 // once every previously issued MMA of this thread has completed
-__device__ inline void tc_commit2(uint64_t* bar) {
+__device__ inline void tc_commit2(uint64_t* bar, unsigned short mask = 3) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
       " [%0], %1;" ::"r"(smem_u32(bar)),
-      "h"((unsigned short)3)
+      "h"(mask)
       : "memory");
 }
 __device__ inline uint32_t cluster_rank() {

@@ -223,6 +223,16 @@ __device__ inline void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// the same copy landing at the same offset in every CTA of ctaMask, each
+// CTA's mbarrier at bar's offset receiving the bytes
+__device__ inline void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                   uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+      : "memory");
+}
 __device__ inline uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
