@@ -1722,16 +1722,8 @@ int mhar_chebyshev_center(const mhar_polytope* p, int device, double* x_out, dou
   }
   if (st) return fail(st, msg);
   // chebyshev.cpp:61-63: the centre must pass containment at kLpFeasTol
+  // (the inequality rows were checked on the device by the solver)
   const int64_t n = p->n;
-  std::vector<double> ax(p->m_in, 0.0);
-  for (int64_t k = 0; k < n; ++k) {
-    const double* col = p->a_in + k * p->m_in;
-    for (int64_t i = 0; i < p->m_in; ++i) ax[i] += col[i] * x_out[k];
-  }
-  for (int64_t i = 0; i < p->m_in; ++i)
-    if (ax[i] > p->b_in[i] + 1e-8)
-      return fail(MHAR_ERR_NUMERICAL_FAILURE,
-                  "NUMERICAL_FAILURE: chebyshev_center: computed center fails containment");
   for (int64_t i = 0; i < p->m_eq; ++i) {
     double s = 0.0;
     for (int64_t k = 0; k < n; ++k) s += p->a_eq[i + k * p->m_eq] * x_out[k];

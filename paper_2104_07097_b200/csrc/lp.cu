@@ -13,7 +13,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -185,24 +188,17 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
   __syncthreads();
   const int row = si[0];
   if (row < 0) return;
-  // capture for the rank-1 update (fcol = T[:,e] is cached above; the pivot
-  // row is divided out by prow_kernel on the whole grid)
+  // capture for the rank-1 update (fcol = T[:,e] is cached above) and the
+  // pivot row divided out (one coalesced sweep; a separate grid-wide launch
+  // cost more in launch gap than it saved)
+  const double piv = fcol[row];
+  const double* __restrict__ Tr = T + (size_t)row * cols;
+#pragma unroll 8
+  for (int j = tid; j < cols; j += kThreads) prow[j] = Tr[j] / piv;
   if (tid == 0) {
-    const double piv = fcol[row];
     pb[0] = b[row] / piv;
     pb[1] = cost[e];
   }
-}
-
-// prow = T[row,:] / T[row,col] for the pivot the select kernel chose
-__global__ void prow_kernel(const double* __restrict__ T, int cols, const int* __restrict__ sel,
-                            const int* __restrict__ done, const double* __restrict__ fcol,
-                            double* __restrict__ prow) {
-  if (*done) return;
-  const int row = sel[1];
-  const double piv = fcol[row];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
-    prow[j] = T[(size_t)row * cols + j] / piv;
 }
 
 // pivot on (row, col): prow = T[row,:]/piv, fcol = T[:,col] captured first
@@ -270,6 +266,92 @@ __global__ void __launch_bounds__(256) pivot_kernel(double* __restrict__ T, doub
   if (threadIdx.x == 0) b[i] -= f * brow;
 }
 
+// The same rank-1 update tiled: a block owns kPivRows rows x one column
+// chunk of 256 x kPivVec double2, each thread keeps its pivot-row segment in
+// registers across the rows (the pivot row is read once per row group, not
+// once per row) and the rows' loads are issued back to back.
+#ifndef MHAR_LP_PIV_ROWS
+#define MHAR_LP_PIV_ROWS 8
+#endif
+#ifndef MHAR_LP_PIV_VEC
+#define MHAR_LP_PIV_VEC 2
+#endif
+constexpr int kPivRows = MHAR_LP_PIV_ROWS, kPivVec = MHAR_LP_PIV_VEC;
+__global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
+                                                         double* __restrict__ b,
+                                                         double* __restrict__ cost, int* basis,
+                                                         int rows, int cols,
+                                                         const int* __restrict__ sel,
+                                                         const int* __restrict__ done,
+                                                         const double* __restrict__ prow,
+                                                         const double* __restrict__ fcol,
+                                                         const double* pb) {
+  if (*done) return;
+  const int col = sel[0], row = sel[1];
+  const double brow = pb[0];
+  const double cf = pb[1];
+  const int c2 = cols >> 1;
+  const int j0 = blockIdx.x * (256 * kPivVec) + threadIdx.x;
+  const double2* __restrict__ p2 = reinterpret_cast<const double2*>(prow);
+  double2 q[kPivVec];
+#pragma unroll
+  for (int v = 0; v < kPivVec; ++v) {
+    const int j = j0 + 256 * v;
+    q[v] = j < c2 ? __ldg(p2 + j) : make_double2(0.0, 0.0);
+  }
+  const int i0 = blockIdx.y * kPivRows;
+#pragma unroll 2
+  for (int r = 0; r < kPivRows; ++r) {
+    const int i = i0 + r;
+    if (i > rows) break;
+    if (i == rows) {  // the cost row (captured cost[col] in pb[1])
+      if (cf != 0.0)
+#pragma unroll
+        for (int v = 0; v < kPivVec; ++v) {
+          const int j = j0 + 256 * v;
+          if (j < c2) {
+            const double c0 = 2 * j == col ? 0.0 : cost[2 * j] - cf * q[v].x;
+            const double c1 = 2 * j + 1 == col ? 0.0 : cost[2 * j + 1] - cf * q[v].y;
+            cost[2 * j] = c0;
+            cost[2 * j + 1] = c1;
+          }
+        }
+      break;
+    }
+    double2* __restrict__ Ti = reinterpret_cast<double2*>(T + (size_t)i * cols);
+    if (i == row) {
+#pragma unroll
+      for (int v = 0; v < kPivVec; ++v) {
+        const int j = j0 + 256 * v;
+        if (j < c2) Ti[j] = q[v];
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        b[i] = brow;
+        basis[i] = col;
+      }
+      continue;
+    }
+    const double f = fcol[i];
+    if (f == 0.0) continue;
+    double2 t[kPivVec];
+#pragma unroll
+    for (int v = 0; v < kPivVec; ++v) {
+      const int j = j0 + 256 * v;
+      if (j < c2) t[v] = Ti[j];
+    }
+#pragma unroll
+    for (int v = 0; v < kPivVec; ++v) {
+      const int j = j0 + 256 * v;
+      if (j < c2) {
+        t[v].x = fma(-f, q[v].x, t[v].x);
+        t[v].y = fma(-f, q[v].y, t[v].y);
+        Ti[j] = t[v];
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) b[i] -= f * brow;
+  }
+}
+
 // v_i = a_i x + |a_i| r - b_i over all rows (A column-major m x n)
 __global__ void violation_kernel(const double* __restrict__ A, const double* __restrict__ norms,
                                  const double* __restrict__ bvec, const double* __restrict__ x,
@@ -279,6 +361,66 @@ __global__ void violation_kernel(const double* __restrict__ A, const double* __r
     double s = 0.0;
     for (int64_t k = 0; k < n; ++k) s = fma(A[i + k * m], x[k], s);
     v[i] = s + norms[i] * r - bvec[i];
+  }
+}
+
+// |a_i| accumulated in ascending k without contraction (the host loop's
+// order, so the LP sees the same norms)
+__global__ void row_norms_kernel(const double* __restrict__ A, int64_t m, int64_t n,
+                                 double* __restrict__ norms) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int64_t k = 0; k < n; ++k) {
+      const double a = A[i + k * m];
+      s = __dadd_rn(s, __dmul_rn(a, a));
+    }
+    norms[i] = sqrt(s);
+  }
+}
+
+// initial working set: block (k, sign) finds the first row maximising
+// sign * a_ik / |a_i| among the positive values (-1 if none)
+__global__ void __launch_bounds__(256) ws_argmax_kernel(const double* __restrict__ A,
+                                                        const double* __restrict__ norms,
+                                                        int64_t m, int64_t* __restrict__ out) {
+  __shared__ double sv[8];
+  __shared__ long long si[8];
+  const int64_t k = blockIdx.x;
+  const double sgn = blockIdx.y ? 1.0 : -1.0;
+  const double* __restrict__ col = A + k * m;
+  double bv = 0.0;
+  long long bi = -1;
+  for (int64_t i = threadIdx.x; i < m; i += 256) {
+    const double v = sgn * col[i] / fmax(norms[i], 1e-300);
+    if (v > bv) {  // ascending i per thread: strict > keeps the first
+      bv = v;
+      bi = i;
+    }
+  }
+  auto better = [](double v, long long i, double bv, long long bi) {
+    return i >= 0 && (bi < 0 || v > bv || (v == bv && i < bi));
+  };
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+    const long long oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+    if (better(ov, oi, bv, bi)) {
+      bv = ov;
+      bi = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w)
+      if (better(sv[w], si[w], bv, bi)) {
+        bv = sv[w];
+        bi = si[w];
+      }
+    out[2 * k + blockIdx.y] = bi;
   }
 }
 
@@ -306,6 +448,19 @@ struct Dev {
   }
 };
 
+// MHAR_LP_PROFILE=1: wall time of the centring stages on stderr
+struct LpClock {
+  bool on = std::getenv("MHAR_LP_PROFILE") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[lp profile] %-28s %9.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 int err(std::string* msg, int code, const std::string& text) {
   *msg = text;
   return code;
@@ -324,6 +479,7 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
             const std::vector<int>& is_eq, const std::vector<int>& is_free,
             const std::vector<double>& obj, int m, int nv, double perturb, double scale,
             int l1_row, std::vector<double>* x, long* pivots, std::string* msg) {
+  LpClock sclk;
   std::vector<int> var_col(nv);
   int ncols = 0;
   for (int v = 0; v < nv; ++v) {
@@ -388,9 +544,18 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
   const long budget = 10000 + 200L * (m + total);
   long npiv = 0;
   int rows = m;
+  // MHAR_LP_PIVOT=row: one block per tableau row (the first form)
+  const char* piv_env = std::getenv("MHAR_LP_PIVOT");
+  const bool row_form = piv_env && !std::strcmp(piv_env, "row");
+  const dim3 tile_grid((unsigned)((W / 2 + 256 * kPivVec - 1) / (256 * kPivVec)),
+                       (unsigned)((rows + 1 + kPivRows - 1) / kPivRows));
   auto pivot_launch = [&](const int* done) {
-    pivot_kernel<<<rows + 1, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, d.sel, done,
-                                             d.prow, d.fcol, d.pb);
+    if (row_form)
+      pivot_kernel<<<rows + 1, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, d.sel, done,
+                                               d.prow, d.fcol, d.pb);
+    else
+      pivot_tile_kernel<<<tile_grid, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, d.sel,
+                                                    done, d.prow, d.fcol, d.pb);
   };
   // a host-chosen pivot (artificials driven out after phase one)
   auto pivot = [&](int row, int col) {
@@ -411,8 +576,6 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
       for (int k = 0; k < batch; ++k) {
         select_kernel<<<1, kThreads, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, limit_col,
                                                d.ctl, d.sel, d.prow, d.fcol, d.pb);
-        prow_kernel<<<std::max(1, std::min(64, (W + 255) / 256)), 256, 0, d.s>>>(
-            d.T, W, d.sel, &d.ctl->done, d.fcol, d.prow);
         pivot_launch(&d.ctl->done);
       }
       cudaMemcpyAsync(&h, d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, d.s);
@@ -436,7 +599,9 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
       if (has_art[i])
         for (int j = 0; j < structural; ++j) c1[j] += T[(size_t)i * W + j];
     cudaMemcpyAsync(d.cost, c1.data(), sizeof(double) * W, cudaMemcpyHostToDevice, d.s);
+    sclk.mark("  tableau build + upload");
     const int st = run_phase(total);
+    sclk.mark("  phase one");
     if (st == 100) return err(msg, 100, "simplex: CUDA failure");
     if (st == 10) return err(msg, 10, "CYCLE_SUSPECTED: solve_lp: pivot budget exhausted");
     if (st == 7) return err(msg, 12, "NUMERICAL_FAILURE: phase one reported an unbounded ray");
@@ -504,7 +669,9 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
     for (int j = 0; j < W; ++j) red[j] -= cb * Ti[j];
   }
   cudaMemcpyAsync(d.cost, red.data(), sizeof(double) * W, cudaMemcpyHostToDevice, d.s);
+  sclk.mark("  drive-out + phase-two costs");
   const int st = run_phase(structural);
+  sclk.mark("  phase two");
   if (st == 100) return err(msg, 100, "simplex: CUDA failure");
   if (st == 10) return err(msg, 10, "CYCLE_SUSPECTED: solve_lp: pivot budget exhausted");
   if (st == 7)
@@ -533,11 +700,7 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
                      const double* b_eq, int64_t me, int64_t n, int device, double* x_out,
                      double* radius, LpStats* stats, std::string* msg) {
   if (cudaSetDevice(device) != cudaSuccess) return err(msg, 100, "cudaSetDevice failed");
-  // row norms and scale
-  std::vector<double> norms(m, 0.0);
-  for (int64_t k = 0; k < n; ++k)
-    for (int64_t i = 0; i < m; ++i) norms[i] += a_in[i + k * m] * a_in[i + k * m];
-  for (auto& v : norms) v = std::sqrt(v);
+  LpClock clk;
   double scale = 1.0;
   for (int64_t i = 0; i < m; ++i) scale = std::max(scale, std::fabs(b_in[i]));
   // device copies for the violation scan
@@ -558,32 +721,49 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
     return err(msg, 100, "chebyshev_center: device allocation failed");
   }
   cudaMemcpy(dA, a_in, sizeof(double) * m * n, cudaMemcpyHostToDevice);
-  cudaMemcpy(dN, norms.data(), sizeof(double) * m, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, b_in, sizeof(double) * m, cudaMemcpyHostToDevice);
+  const int64_t gm = std::max<int64_t>(1, std::min<int64_t>(4096, (m + 255) / 256));
+  // row norms on the device (the LP's radius coefficients)
+  std::vector<double> norms(m);
+  row_norms_kernel<<<(unsigned)gm, 256>>>(dA, m, n, dN);
+  if (cudaMemcpy(norms.data(), dN, sizeof(double) * m, cudaMemcpyDeviceToHost) != cudaSuccess) {
+    free_all();
+    return err(msg, 100, "chebyshev_center: row norms failed");
+  }
+  clk.mark("upload + norms");
 
   // initial working set: per coordinate and sign the row that bounds it most
   // tightly (largest a_ij / |a_i|), so the restricted LP is usually bounded
   std::vector<char> in_w(m, 0);
   std::vector<int64_t> work;
-  for (int64_t k = 0; k < n; ++k)
-    for (int sgn = -1; sgn <= 1; sgn += 2) {
-      int64_t best = -1;
-      double bv = 0.0;
-      for (int64_t i = 0; i < m; ++i) {
-        const double v = sgn * a_in[i + k * m] / std::max(norms[i], 1e-300);
-        if (v > bv) {
-          bv = v;
-          best = i;
+  {
+    int64_t* dbest = nullptr;
+    std::vector<int64_t> best(2 * n);
+    if (cudaMalloc(&dbest, sizeof(int64_t) * 2 * n) != cudaSuccess) {
+      free_all();
+      return err(msg, 100, "chebyshev_center: device allocation failed");
+    }
+    ws_argmax_kernel<<<dim3((unsigned)n, 2), 256>>>(dA, dN, m, dbest);
+    const cudaError_t e =
+        cudaMemcpy(best.data(), dbest, sizeof(int64_t) * 2 * n, cudaMemcpyDeviceToHost);
+    cudaFree(dbest);
+    if (e != cudaSuccess) {
+      free_all();
+      return err(msg, 100, "chebyshev_center: working-set scan failed");
+    }
+    for (int64_t k = 0; k < n; ++k)
+      for (int sg = 0; sg < 2; ++sg) {  // sign -1 first, as the scan order
+        const int64_t i = best[2 * k + sg];
+        if (i >= 0 && !in_w[i]) {
+          in_w[i] = 1;
+          work.push_back(i);
         }
       }
-      if (best >= 0 && !in_w[best]) {
-        in_w[best] = 1;
-        work.push_back(best);
-      }
-    }
+  }
   if ((int64_t)work.size() == m) {
     // everything is already in
   }
+  clk.mark("initial working set");
   const double box = 1e6 * scale;  // temporary bound; touching it means unbounded
   std::vector<double> xr;
   int rounds = 0;
@@ -618,6 +798,7 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
     for (double eps : {1e-7, 1e-10, 0.0}) {
       status = simplex(A, rhs, is_eq, is_free, obj, mw, nv, eps * scale, scale, l1_row, &xr,
                        &pivots, msg);
+      clk.mark("simplex");
       if (status != kPerturbedOnly) break;
     }
     if (status) break;
@@ -633,6 +814,7 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
     std::vector<int64_t> viol;
     for (int64_t i = 0; i < m; ++i)
       if (!in_w[i] && v[i] > 1e-10 * scale) viol.push_back(i);
+    clk.mark("violation scan");
     if (viol.empty()) break;
     const size_t add = std::min<size_t>(viol.size(), (size_t)std::max<int64_t>(64, 2 * n));
     std::partial_sort(viol.begin(), viol.begin() + add, viol.end(),
@@ -641,6 +823,24 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
       in_w[viol[t]] = 1;
       work.push_back(viol[t]);
     }
+  }
+  bool outside = false;
+  if (!status) {
+    // chebyshev.cpp:61-63: the centre must pass containment at kLpFeasTol
+    // (a_i x - b_i over every row on the device: the scan with r = 0)
+    cudaMemcpy(dX, xr.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
+    violation_kernel<<<(unsigned)gm, 256>>>(dA, dN, dB, dX, 0.0, m, n, dV);
+    std::vector<double> v(m);
+    if (cudaMemcpy(v.data(), dV, sizeof(double) * m, cudaMemcpyDeviceToHost) != cudaSuccess) {
+      status = err(msg, 100, "chebyshev_center: containment scan failed");
+    } else {
+      for (int64_t i = 0; i < m; ++i)
+        if (v[i] > 1e-8) {
+          outside = true;  // reported after the unbounded / no-interior checks
+          break;
+        }
+    }
+    clk.mark("containment");
   }
   free_all();
   if (stats) {
@@ -658,6 +858,8 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
   if (*radius <= 1e-10)  // chebyshev.hpp:21 kMinInteriorRadius
     return err(msg, 6, "NO_INTERIOR: chebyshev_center: optimal radius " + std::to_string(*radius) +
                            " leaves no interior to walk in");
+  if (outside)
+    return err(msg, 12, "NUMERICAL_FAILURE: chebyshev_center: computed center fails containment");
   return 0;
 }
 
