@@ -33,6 +33,7 @@ constexpr double kDegenerateStep = 1e-12;
 constexpr double kReducedCostTol = 1e-9;
 constexpr double kFeasTol = 1e-8;
 constexpr int kThreads = 1024;
+constexpr int kRegRows = 8;  // ratio-test rows per thread kept in registers
 
 // ---------------------------------------------------------------- kernels --
 // Tableau T: rows x cols row-major; b: rows; cost: cols.
@@ -62,9 +63,10 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
                                                           int* out /* entering, leaving */,
                                                           double* prow, double* fcol,
                                                           double* pb /* [b_row/piv, cost_col] */) {
+  static_assert(kThreads == 1024, "one reduction partial per lane of warp 0");
   __shared__ double sv[kThreads / 32];
-  __shared__ int si[kThreads / 32];
-  __shared__ int s_enter;
+  __shared__ int si[kThreads / 32], sb[kThreads / 32];
+  __shared__ int s_enter, s_row;
   __shared__ double s_min;
   __shared__ int s_go;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -106,27 +108,49 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
     si[warp] = bi;
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < kThreads / 32; ++w)
-      if (bland ? (si[w] < bi) : (sv[w] > bv || (sv[w] == bv && si[w] < bi))) {
-        bv = sv[w];
-        bi = si[w];
+  if (warp == 0) {  // kThreads / 32 == 32 partials: one per lane
+    bv = sv[lane];
+    bi = si[lane];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xFFFFFFFFu, bv, o);
+      const int oi = __shfl_xor_sync(0xFFFFFFFFu, bi, o);
+      if (bland ? (oi < bi) : (ov > bv || (ov == bv && oi < bi))) {
+        bv = ov;
+        bi = oi;
       }
-    s_enter = (bi == 0x7FFFFFFF) ? -1 : bi;
-    out[0] = s_enter;
-    if (s_enter < 0) {  // optimal
-      ctl->done = 1;
-      ctl->status = 0;
+    }
+    if (lane == 0) {
+      s_enter = (bi == 0x7FFFFFFF) ? -1 : bi;
+      out[0] = s_enter;
+      if (s_enter < 0) {  // optimal
+        ctl->done = 1;
+        ctl->status = 0;
+      }
     }
   }
   __syncthreads();
   const int e = s_enter;
   if (e < 0) return;
   // ratio test, pass 1: minimum ratio; the entering column (one strided
-  // sector per row) is cached in fcol for pass 2 and the rank-1 update
-  double mr = __longlong_as_double(0x7FF0000000000000LL);
-#pragma unroll 4
-  for (int i = tid; i < rows; i += kThreads) {
+  // sector per row) is cached in fcol for the rank-1 update, and the first
+  // kRegRows rows per thread keep their ratios in registers for pass 2
+  const double kInf = __longlong_as_double(0x7FF0000000000000LL);
+  double ra[kRegRows];
+  double mr = kInf;
+#pragma unroll
+  for (int q = 0; q < kRegRows; ++q) {
+    const int i = tid + q * kThreads;
+    ra[q] = kInf;
+    if (i < rows) {
+      const double a = T[(size_t)i * cols + e];
+      fcol[i] = a;
+      if (a > kPivotTol) {
+        ra[q] = b[i] / a;
+        mr = fmin(mr, ra[q]);
+      }
+    }
+  }
+  for (int i = tid + kRegRows * kThreads; i < rows; i += kThreads) {
     const double a = T[(size_t)i * cols + e];
     fcol[i] = a;
     if (a > kPivotTol) mr = fmin(mr, b[i] / a);
@@ -134,17 +158,28 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
   for (int o = 16; o > 0; o >>= 1) mr = fmin(mr, __shfl_xor_sync(0xFFFFFFFFu, mr, o));
   if (lane == 0) sv[warp] = mr;
   __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < kThreads / 32; ++w) mr = fmin(mr, sv[w]);
-    s_min = mr;
+  if (warp == 0) {
+    mr = sv[lane];
+    for (int o = 16; o > 0; o >>= 1) mr = fmin(mr, __shfl_xor_sync(0xFFFFFFFFu, mr, o));
+    if (lane == 0) s_min = mr;
   }
   __syncthreads();
   // pass 2: among ratios within 1e-15 of the minimum, the smallest basic column
   const double lim = s_min + 1e-15;
   int best_basic = 0x7FFFFFFF, best_row = -1;
-  if (s_min < __longlong_as_double(0x7FF0000000000000LL)) {
-#pragma unroll 4
-    for (int i = tid; i < rows; i += kThreads) {
+  if (s_min < kInf) {
+#pragma unroll
+    for (int q = 0; q < kRegRows; ++q) {
+      const int i = tid + q * kThreads;
+      if (ra[q] <= lim) {
+        const int bs = basis[i];
+        if (bs < best_basic) {
+          best_basic = bs;
+          best_row = i;
+        }
+      }
+    }
+    for (int i = tid + kRegRows * kThreads; i < rows; i += kThreads) {
       const double a = fcol[i];
       if (a > kPivotTol && b[i] / a <= lim && basis[i] < best_basic) {
         best_basic = basis[i];
@@ -162,31 +197,38 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
   }
   if (lane == 0) {
     si[warp] = best_row;
-    sv[warp] = (double)best_basic;
+    sb[warp] = best_basic;
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < kThreads / 32; ++w)
-      if (sv[w] < (double)best_basic) {
-        best_basic = (int)sv[w];
-        best_row = si[w];
+  if (warp == 0) {
+    best_row = si[lane];
+    best_basic = sb[lane];
+    for (int o = 16; o > 0; o >>= 1) {
+      const int ob = __shfl_xor_sync(0xFFFFFFFFu, best_basic, o);
+      const int orow = __shfl_xor_sync(0xFFFFFFFFu, best_row, o);
+      if (ob < best_basic) {
+        best_basic = ob;
+        best_row = orow;
       }
-    out[1] = best_row;
-    if (best_row < 0) {  // unbounded ray
-      ctl->done = 1;
-      ctl->status = 7;
-    } else {
-      if (s_min < kDegenerateStep) {
-        if (++ctl->stall > ctl->stall_limit) ctl->bland = 1;
-      } else {
-        ctl->stall = 0;
-      }
-      ++ctl->npiv;
     }
-    si[0] = best_row;
+    if (lane == 0) {
+      out[1] = best_row;
+      if (best_row < 0) {  // unbounded ray
+        ctl->done = 1;
+        ctl->status = 7;
+      } else {
+        if (s_min < kDegenerateStep) {
+          if (++ctl->stall > ctl->stall_limit) ctl->bland = 1;
+        } else {
+          ctl->stall = 0;
+        }
+        ++ctl->npiv;
+      }
+      s_row = best_row;
+    }
   }
   __syncthreads();
-  const int row = si[0];
+  const int row = s_row;
   if (row < 0) return;
   // capture for the rank-1 update (fcol = T[:,e] is cached above) and the
   // pivot row divided out (one coalesced sweep; a separate grid-wide launch
