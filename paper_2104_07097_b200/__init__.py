@@ -635,21 +635,29 @@ def chebyshev_center(p: Polytope, device: int = 0) -> ChebyshevCenter:
 
 
 def run(p: Polytope, cfg: SamplerConfig, x0=None, rng: str = "philox", slack: str = "incremental",
-        device: int = 0) -> SampleSet:
+        device: int = 0, clock=None) -> SampleSet:
     """run() (sampler.cpp:274-335) on one B200.  Without x0 the start is the
     Chebyshev centre (sampler.cpp:276), computed before the clock starts as
-    in the reference; with x0 that warm start replaces it (start_radius 0)."""
+    in the reference; with x0 that warm start replaces it (start_radius 0).
+    `clock` (the reference's ClockFn, sampler.cpp:278-282) is read once
+    before the projector is built and once after the last collection; by
+    default the engine's own run timer supplies `seconds`."""
     rc = resolve(cfg, p)
     radius = 0.0
     if x0 is None:
         center = chebyshev_center(p, device=device)
         x0, radius = center.x, center.radius
+    t0 = clock() if clock is not None else None
     projector = compute_projection(p.a_eq) if p.num_equalities() > 0 else None
     windows = (rc.t_target + rc.z - 1) // rc.z
     with Engine(p, rc.z, seed=rc.seed, projector=projector, eps_dir=rc.eps_dir,
                 eps_feas=rc.eps_feas, rng=rng, slack=slack, device=device) as eng:
         samples, st = eng.run(x0, rc.phi, windows, rc.burn_in,
                               rc.reproject_every if projector is not None else 0)
+    seconds = st.seconds if clock is None else clock() - t0
     return SampleSet(samples=samples, config=rc, start=np.asarray(x0, dtype=np.float64),
-                     start_radius=radius, seconds=st.seconds, iterate_count=st.iterate_count,
+                     start_radius=radius, seconds=seconds, iterate_count=st.iterate_count,
                      windows=st.windows, redraw_count=st.redraw_count)
+
+
+from .throughput import BenchConfig, BenchRecord, measure_throughput, sweep_padding  # noqa: E402

@@ -12,10 +12,12 @@
 #include <fstream>
 #include <sstream>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "../../../oracle/mhar_oracle.h"
+#include "mhar/bench.hpp"
 #include "mhar/io.hpp"
 #include "mhar/sampler.hpp"
 
@@ -292,6 +294,55 @@ int main() {
     CHECK(man.find("\"iterate_count\": 1280") != std::string::npos);
     CHECK(man.find("\"eps_dir\": 1e-11") != std::string::npos);
     if (std::system(("rm -rf " + dir).c_str()) != 0) CHECK(false);
+  });
+
+  // proj/tests/test_bench.cpp with scripted clocks
+  auto scripted = [](std::vector<double> t) {
+    auto st = std::make_shared<std::pair<std::vector<double>, size_t>>(std::move(t), 0);
+    return mhar::ClockFn([st]() { return st->first[st->second++]; });
+  };
+  run_case("throughput: a scripted thousand-second run reports three thousand per second",
+           [&] {
+             mhar::BenchConfig cfg;
+             cfg.phi = 30000;
+             cfg.repetitions = 1;
+             cfg.seed = 3;
+             const auto r = mhar::measure_throughput(mhar::make_hypercube(2), 100, cfg,
+                                                     "hypercube(2)", scripted({0.0, 1000.0}));
+             CHECK(r.total_samples == 3000000);
+             CHECK(r.run_seconds.size() == 1 && r.run_seconds[0] == 1000.0);
+             CHECK(r.mean_sps == 3000.0 && r.std_sps == 0.0);
+           });
+  run_case("throughput: zero counts are rejected, rates are iterates over seconds", [&] {
+    const auto cube = mhar::make_hypercube(3);
+    mhar::BenchConfig cfg;
+    cfg.repetitions = 0;
+    expect_error(mhar::ErrorCode::invalid_argument,
+                 [&] { mhar::measure_throughput(cube, 1, cfg, "hypercube(3)"); });
+    cfg.repetitions = 1;
+    expect_error(mhar::ErrorCode::invalid_argument,
+                 [&] { mhar::measure_throughput(cube, 0, cfg, "hypercube(3)"); });
+    expect_error(mhar::ErrorCode::invalid_argument,
+                 [&] { mhar::sweep_padding(cube, {}, cfg, "hypercube(3)"); });
+    cfg.phi = 7;
+    cfg.windows = 3;
+    cfg.repetitions = 2;
+    const auto r = mhar::measure_throughput(cube, 5, cfg, "hypercube(3)", scripted({0, 4, 0, 8}));
+    CHECK(r.total_samples == 5 * 7 * 3 && r.run_sps.size() == 2);
+    for (size_t k = 0; k < 2; ++k) CHECK(r.run_sps[k] == (double)r.total_samples / r.run_seconds[k]);
+    CHECK(r.mean_sps == (r.run_sps[0] + r.run_sps[1]) / 2.0);
+  });
+  run_case("throughput: a one-element sweep equals the direct measurement", [&] {
+    const auto simplex = mhar::make_simplex(3);
+    mhar::BenchConfig cfg;
+    cfg.phi = 4;
+    cfg.repetitions = 2;
+    cfg.seed = 9;
+    const auto d = mhar::measure_throughput(simplex, 2, cfg, "simplex(3)", scripted({0, 1, 1, 3}));
+    const auto s = mhar::sweep_padding(simplex, {2}, cfg, "simplex(3)", scripted({0, 1, 1, 3}));
+    CHECK(s.size() == 1 && s[0].z == d.z && s[0].total_samples == d.total_samples);
+    CHECK(s[0].run_seconds == d.run_seconds && s[0].mean_sps == d.mean_sps &&
+          s[0].std_sps == d.std_sps);
   });
 
   std::printf("%d passed, %d failed checks\n", g_pass, g_fail);
