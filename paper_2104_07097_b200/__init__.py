@@ -660,4 +660,5 @@ def run(p: Polytope, cfg: SamplerConfig, x0=None, rng: str = "philox", slack: st
                      windows=st.windows, redraw_count=st.redraw_count)
 
 
-from .throughput import BenchConfig, BenchRecord, measure_throughput, sweep_padding  # noqa: E402
+from .throughput import (BenchConfig, BenchRecord, bench_csv_string, bench_json_string,  # noqa: E402
+                         measure_throughput, sweep_padding, write_bench_csv, write_bench_json)

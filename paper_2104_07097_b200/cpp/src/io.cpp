@@ -184,4 +184,54 @@ Matrix read_sample_bin(const std::string& path) {
   return out;
 }
 
+// Throughput records (io.hpp bench writers): one CSV line per record,
+// doubles as shortest round trips; JSON in dump(2) layout, sorted keys.
+std::string bench_csv_string(const std::vector<BenchRecord>& records) {
+  std::string s = "figure,n,z,phi,windows,total_samples,mean_sps,std_sps,runs\n";
+  for (const BenchRecord& r : records)
+    s += r.figure + "," + std::to_string(r.n) + "," + std::to_string(r.z) + "," +
+         std::to_string(r.phi) + "," + std::to_string(r.windows) + "," +
+         std::to_string(r.total_samples) + "," + format_double(r.mean_sps) + "," +
+         format_double(r.std_sps) + "," + std::to_string(r.run_seconds.size()) + "\n";
+  return s;
+}
+
+void write_bench_csv(const std::string& path, const std::vector<BenchRecord>& records) {
+  write_text(path, bench_csv_string(records));
+}
+
+std::string bench_json_string(const std::vector<BenchRecord>& records) {
+  auto array = [](const std::vector<double>& v, const std::string& pad) {
+    if (v.empty()) return std::string("[]");
+    std::string a = "[\n";
+    for (size_t i = 0; i < v.size(); ++i)
+      a += pad + "  " + json_double(v[i]) + (i + 1 < v.size() ? ",\n" : "\n");
+    return a + pad + "]";
+  };
+  std::string s = "{\n  \"format_version\": 1,\n  \"records\": ";
+  if (records.empty()) return s + "[]\n}\n";
+  s += "[\n";
+  for (size_t i = 0; i < records.size(); ++i) {
+    const BenchRecord& r = records[i];
+    const std::string p = "      ";
+    s += "    {\n";
+    s += p + "\"figure\": " + json_string(r.figure) + ",\n";
+    s += p + "\"mean_sps\": " + json_double(r.mean_sps) + ",\n";
+    s += p + "\"n\": " + std::to_string(r.n) + ",\n";
+    s += p + "\"phi\": " + std::to_string(r.phi) + ",\n";
+    s += p + "\"run_seconds\": " + array(r.run_seconds, p) + ",\n";
+    s += p + "\"run_sps\": " + array(r.run_sps, p) + ",\n";
+    s += p + "\"std_sps\": " + json_double(r.std_sps) + ",\n";
+    s += p + "\"total_samples\": " + std::to_string(r.total_samples) + ",\n";
+    s += p + "\"windows\": " + std::to_string(r.windows) + ",\n";
+    s += p + "\"z\": " + std::to_string(r.z) + "\n";
+    s += i + 1 < records.size() ? "    },\n" : "    }\n";
+  }
+  return s + "  ]\n}\n";
+}
+
+void write_bench_json(const std::string& path, const std::vector<BenchRecord>& records) {
+  write_text(path, bench_json_string(records));
+}
+
 }  // namespace mhar

@@ -345,6 +345,44 @@ int main() {
           s[0].std_sps == d.std_sps);
   });
 
+  run_case("throughput csv and json (test_io.cpp bench cases)", [] {
+    mhar::BenchRecord r;
+    r.figure = "hypercube(50)";
+    r.n = 50;
+    r.z = 16;
+    r.phi = 1000;
+    r.windows = 1;
+    r.total_samples = 16000;
+    r.run_seconds = {1.0, 2.0};
+    r.run_sps = {16000.0, 8000.0};
+    r.mean_sps = 12000.0;
+    r.std_sps = 4000.0;
+    const std::string header = "figure,n,z,phi,windows,total_samples,mean_sps,std_sps,runs\n";
+    const std::string text = mhar::bench_csv_string({r});
+    CHECK(text.rfind(header, 0) == 0);
+    CHECK(text.substr(header.size()) == "hypercube(50),50,16,1000,1,16000,12000,4000,2\n");
+    CHECK(mhar::bench_csv_string({}) == header);
+    mhar::BenchRecord q;
+    q.figure = "simplex(10)";
+    q.n = 10;
+    q.z = 4;
+    q.phi = 729;
+    q.windows = 2;
+    q.total_samples = 5832;
+    q.run_seconds = {0.5, 0.25, 0.125};
+    q.run_sps = {11664.0, 23328.0, 46656.0};
+    q.mean_sps = 27216.0;
+    q.std_sps = 17750.0;
+    const std::string js = mhar::bench_json_string({q});
+    CHECK(js.rfind("{\n  \"format_version\": 1,\n  \"records\": [\n    {\n", 0) == 0);
+    CHECK(js.find("\"figure\": \"simplex(10)\"") != std::string::npos);
+    CHECK(js.find("\"run_sps\": [\n        11664.0,\n        23328.0,\n        46656.0\n      ]") !=
+          std::string::npos);
+    CHECK(js.find("\"mean_sps\": 27216.0") != std::string::npos);
+    expect_error(mhar::ErrorCode::io_failure,
+                 [&] { mhar::write_bench_json("/nonexistent/dir/b.json", {q}); });
+  });
+
   std::printf("%d passed, %d failed checks\n", g_pass, g_fail);
   return g_fail == 0 ? 0 : 1;
 }

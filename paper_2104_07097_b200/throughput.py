@@ -77,3 +77,46 @@ def sweep_padding(p, z_values: Sequence[int], cfg: BenchConfig, figure: str,
                         "INVALID_ARGUMENT: sweep_padding: z list is empty")
     return [measure_throughput(p, int(z), cfg, figure, clock=clock, x0=x0, device=device)
             for z in z_values]
+
+
+def _fmt(v: float) -> str:
+    """Shortest round-trip decimal (io.hpp:13); integral values without '.0'."""
+    r = repr(float(v))
+    return r[:-2] if r.endswith(".0") else r
+
+
+def bench_csv_string(records: Sequence[BenchRecord]) -> str:
+    """bench_csv_string (io.hpp): header, then one line per record."""
+    s = "figure,n,z,phi,windows,total_samples,mean_sps,std_sps,runs\n"
+    for r in records:
+        s += (f"{r.figure},{r.n},{r.z},{r.phi},{r.windows},{r.total_samples},"
+              f"{_fmt(r.mean_sps)},{_fmt(r.std_sps)},{len(r.run_seconds)}\n")
+    return s
+
+
+def bench_json_string(records: Sequence[BenchRecord]) -> str:
+    """bench_json_string (io.hpp): {"format_version": 1, "records": [...]},
+    sorted keys, two-space indent, per-run detail kept."""
+    import json
+    recs = [{"figure": r.figure, "n": r.n, "z": r.z, "phi": r.phi, "windows": r.windows,
+             "total_samples": r.total_samples, "mean_sps": float(r.mean_sps),
+             "std_sps": float(r.std_sps), "run_seconds": [float(v) for v in r.run_seconds],
+             "run_sps": [float(v) for v in r.run_sps]} for r in records]
+    return json.dumps({"format_version": 1, "records": recs}, indent=2, sort_keys=True) + "\n"
+
+
+def write_bench_csv(path: str, records: Sequence[BenchRecord]) -> None:
+    _write(path, bench_csv_string(records))
+
+
+def write_bench_json(path: str, records: Sequence[BenchRecord]) -> None:
+    _write(path, bench_json_string(records))
+
+
+def _write(path: str, text: str) -> None:
+    from . import MharError, ErrorCode
+    try:
+        with open(path, "w") as f:
+            f.write(text)
+    except OSError as e:
+        raise MharError(ErrorCode.io_failure, f"IO_FAILURE: cannot write {path}: {e}") from e

@@ -69,3 +69,29 @@ def test_acceptance8_padding_raises_throughput():
     wide = mh.measure_throughput(cube, 16, cfg, "hypercube(50)")
     assert wide.mean_sps >= narrow.mean_sps
     assert narrow.total_samples == 1000 and wide.total_samples == 16000
+
+
+def test_bench_csv_and_json_formats(tmp_path):
+    # proj/tests/test_io.cpp throughput cases
+    r = mh.BenchRecord(figure="hypercube(50)", n=50, z=16, phi=1000, windows=1,
+                       total_samples=16000, run_seconds=[1.0, 2.0], run_sps=[16000.0, 8000.0],
+                       mean_sps=12000.0, std_sps=4000.0)
+    header = "figure,n,z,phi,windows,total_samples,mean_sps,std_sps,runs\n"
+    text = mh.bench_csv_string([r])
+    assert text == header + "hypercube(50),50,16,1000,1,16000,12000,4000,2\n"
+    assert mh.bench_csv_string([]) == header
+    q = mh.BenchRecord(figure="simplex(10)", n=10, z=4, phi=729, windows=2, total_samples=5832,
+                       run_seconds=[0.5, 0.25, 0.125], run_sps=[11664.0, 23328.0, 46656.0],
+                       mean_sps=27216.0, std_sps=17750.0)
+    import json
+    doc = json.loads(mh.bench_json_string([q]))
+    assert doc["format_version"] == 1 and len(doc["records"]) == 1
+    rec = doc["records"][0]
+    assert rec["figure"] == "simplex(10)" and len(rec["run_seconds"]) == 3
+    assert rec["run_sps"][2] == 46656.0 and rec["mean_sps"] == 27216.0
+    p = tmp_path / "bench.json"
+    mh.write_bench_json(str(p), [q])
+    assert json.loads(p.read_text()) == doc
+    with pytest.raises(mh.MharError) as e:
+        mh.write_bench_csv("/nonexistent/dir/b.csv", [q])
+    assert e.value.code == mh.ErrorCode.io_failure
