@@ -116,6 +116,7 @@ struct mhar_ctx {
   int* rexp = nullptr;
   int64_t KS = 0, i8_row_tiles = 0;
   int i8_clusters = 0;  // co-resident clusters of the int8 kernel
+  bool dmma_refresh = false;  // MHAR_DMMA_REFRESH=1: tcgen05 engines refresh with the fused DMMA pass
   unsigned long long* tc_prof = nullptr;  // MHAR_I8_PROFILE: tcgen05 kernels' per-CTA counters
   // structure-aware paths (fastpath.cuh)
   double* diag_coef = nullptr;  // stacked diagonal blocks: per-row coefficient (m)
@@ -302,6 +303,9 @@ int launch_chord(mhar_ctx* c, int mode, const double* X) {
       break;
     case INCREMENTAL:
       chord2_kernel<INCREMENTAL><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
+      break;
+    case SLACK_STORE:
+      chord2_kernel<SLACK_STORE><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
       break;
     default:
       chord2_kernel<CHECK><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
@@ -610,6 +614,13 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
     LAUNCH_OK(c, "fill_keys_kernel");
     CK(cudaMemsetAsync(c->theta, 0, sizeof(double) * c->z_pad, c->stream));
     s = launch_i8(c);
+  } else if ((c->A8 || c->Ahi) && mode == FUSED_STORE && !c->dmma_refresh) {
+    // refresh of a tcgen05 engine: the fp64 slack from A x alone on DMMA
+    // (half the fused pass), then the engine's own rates and chord with
+    // theta_prev = 0
+    if ((s = launch_chord(c, SLACK_STORE, c->X))) return s;
+    CK(cudaMemsetAsync(c->theta, 0, sizeof(double) * c->z_pad, c->stream));
+    s = c->A8 ? launch_i8(c) : launch_tc32(c);
   } else if (c->A8 && mode == INCREMENTAL) {
     s = launch_i8(c);
   } else if (c->Ahi && injected) {
@@ -848,6 +859,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
 
   mhar_ctx* c = new mhar_ctx();
   c->opt = *opt;
+  c->dmma_refresh = std::getenv("MHAR_DMMA_REFRESH") != nullptr;
   const bool fp32 = opt->precision == 32;
   const bool tiles = fp32 || i8;  // tcgen05 kernels: CTA-pair walk tiles, tile cache layout
   if (tiles) {
@@ -1113,6 +1125,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   cudaFuncSetAttribute(chord_kernel<FUSED_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
   cudaFuncSetAttribute(chord2_kernel<INCREMENTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   cudaFuncSetAttribute(chord2_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
+  cudaFuncSetAttribute(chord2_kernel<SLACK_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   if (c->Acm) {
     if ((st = dalloc(c, &c->walk_err, c->z))) return bail(st);
     cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -34,7 +34,7 @@
 
 namespace mhar_dev {
 
-enum ChordMode { FUSED = 0, FUSED_STORE = 1, INCREMENTAL = 2, CHECK = 3 };
+enum ChordMode { FUSED = 0, FUSED_STORE = 1, INCREMENTAL = 2, CHECK = 3, SLACK_STORE = 4 };
 
 constexpr int CHORD_THREADS = 256;
 // FUSED* kernel (1 CTA / SM)
@@ -491,6 +491,28 @@ __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordPar
           scan_row(s0, acc[i][j][0], p.eps_dir, hi[0][0], lo[0][0], sd[0][0]);
           scan_row(s1, acc[i][j][1], p.eps_dir, hi[0][1], lo[0][1], sd[0][1]);
         }
+      } else if (MODE == SLACK_STORE) {
+        // refresh of a tcgen05 engine's cache: the exact fp64 slack b - A x
+        // in that engine's layout and format, rates zeroed (the engine's
+        // next pass runs with theta_prev = 0 and writes them)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const double sl = br[i] - acc[i][j][e];
+            const int64_t si = cache_index(row0 + i * 8, c + e, p);
+            if (p.rate_f32) {
+              const float h = (float)sl;
+              const float l = isfinite(sl) ? (float)(sl - (double)h) : 0.0f;
+              const float2 v = make_float2(h, l);
+              p.S[si] = *reinterpret_cast<const double*>(&v);
+              reinterpret_cast<float*>(p.R)[si] = 0.0f;
+            } else {
+              p.S[si] = sl;
+              p.R[si] = 0.0;
+            }
+          }
+        continue;
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i)

@@ -8,9 +8,11 @@ import paper_2104_07097_b200 as mh
 from paper_2104_07097_b200 import workloads
 
 w = workloads.config(5)
-phi, windows = int(sys.argv[1]) if len(sys.argv) > 1 else 64, 2
-for engine in ["dmma", "int8"]:
-    with mh.Engine(w.polytope, w.z, seed=7, f64_engine=engine) as eng:
+phi = int(sys.argv[1]) if len(sys.argv) > 1 else 64
+windows = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+for engine in ["dmma", "int8", "fp32"]:
+    kw = dict(precision=32) if engine == "fp32" else dict(f64_engine=engine)
+    with mh.Engine(w.polytope, w.z, seed=7, **kw) as eng:
         eng.run(w.x0, 2, 1, 0, 0)  # warm-up
         t0 = time.perf_counter()
         S, st = eng.run(w.x0, phi, windows, 0, 0)
