@@ -31,7 +31,7 @@ def max_over_ranks(value: float, device=None) -> float:
     """Max of a per-rank scalar (device time of a timed region)."""
     import torch
     import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_initialized():
         return float(value)
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -63,7 +63,7 @@ def reduce_diagnostics(redraws: int, max_violation: float, max_eq: float, rows, 
                                    device=rows_t.device)])
     mx = torch.tensor([float(max_violation), float(max_eq)], dtype=torch.float64,
                       device=rows_t.device)
-    if dist.is_initialized() and dist.get_world_size() > 1:
+    if dist.is_initialized():
         dist.all_reduce(sums, op=dist.ReduceOp.SUM)
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     s = sums.cpu().numpy()
@@ -79,7 +79,7 @@ def gather_rows(local_rows, z_counts, dst: int = 0):
     largest.  Returns the (sum z) x n tensor on dst, None elsewhere."""
     import torch
     import torch.distributed as dist
-    if not dist.is_initialized() or dist.get_world_size() == 1:
+    if not dist.is_initialized():
         return local_rows
     zmax = max(z_counts)
     n = local_rows.shape[1]
