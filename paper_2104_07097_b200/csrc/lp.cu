@@ -607,13 +607,15 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
     pivot_launch(d.zero);
     ++npiv;
   };
+  const bool lp_trace = std::getenv("MHAR_LP_TRACE") != nullptr;  // one pivot per batch, logged
   // one phase, driven on the device: 0 optimal, 7 unbounded ray, 10 budget, 100 CUDA
   auto run_phase = [&](int limit_col) -> int {
     Ctl h{};
     h.budget = budget - npiv;
     h.stall_limit = rows + total;
     cudaMemcpyAsync(d.ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, d.s);
-    int batch = 8;
+    const char* bat_env = std::getenv("MHAR_LP_BATCH");
+    int batch = bat_env ? std::max(1, std::atoi(bat_env)) : lp_trace ? 1 : 8;
     for (;;) {
       for (int k = 0; k < batch; ++k) {
         select_kernel<<<1, kThreads, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, limit_col,
@@ -622,11 +624,17 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
       }
       cudaMemcpyAsync(&h, d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, d.s);
       if (cudaStreamSynchronize(d.s) != cudaSuccess) return 100;
+      if (lp_trace) {
+        int hs[2];
+        cudaMemcpy(hs, d.sel, sizeof(hs), cudaMemcpyDeviceToHost);
+        std::fprintf(stderr, "[lp trace] limit %d npiv %lld sel %d %d done %d st %d bland %d\n",
+                     limit_col, h.npiv, hs[0], hs[1], h.done, h.status, h.bland);
+      }
       if (h.done) {
         npiv += h.npiv;
         return h.status;
       }
-      batch = std::min(batch * 2, 256);
+      if (!lp_trace && !bat_env) batch = std::min(batch * 2, 256);
     }
   };
   auto fetch_row = [&](int i, double* dst) {
