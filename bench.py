@@ -201,6 +201,18 @@ def max_over_ranks(v: float, world: int) -> float:
     return float(t.item())
 
 
+def cpu_model() -> str:
+    """Host CPU model name (state the CPU beside the core count)."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_sample(w, z_sample: int, iters: int, threads: int):
     """The oracle (CPU restatement of the reference step) on a bounded
     sample of the same workload: z_sample walks x iters iterates."""
@@ -252,6 +264,7 @@ def run_reference(args, world, rank):
         "config": {"workload": w.name, "n": w.polytope.dim(), "m_I": w.polytope.num_inequalities(),
                    "m_E": w.polytope.num_equalities(), "walks_per_step": args.cpu_walks},
         "cpu_baseline": {"value": value, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+                         "cpu_model": cpu_model(),
                          "sample": f"{args.cpu_walks} walks x 1 iterate per step of the config-"
                                    f"{args.config} polytope (oracle/mhar_oracle.c, OpenMP GEMM)"},
         "e2e": {"value": value, "unit": "chain-steps/s", "h2d_bytes_per_step": 0,
@@ -480,6 +493,7 @@ def run_engine(args, world, rank, local):
         threads = os.cpu_count() or 1
         v, dt = cpu_sample(w, args.cpu_walks, args.cpu_iters, threads)
         cpu = {"value": v, "unit": "chain-steps/s", "cores": threads, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"{args.cpu_walks} walks x {args.cpu_iters} iterates of the same polytope "
                          f"({dt:.1f} s; oracle/mhar_oracle.c restating proj/src/sampler.cpp, "
                          f"OpenMP AVX-512 GEMM)"}
