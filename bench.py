@@ -106,6 +106,40 @@ def tf32_dense_peak():
         return 1590.0 / 2.0
 
 
+def f16_dense_peak():
+    """FP16 (f32 accumulate) tensor-core peak: the tcgen05 kind::f16
+    microbench (CTA pair, N = 256); fallback the driver-measured bf16 GEMM."""
+    v = _probe_peak("f16_tflops")
+    if v:
+        return v
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["bf16_tflops"]
+    except (OSError, KeyError, ValueError):
+        return 1590.0
+
+
+def tc_form():
+    """Form of the fp32 variant's kernel: "f16" (default) or "tf32" (MHAR_TC_F16=0)."""
+    return "tf32" if os.environ.get("MHAR_TC_F16", "1") == "0" else "f16"
+
+
+def tc_roofline_terms():
+    """(peak, unit, kernel, dtype, peak source) of the fp32 variant's form."""
+    if tc_form() == "f16":
+        return (f16_dense_peak(), "TFLOP/s (F16 executed)",
+                "chord_tc32_kernel<F16> (tcgen05.mma kind::f16, TMEM, bulk-copy ring)",
+                "A_I as two fp16 halves per row scale (22 bits of the row maximum), the "
+                "direction as one fp16 per walk scale; products exact, f32 accumulate; "
+                "slack and walks f64",
+                "tcgen05 kind::f16 microbench, profiles/tensor_probe_r01.jsonl")
+    return (tf32_dense_peak(), "TFLOP/s (TF32 executed)",
+            "chord_tc32_kernel (tcgen05.mma kind::tf32, TMEM, bulk-copy ring)",
+            "A_I rounded to f32; rates f32-accurate on tcgen05 (TF32 hi/lo split); "
+            "slack and walks f64",
+            "tcgen05 kind::tf32 microbench, profiles/tensor_probe_r01.jsonl")
+
+
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled during the timed region."""
 
@@ -472,18 +506,16 @@ def run_engine(args, world, rank, local):
         s32 = e32.stats()
         bad32, viol32, _ = e32.check_state(e32.eps_feas)
         e32.close()
-        tf32_exec = 2.0 * s32["chord_flops"] / max(s32["chord_ms"] * 1e-3, 1e-30) / 1e12
-        tf32_peak = tf32_dense_peak()
+        tc_exec = 2.0 * s32["chord_flops"] / max(s32["chord_ms"] * 1e-3, 1e-30) / 1e12
+        tc_peak, tc_unit, tc_kernel, tc_dtype, tc_src = tc_roofline_terms()
         fp32 = {"value": total_walks * args.steps / (ms32 * 1e-3), "unit": "chain-steps/s",
-                "ms_per_step": ms32 / args.steps,
-                "dtype": "A_I rounded to f32; rates f32-accurate on tcgen05 (TF32 hi/lo split); "
-                         "slack and walks f64",
-                "kernel": "chord_tc32_kernel (tcgen05.mma kind::tf32, TMEM, bulk-copy ring)",
-                "roofline": {"bound": "tensor", "achieved": tf32_exec, "peak": tf32_peak,
-                             "unit": "TFLOP/s (TF32 executed)", "frac": tf32_exec / tf32_peak,
+                "ms_per_step": ms32 / args.steps, "form": tc_form(), "dtype": tc_dtype,
+                "kernel": tc_kernel,
+                "roofline": {"bound": "tensor", "achieved": tc_exec, "peak": tc_peak,
+                             "unit": tc_unit, "frac": tc_exec / tc_peak,
                              "traffic": ncu_traffic("tc32_full") if captured else None,
                              "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
-                             "peak_source": "tcgen05 kind::tf32 microbench, profiles/tensor_probe_r01.jsonl"},
+                             "peak_source": tc_src},
                 "all_inside_eps_feas": bool(bad32 == -1)}
 
     if rank != 0:
@@ -549,13 +581,12 @@ def run_engine(args, world, rank, local):
     if i8:
         line["fp64_int8_variant"] = i8
     if args.precision == 32:
-        line["dtype"] = "f32 rates (tcgen05 TF32 split), f64 slack/state"
-        line["roofline"].update({"achieved": 2.0 * achieved, "peak": tf32_dense_peak(),
-                                 "unit": "TFLOP/s (TF32 executed)",
-                                 "frac": 2.0 * achieved / tf32_dense_peak(),
-                                 "kernel": "chord_tc32_kernel",
+        tc_peak, tc_unit, tc_kernel, tc_dtype, tc_src = tc_roofline_terms()
+        line["dtype"] = "f32 rates (" + tc_dtype + ")"
+        line["roofline"].update({"achieved": 2.0 * achieved, "peak": tc_peak, "unit": tc_unit,
+                                 "frac": 2.0 * achieved / tc_peak, "kernel": tc_kernel,
                                  "traffic": ncu_traffic("tc32_full") if captured else None,
-                                 "peak_source": "tcgen05 kind::tf32 microbench"})
+                                 "peak_source": tc_src})
     print(json.dumps(line), flush=True)
 
 

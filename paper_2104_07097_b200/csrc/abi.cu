@@ -109,6 +109,9 @@ struct mhar_ctx {
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
   int tc_group_n = 1;   // tc32 rasterisation band (row tiles); MHAR_TC_GROUP overrides
   int tc_a_policy = 0;  // L2 policy of the tc32 A stream (evict_normal); MHAR_TC_APOL overrides
+  bool tc_f16 = true;   // fp32 variant on kind::f16 with per-row / per-walk scales (MHAR_TC_F16=0: TF32)
+  int64_t tc_kt = 0;    // k stages of the fp32 variant (16 floats or 32 halves each)
+  float *tc_rsc = nullptr, *tc_csc = nullptr;
   int64_t cache_rows = 0;  // row tile of the tcgen05 cache layout (256 tc32, 64 int8)
   // int8-slice fp64 engine (chord_i8.cuh)
   uint8_t *A8 = nullptr, *D8 = nullptr;
@@ -340,7 +343,9 @@ int launch_tc32(mhar_ctx* c) {
   p.err = c->err;
   p.row_tiles = c->tc_row_tiles;
   p.walk_tiles = c->tc_walk_tiles;
-  p.KT = c->KT;
+  p.KT = c->tc_kt;
+  p.rsc = c->tc_rsc;
+  p.csc = c->tc_csc;
   p.m = c->m;
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
@@ -356,7 +361,11 @@ int launch_tc32(mhar_ctx* c) {
     ev = take_events(c);
     cudaEventRecord(ev.first, c->stream);
   }
-  if (c->Dlo)
+  if (c->tc_f16 && c->Dlo)
+    chord_tc32_kernel<true, true><<<grid, TC_THREADS, TcCfg<true>::smem, c->stream>>>(p);
+  else if (c->tc_f16)
+    chord_tc32_kernel<false, true><<<grid, TC_THREADS, TcCfg<false>::smem, c->stream>>>(p);
+  else if (c->Dlo)
     chord_tc32_kernel<true><<<grid, TC_THREADS, TcCfg<true>::smem, c->stream>>>(p);
   else
     chord_tc32_kernel<false><<<grid, TC_THREADS, TcCfg<false>::smem, c->stream>>>(p);
@@ -596,9 +605,16 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
   if (c->Ahi) {
     // fp32 variant: the tensor cores see D_hi + D_lo; D becomes that direction
     const int64_t total = c->z_pad * c->KT * BK;
-    tc_split_d_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        c->D, c->n, c->z_pad, c->KT, c->Dhi, c->Dlo, c->err);
-    LAUNCH_OK(c, "tc_split_d_kernel");
+    if (c->tc_f16) {
+      tc16_split_d_kernel<<<(unsigned)((c->z_pad * 32 + 255) / 256), 256, 0, c->stream>>>(
+          c->D, c->n, c->z_pad, c->KT, c->tc_kt, reinterpret_cast<__half*>(c->Dhi),
+          reinterpret_cast<__half*>(c->Dlo), c->tc_csc, c->err);
+      LAUNCH_OK(c, "tc16_split_d_kernel");
+    } else {
+      tc_split_d_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+          c->D, c->n, c->z_pad, c->KT, c->Dhi, c->Dlo, c->err);
+      LAUNCH_OK(c, "tc_split_d_kernel");
+    }
   }
   if (c->A8) {
     // int8-slice engine: per-walk fixed point, slices; D becomes the quantised direction
@@ -957,6 +973,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   if (const char* g = std::getenv("MHAR_WALK_BAND")) c->walk_band = std::max(0, std::atoi(g));
   if (const char* g = std::getenv("MHAR_TC_GROUP")) c->tc_group_n = std::max(1, std::atoi(g));
   if (const char* g = std::getenv("MHAR_TC_APOL")) c->tc_a_policy = std::atoi(g) % 3;
+  if (const char* g = std::getenv("MHAR_TC_F16")) c->tc_f16 = std::atoi(g) != 0;
   if ((st = dalloc(c, &c->redraw_scratch, (size_t)c->redraw_grid * 3 * c->n))) return bail(st);
   if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
     const size_t cache = (size_t)c->m_pad * c->z_pad;
@@ -993,8 +1010,20 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         cudaFree(tmp);
         return bail(st);
       }
-      tc_split_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
-          tmp, c->m, c->n, c->m_pad, c->KT, c->Ahi, c->Alo, c->A, c->KT);
+      if (c->tc_f16) {
+        c->tc_kt = (c->n + TC_BK16 - 1) / TC_BK16;
+        if ((st = dalloc(c, &c->tc_rsc, c->m_pad)) || (st = dalloc(c, &c->tc_csc, c->z_pad))) {
+          cudaFree(tmp);
+          return bail(st);
+        }
+        tc16_split_a_kernel<<<blocks_for(c->m_pad, 128, c->num_sms * 8), 128, 0, c->stream>>>(
+            tmp, c->m, c->n, c->m_pad, c->tc_kt, reinterpret_cast<__half*>(c->Ahi),
+            reinterpret_cast<__half*>(c->Alo), c->tc_rsc, c->A, c->KT);
+      } else {
+        c->tc_kt = c->KT;
+        tc_split_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
+            tmp, c->m, c->n, c->m_pad, c->KT, c->Ahi, c->Alo, c->A, c->KT);
+      }
       ++c->launches;
       cudaMemsetAsync(c->Dhi, 0, dn * sizeof(float), c->stream);
       cudaStreamSynchronize(c->stream);
@@ -1002,6 +1031,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
                            (int)TcCfg<false>::smem);
       cudaFuncSetAttribute(chord_tc32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TcCfg<true>::smem);
+      cudaFuncSetAttribute(chord_tc32_kernel<false, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<false>::smem);
+      cudaFuncSetAttribute(chord_tc32_kernel<true, true>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TcCfg<true>::smem);
       if (std::getenv("MHAR_I8_PROFILE") && (st = dalloc(c, &c->tc_prof, kProfWords * (size_t)c->num_sms))) {
         cudaFree(tmp);
         return bail(st);

@@ -31,6 +31,8 @@
 // MMAs of the next.
 #pragma once
 
+#include <cuda_fp16.h>
+
 #include "chord_kernel.cuh"
 #include "common.cuh"
 
@@ -106,6 +108,33 @@ __device__ inline void tc_mma2(uint32_t tmem, uint64_t da, uint64_t db, uint32_t
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
       "l"(da), "l"(db), "r"(TC_IDESC), "r"(accumulate));
+}
+// The fp16 form (MHAR_TC_F16=1): the same 32-byte K chunks hold 16 halves, so
+// one MMA covers K = 16 at twice the TF32 rate.  Operands are scaled per row
+// (A) and per walk (D) by powers of two so their maxima sit in [2^14, 2^15);
+// a = (a_hi + a_lo) 2^-s_r exactly, d = d_h 2^-t_c is the direction moved
+// along (centrally symmetric rounding), products are exact in fp32.
+constexpr uint32_t TC_IDESC_F16 = (1u << 4) | (0u << 7) | (0u << 10) |
+                                  ((uint32_t)(TC_N >> 3) << 17) |
+                                  ((uint32_t)((2 * TC_M) >> 4) << 24);
+__device__ inline void tc_mma2_f16(uint32_t tmem, uint64_t da, uint64_t db, uint32_t accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(TC_IDESC_F16), "r"(accumulate));
+}
+// half layouts: the float layouts' bytes with 8 halves per 16-byte chunk
+constexpr int TC_BK16 = 2 * TC_BK;  // halves per stage row
+__host__ __device__ inline int64_t tc_piece_index16(int64_t r, int64_t kk, int64_t R) {
+  return ((kk >> 3) * (R >> 3) + (r >> 3)) * 64 + (r & 7) * 8 + (kk & 7);
+}
+__host__ __device__ inline int64_t tc_d_index16(int64_t c, int64_t k, int64_t KT) {
+  return ((c / TC_M) * KT + k / TC_BK16) * (TC_M * TC_BK16) +
+         tc_piece_index16(c % TC_M, k % TC_BK16, TC_M);
+}
+__host__ __device__ inline int64_t tc_a_index16(int64_t r, int64_t k, int64_t KT) {
+  return (((r / TC_N) * KT + k / TC_BK16) * 2 + (r % TC_N) / TC_NH) * (TC_NH * TC_BK16) +
+         tc_piece_index16(r % TC_NH, k % TC_BK16, TC_NH);
 }
 // arrive on the barrier at the same smem offset in both CTAs of the pair
 // once every previously issued MMA of this thread has completed
@@ -208,6 +237,8 @@ struct TcParams {
   int group_n;         // rasterisation band (row tiles)
   int a_policy;        // L2 policy of the A_hi/A_lo stream: 0 normal, 1 evict_last, 2 evict_first
   unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
+  const float* rsc;  // fp16 form: per-row 2^s (rate = acc * rsc[r] * csc[c]), else null
+  const float* csc;  // fp16 form: per-walk 2^t
 };
 
 // unit u -> (row tile, walk-tile pair), banded over group_n row tiles
@@ -222,7 +253,7 @@ __device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_
   *wp = in_band / h;
 }
 
-template <bool SPLIT_D>
+template <bool SPLIT_D, bool F16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     chord_tc32_kernel(const TcParams p) {
   constexpr int kStages = TcCfg<SPLIT_D>::stages;
@@ -345,11 +376,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             const uint64_t dd = umma_desc(sd + dofs, TC_M * 16, 128);
             const uint64_t ah = umma_desc(sa_hi + aofs, TC_NH * 16, 128);
             const uint64_t al = umma_desc(sa_lo + aofs, TC_NH * 16, 128);
-            tc_mma2(acc, dd, ah, (kt | k) ? 1u : 0u);
-            tc_mma2(acc, dd, al, 1u);
+            if (F16) {
+              tc_mma2_f16(acc, dd, ah, (kt | k) ? 1u : 0u);
+              tc_mma2_f16(acc, dd, al, 1u);
+            } else {
+              tc_mma2(acc, dd, ah, (kt | k) ? 1u : 0u);
+              tc_mma2(acc, dd, al, 1u);
+            }
             if (SPLIT_D) {
               const uint64_t dl = umma_desc(sa_lo + TC_A_PIECE + dofs, TC_M * 16, 128);
-              tc_mma2(acc, dl, ah, 1u);
+              if (F16)
+                tc_mma2_f16(acc, dl, ah, 1u);
+              else
+                tc_mma2(acc, dl, ah, 1u);
             }
           }
           tc_commit2(&empty[stage]);  // frees the slot in both CTAs when these MMAs finish
@@ -447,9 +486,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           lo = dn ? fmaxf(lo, qt) : lo;
         }
       };
+      const float cs = F16 ? p.csc[c] : 1.0f;
       for (int c0 = rh * (TC_N / 2); c0 < (rh + 1) * (TC_N / 2); c0 += 32) {
         float v[32];
         tc_ld32(taddr + (uint32_t)c0, v);
+        if (F16) {
+          // accumulator -> rate: the row and walk scales (powers of two)
+          const float rs = __ldg(p.rsc + rt * TC_N + c0 + lane);  // lane j: row c0 + j
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] *= __shfl_sync(0xFFFFFFFFu, rs, j) * cs;
+        }
 #pragma unroll
         for (int g = 0; g < 32; g += TC_GROUP) rows8(c0 + g, v + g);
       }
@@ -535,6 +581,77 @@ __global__ void tc_split_d_kernel(double* __restrict__ D, int64_t n, int64_t z_p
       Dlo[tc_d_index(c, k, KT)] = tf32_trunc((float)(d - (double)h));
     else
       D[i] = (double)h;
+  }
+}
+
+// ---- fp16 form: per-row / per-walk power-of-two scales and half splits ----
+
+// scale exponent: max|x| < 2^e  ->  x 2^(14 - e) in (-2^14, 2^14); clamped so
+// the inverse scale stays a normal float
+__device__ inline int tc16_exp(double mx) {
+  int e = mx > 0.0 ? ilogb(mx) + 1 : 0;
+  return e < -100 ? -100 : (e > 100 ? 100 : e);
+}
+// half of v with values below the fp16 normal range flushed (the tensor
+// cores then see exactly what the fp64 copies say they see)
+__device__ inline __half tc16_half(double v) {
+  const __half h = __double2half(v);
+  return fabs((double)__half2float(h)) < 6.103515625e-05 ? __float2half(0.0f) : h;
+}
+
+// per-row exponents of A_I (column-major m x n), the split, and A_used back
+// into the packed fp64 copy: one thread per row
+__global__ void tc16_split_a_kernel(const double* __restrict__ Acm, int64_t m, int64_t n,
+                                    int64_t m_pad, int64_t KT16, __half* __restrict__ Ahi,
+                                    __half* __restrict__ Alo, float* __restrict__ rsc,
+                                    double* __restrict__ Apk, int64_t KT64) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < m_pad;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double mx = 0.0;
+    if (r < m)
+      for (int64_t k = 0; k < n; ++k) mx = fmax(mx, fabs(Acm[r + k * m]));
+    const int e = tc16_exp(mx);
+    const double s = ldexp(1.0, 14 - e);
+    rsc[r] = ldexpf(1.0f, e - 14);
+    for (int64_t k = 0; k < KT16 * TC_BK16; ++k) {
+      const double a = (r < m && k < n) ? Acm[r + k * m] * s : 0.0;
+      const __half h = tc16_half(a);
+      const __half l = tc16_half(a - (double)__half2float(h));
+      const int64_t ti = tc_a_index16(r, k, KT16);
+      Ahi[ti] = h;
+      Alo[ti] = l;
+      if (r < m && k < n)
+        Apk[a_index(r, k, KT64)] =
+            ((double)__half2float(h) + (double)__half2float(l)) * ldexp(1.0, e - 14);
+    }
+  }
+}
+
+// per-walk exponent and the half direction; D becomes the direction moved
+// along (or keeps fp64 and gets a low half: bodies with equalities).  One
+// warp per walk.
+__global__ void tc16_split_d_kernel(double* __restrict__ D, int64_t n, int64_t z_pad, int64_t KT,
+                                    int64_t KT16, __half* __restrict__ Dhi,
+                                    __half* __restrict__ Dlo, float* __restrict__ csc,
+                                    const unsigned long long* err) {
+  if (*err != kNoError) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= z_pad) return;
+  double mx = 0.0;
+  for (int64_t k = lane; k < n; k += 32) mx = fmax(mx, fabs(D[b_index(c, k, KT)]));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+  const int e = tc16_exp(mx);
+  const double t = ldexp(1.0, 14 - e), ti = ldexp(1.0, e - 14);
+  if (lane == 0) csc[c] = ldexpf(1.0f, e - 14);
+  for (int64_t k = lane; k < KT16 * TC_BK16; k += 32) {
+    const double d = k < n ? D[b_index(c, k, KT)] * t : 0.0;
+    const __half h = tc16_half(d);
+    Dhi[tc_d_index16(c, k, KT16)] = h;
+    if (Dlo)
+      Dlo[tc_d_index16(c, k, KT16)] = tc16_half(d - (double)__half2float(h));
+    else if (k < n)
+      D[b_index(c, k, KT)] = (double)__half2float(h) * ti;
   }
 }
 

@@ -33,6 +33,7 @@ def test_roofline_peaks_and_traffic_are_committed():
     assert 30.0 < bench.fp64_peak() < 45.0          # DMMA TFLOP/s
     assert 3000.0 < bench.int8_dense_peak() < 5000.0  # int8 TOPS
     assert 800.0 < bench.tf32_dense_peak() < 1300.0   # TF32 TFLOP/s
+    assert 1600.0 < bench.f16_dense_peak() < 2600.0   # FP16 TFLOP/s
     for cap in ("chord2_full", "tc32_full", "i8_full"):
         t = bench.ncu_traffic(cap)
         assert t is not None and t > 1.0

@@ -19,12 +19,43 @@ def _tf32(x):
     return u.view(np.float32)
 
 
-def split_used(a):
-    """The value the tensor cores see for a: fp32(a) = hi + tf32(fp32(a) - hi)."""
+@pytest.fixture(autouse=True, params=["f16", "tf32"])
+def form(request, monkeypatch):
+    """Both forms of the variant: kind::f16 with per-row / per-walk scales
+    (default) and kind::tf32 (MHAR_TC_F16=0)."""
+    monkeypatch.setenv("MHAR_TC_F16", "1" if request.param == "f16" else "0")
+    return request.param
+
+
+def _f16_split(x, axis):
+    """x scaled by 2^(14 - e) (max |x| < 2^e along `axis`), split into two
+    halves below the fp16 normal range flushed: (hi, hi + lo), unscaled."""
+    mx = np.abs(x).max(axis=axis, keepdims=True)
+    e = np.where(mx > 0, np.floor(np.log2(np.where(mx > 0, mx, 1.0))) + 1, 0)
+    s = 2.0 ** (14 - e)
+    h = (x * s).astype(np.float16).astype(np.float64)
+    h[np.abs(h) < 2.0 ** -14] = 0.0
+    lo = (x * s - h).astype(np.float16).astype(np.float64)
+    lo[np.abs(lo) < 2.0 ** -14] = 0.0
+    return h / s, (h + lo) / s
+
+
+def split_used(a, form="tf32"):
+    """The A_I the tensor cores see: tf32 hi + tf32 lo of fp32(a), or the
+    per-row-scaled half pair."""
+    if form == "f16":
+        return _f16_split(np.asarray(a, dtype=np.float64), 1)[1]
     a32 = np.asarray(a, dtype=np.float32)
     hi = _tf32(a32)
     lo = _tf32((a32 - hi).astype(np.float32))
     return hi.astype(np.float64) + lo.astype(np.float64)
+
+
+def dir_used(H, form="tf32"):
+    """The direction moved along: TF32-rounded, or the per-walk-scaled half."""
+    if form == "f16":
+        return _f16_split(np.asarray(H, dtype=np.float64), 0)[0]
+    return _tf32(H).astype(np.float64)
 
 
 def _interior(p, z, rng, shrink=0.4):
@@ -34,7 +65,7 @@ def _interior(p, z, rng, shrink=0.4):
 
 
 @pytest.mark.parametrize("n,m,z", [(16, 300, 128), (37, 1000, 200), (500, 20000, 256)])
-def test_fp32_injected_step_parity(orc, n, m, z):
+def test_fp32_injected_step_parity(orc, form, n, m, z):
     p = workloads.random_polytope(n, m, seed=n)
     rng = np.random.default_rng(m)
     X = _interior(p, z, rng)
@@ -44,8 +75,8 @@ def test_fp32_injected_step_parity(orc, n, m, z):
         eng.set_state(X)
         lo, hi, th, fl = eng.step_injected(H, U)
         Xg = eng.get_state()
-    A_used = np.asfortranarray(split_used(p.a_in))
-    D_used = np.asfortranarray(_tf32(H).astype(np.float64))  # TF32-exact directions
+    A_used = np.asfortranarray(split_used(p.a_in, form))
+    D_used = np.asfortranarray(dir_used(H, form))  # the direction moved along
     st, Xr, lor, hir, thr, flr, _ = orc.step_injected(A_used, p.b_in, None, 1e-11, X, D_used, U)
     assert st == 0
     assert np.array_equal(fl & mh.FLAG_DEGENERATE, flr & mh.FLAG_DEGENERATE)
@@ -57,7 +88,7 @@ def test_fp32_injected_step_parity(orc, n, m, z):
     assert np.abs(Xg - Xr).max() <= RTOL32 * np.abs(Xr).max()
 
 
-def test_fp32_walks_stay_exactly_feasible():
+def test_fp32_walks_stay_exactly_feasible(form):
     p = workloads.random_polytope(64, 4000, seed=3)
     with mh.Engine(p, 256, seed=4, precision=32, refresh_every=64) as eng:
         eng.set_state(np.zeros((64, 256)))
@@ -66,7 +97,7 @@ def test_fp32_walks_stay_exactly_feasible():
             bad, viol, _ = eng.check_state(1e-9)   # fresh fp64 product on A_used
             assert bad == -1 and viol.max() <= 0.0
         X = eng.get_state()
-    A_used = split_used(p.a_in)
+    A_used = split_used(p.a_in, form)
     assert (A_used @ X - p.b_in[:, None]).max() <= 1e-9
     assert np.abs(X).max() > 0.1
 

@@ -29,7 +29,8 @@ __device__ inline uint32_t ctarank() {
 
 constexpr int KB = 32;  // bytes of K per MMA
 
-// MODE 0: cg1 SS, 1: cg1 TS (A in TMEM), 2: cg2 SS, 3: cg2 SS kind::tf32 (K = 8 per MMA)
+// MODE 0: cg1 SS, 1: cg1 TS (A in TMEM), 2: cg2 SS, 3: cg2 SS kind::tf32 (K = 8 per MMA),
+// 4: cg2 SS kind::f16 (K = 16 per MMA, f32 accumulate)
 template <int MODE, int N>
 __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, unsigned long long* sink) {
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
   const uint32_t M = (MODE >= 2) ? 256 : 128;
   const uint32_t idesc = MODE == 3
       ? (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((M >> 4) << 24)
+      : MODE == 4 ? (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((M >> 4) << 24)
       : (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((M >> 4) << 24);
   const int nb = (MODE >= 2) ? N / 2 : N;  // B rows staged per CTA
   if (tid == 0 && rank == 0) {
@@ -80,8 +82,11 @@ __global__ void __launch_bounds__(128, 1) probe(int iters, int mmas_per_iter, un
         } else if (MODE == 2) {
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n"
                        ::"r"(acc), "l"(da), "l"(db), "r"(idesc), "r"(1u));
-        } else {
+        } else if (MODE == 3) {
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                       ::"r"(acc), "l"(da), "l"(db), "r"(idesc), "r"(1u));
+        } else {
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n"
                        ::"r"(acc), "l"(da), "l"(db), "r"(idesc), "r"(1u));
         }
       }
@@ -135,10 +140,14 @@ void run(unsigned long long* sink, int sms) {
   float ms;
   cudaEventElapsedTime(&ms, t0, t1);
   cudaError_t e = cudaGetLastError();
-  const double ops_per_sm = 2.0 * 128 * N * (MODE == 3 ? KB / 4 : KB) * (double)iters * per;  // M per SM is 128
+  const double ops_per_sm =
+      2.0 * 128 * N * (MODE == 3 ? KB / 4 : MODE == 4 ? KB / 2 : KB) * (double)iters * per;  // M per SM is 128
   const double tops = ops_per_sm * sms / (ms * 1e-3) / 1e12;
   if (MODE == 3)
     printf("{\"mode\": \"cg2_SS_tf32\", \"N\": %d, \"status\": \"%s\", \"ms\": %.3f, \"tf32_tflops\": %.1f}\n",
+           N, cudaGetErrorString(e), ms, tops);
+  else if (MODE == 4)
+    printf("{\"mode\": \"cg2_SS_f16\", \"N\": %d, \"status\": \"%s\", \"ms\": %.3f, \"f16_tflops\": %.1f}\n",
            N, cudaGetErrorString(e), ms, tops);
   else
     printf("{\"mode\": \"%s\", \"N\": %d, \"status\": \"%s\", \"ms\": %.3f, \"int8_tops\": %.1f}\n",
@@ -256,6 +265,8 @@ int main() {
   run<2, 256>(sink, sms);
   run<3, 128>(sink, sms);
   run<3, 256>(sink, sms);
+  run<4, 128>(sink, sms);
+  run<4, 256>(sink, sms);
   run_seq<0>(sink, sms);
   run_seq<1>(sink, sms);
   run_seq<2>(sink, sms);
