@@ -1,5 +1,8 @@
 // chord_tc32.cuh -- fp32 variant of the incremental chord kernel on the
-// Blackwell 5th-gen tensor cores (tcgen05.mma kind::tf32, TMEM accumulators).
+// Blackwell 5th-gen tensor cores (tcgen05.mma, TMEM accumulators).  Two forms
+// share the kernel: kind::f16 with per-row / per-walk power-of-two scales
+// (default; template F16, see tc_mma2_f16) and kind::tf32 (MHAR_TC_F16=0),
+// described below.
 //
 // Same computation as chord2_kernel<INCREMENTAL> (compute_lambda_intervals,
 // /root/reference/proj/src/sampler.cpp:150-208, with the slack carried
