@@ -120,6 +120,15 @@ struct mhar_ctx {
   int64_t KS = 0, i8_row_tiles = 0;
   int i8_clusters = 0;  // co-resident clusters of the int8 kernel
   bool dmma_refresh = false;  // MHAR_DMMA_REFRESH=1: tcgen05 engines refresh with the fused DMMA pass
+  // CUDA graph of one steady iterate (multi-kernel path, MHAR_NO_GRAPHS=1 disables):
+  // the kernels read the Philox iterate counter from d_iter
+  bool no_graphs = false, graph_capturing = false;
+  unsigned long long* d_iter = nullptr;
+  unsigned long long d_iter_value = ~0ull;  // what d_iter holds once queued work ran
+  cudaGraphExec_t graph_exec = nullptr;
+  const double* graph_X = nullptr;           // X the graph was captured with
+  int64_t graph_launches = 0, graph_chord_launches = 0;
+  int64_t graph_replays = 0;
   unsigned long long* tc_prof = nullptr;  // MHAR_I8_PROFILE: tcgen05 kernels' per-CTA counters
   // structure-aware paths (fastpath.cuh)
   double* diag_coef = nullptr;  // stacked diagonal blocks: per-row coefficient (m)
@@ -266,8 +275,9 @@ int launch_diag(mhar_ctx* c, int mode, const double* X) {
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
   p.bounds = mode == CHECK ? 0 : 1;
+  // one 1024-thread CTA per SM (the register budget allows one), one wave
   const int64_t splits = std::max<int64_t>(
-      1, std::min<int64_t>(c->KT, (4 * (int64_t)c->num_sms + c->ct64 - 1) / c->ct64));
+      1, std::min<int64_t>(c->KT, (int64_t)c->num_sms / c->ct64));
   p.kt_per_cta = (c->KT + splits - 1) / splits;
   const dim3 grid((unsigned)c->ct64, (unsigned)((c->KT + p.kt_per_cta - 1) / p.kt_per_cta));
   std::pair<cudaEvent_t, cudaEvent_t> ev{};
@@ -455,6 +465,7 @@ int launch_normals(mhar_ctx* c, double* out) {
   RngParams rp;
   rp.seed = c->opt.seed;
   rp.iterate = (uint64_t)c->iterations;
+  rp.iter_dev = c->graph_capturing ? c->d_iter : nullptr;
   rp.chain_offset = c->opt.chain_offset;
   rp.n = c->n;
   rp.z = c->z;
@@ -512,6 +523,7 @@ int launch_redraw(mhar_ctx* c) {
   rp.err = c->err;
   rp.seed = c->opt.seed;
   rp.iterate = (uint64_t)c->iterations;
+  rp.iter_dev = c->graph_capturing ? c->d_iter : nullptr;
   rp.chain_offset = c->opt.chain_offset;
   rp.col_state = c->col_state;
   rp.mode = c->opt.rng;
@@ -533,6 +545,7 @@ ThetaParams theta_params(mhar_ctx* c, const double* injected_u) {
   tp.err = c->err;
   tp.seed = c->opt.seed;
   tp.iterate = (uint64_t)c->iterations;
+  tp.iter_dev = c->graph_capturing ? c->d_iter : nullptr;
   tp.chain_offset = c->opt.chain_offset;
   tp.z = c->z;
   tp.mode = c->opt.rng;
@@ -670,13 +683,91 @@ int enqueue_iterate(mhar_ctx* c, int64_t reproject_every, bool injected) {
   return 0;
 }
 
+// A steady iterate: the same kernel chain as the last one -- no slack
+// refresh due, no reprojection after it.
+bool steady_iterate(const mhar_ctx* c, int64_t reproject_every) {
+  if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
+    const int64_t every = c->opt.refresh_every > 0 ? c->opt.refresh_every : 128;
+    if (!c->slack_valid || c->since_refresh >= every) return false;
+  }
+  return !(c->me > 0 && reproject_every > 0 && (c->iterations + 1) % reproject_every == 0);
+}
+
+void drop_graph(mhar_ctx* c) {
+  if (c->graph_exec) cudaGraphExecDestroy(c->graph_exec);
+  c->graph_exec = nullptr;
+}
+
+// One steady iterate as a CUDA-graph replay: the launch-bound part of the
+// multi-kernel path (7-10 kernels of a few microseconds each on mid-size
+// bodies) costs one graph launch on the host.  The graph is captured from
+// enqueue_iterate itself on first use; its kernels take the Philox counter
+// from d_iter, which the graph's last node advances.
+int graph_iterate(mhar_ctx* c) {
+  if (c->graph_exec && c->graph_X != c->X) drop_graph(c);  // set_state swapped the state buffer
+  if (!c->graph_exec) {
+    const int64_t it0 = c->iterations, sr0 = c->since_refresh, l0 = c->launches,
+                  cl0 = c->chord_launches;
+    mhar_dev::iter_set_kernel<<<1, 1, 0, c->stream>>>(c->d_iter, (unsigned long long)it0);
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      c->no_graphs = true;
+      return enqueue_iterate(c, 0, false);
+    }
+    c->graph_capturing = true;
+    int s = enqueue_iterate(c, 0, false);
+    if (!s) mhar_dev::iter_inc_kernel<<<1, 1, 0, c->stream>>>(c->d_iter);
+    c->graph_capturing = false;
+    const cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
+    cudaGraphExec_t ex = nullptr;
+    const bool ok = !s && ec == cudaSuccess && g &&
+                    cudaGraphInstantiate(&ex, g, 0) == cudaSuccess;
+    if (g) cudaGraphDestroy(g);
+    c->graph_launches = c->launches - l0;
+    c->graph_chord_launches = c->chord_launches - cl0;
+    // the capture ran enqueue_iterate's host bookkeeping; undo it, the replay
+    // below applies it
+    c->iterations = it0;
+    c->since_refresh = sr0;
+    c->launches = l0;
+    c->chord_launches = cl0;
+    cudaGetLastError();
+    if (!ok) {
+      if (ex) cudaGraphExecDestroy(ex);
+      c->no_graphs = true;  // not capturable here: the launch-per-kernel path
+      return s ? s : enqueue_iterate(c, 0, false);
+    }
+    c->graph_exec = ex;
+    c->graph_X = c->X;
+    c->d_iter_value = (unsigned long long)it0;
+  }
+  if (c->d_iter_value != (unsigned long long)c->iterations) {
+    mhar_dev::iter_set_kernel<<<1, 1, 0, c->stream>>>(c->d_iter,
+                                                      (unsigned long long)c->iterations);
+    c->d_iter_value = (unsigned long long)c->iterations;
+  }
+  CK(cudaGraphLaunch(c->graph_exec, c->stream));
+  ++c->graph_replays;
+  ++c->iterations;
+  ++c->d_iter_value;
+  if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) ++c->since_refresh;
+  c->launches += c->graph_launches;
+  c->chord_launches += c->graph_chord_launches;
+  return 0;
+}
+
 // `iters` iterates of every walk: one walk-resident launch for small bodies,
-// else the per-iterate kernel chain.
+// else the per-iterate kernel chain (steady iterates replayed as a CUDA graph
+// when a call runs several and no per-launch timing is requested).
 int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   if (iters <= 0) return 0;
   if (!c->Acm) {
+    const bool graphs = !c->no_graphs && !c->timing && iters >= 4 && c->d_iter;
     for (int64_t i = 0; i < iters; ++i) {
-      int s = enqueue_iterate(c, reproject_every, false);
+      const int s = graphs && steady_iterate(c, reproject_every)
+                        ? graph_iterate(c)
+                        : enqueue_iterate(c, reproject_every, false);
       if (s) return s;
     }
     return 0;
@@ -1151,6 +1242,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   cudaMemsetAsync(c->err, 0xFF, sizeof(unsigned long long), c->stream);
   int big = 0x7FFFFFFF;
   cudaMemcpyAsync(c->first_reject, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
+  c->no_graphs = std::getenv("MHAR_NO_GRAPHS") != nullptr;
+  if ((st = dalloc(c, &c->d_iter, 1))) return bail(st);
   fill_keys_kernel<<<blocks_for(c->z_pad, 256, 1 << 20), 256, 0, c->stream>>>(
       c->hi_key, c->lo_key, c->viol_key, c->sides, c->z_pad);
   ++c->launches;
@@ -1182,6 +1275,7 @@ int mhar_ctx_destroy(mhar_ctx* c) {
   if (!c) return 0;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graph(c);
   if (c->tc_prof) report_tc_profile(c);
   for (auto& ev : c->pending) {
     cudaEventDestroy(ev.first);

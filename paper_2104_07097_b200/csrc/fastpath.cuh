@@ -20,7 +20,7 @@
 
 namespace mhar_dev {
 
-constexpr int kDiagThreads = 256;
+constexpr int kDiagThreads = 1024;  // = B_PIECE: one packed element per thread
 
 struct DiagParams {
   const double* coef;  // m per-row coefficients (row r: column r % n)
@@ -38,8 +38,9 @@ struct DiagParams {
   int bounds;          // 0: containment only (max_i (A x - b)_i)
 };
 
-// grid = (walk tiles of 64, coordinate splits); thread t owns packed element
-// t + 256 j (j = 0..3) of every piece, i.e. a fixed (walk, k-offset) set.
+// grid = (walk tiles of 64, coordinate splits); thread t owns packed element t
+// of every piece (B_PIECE = 1024 = blockDim), i.e. one (walk, k-offset) slot,
+// and walks its k tiles four at a time with all eight loads in flight.
 __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagParams p) {
   if (*p.err != kNoError) return;
   __shared__ long long s_hi[BC], s_lo[BC], s_viol[BC];
@@ -55,50 +56,45 @@ __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagPara
   __syncthreads();
   const int64_t kt0 = blockIdx.y * p.kt_per_cta;
   const int64_t kt1 = kt0 + p.kt_per_cta < p.KT ? kt0 + p.kt_per_cta : p.KT;
-  const double* Xt = p.X + ct * p.KT * B_PIECE;
-  const double* Dt = p.D + ct * p.KT * B_PIECE;
-  double hi[4], lo[4], viol[4];
-  unsigned sd[4];
-  int wl[4];
-  int64_t kof[4];
+  const double* Xt = p.X + ct * p.KT * B_PIECE + tid;
+  const double* Dt = p.D + ct * p.KT * B_PIECE + tid;
+  int64_t wc, kof;
+  b_coords(tid, p.KT, &wc, &kof);  // within the first piece of tile 0
+  double ehi = __longlong_as_double(0x7FF0000000000000LL), elo = -ehi;
+  double viol = __longlong_as_double((long long)0xFFF0000000000000ULL);
+  unsigned sd = 0u;
+  for (int64_t kt = kt0; kt < kt1; kt += 4) {
+    double x[4], d[4];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    int64_t c, k;
-    b_coords(tid + 256 * j, p.KT, &c, &k);  // within the first piece of tile 0
-    wl[j] = (int)c;
-    kof[j] = k;
-    hi[j] = __longlong_as_double(0x7FF0000000000000LL);
-    lo[j] = -hi[j];
-    viol[j] = -hi[j];
-    sd[j] = 0u;
-  }
-  for (int64_t kt = kt0; kt < kt1; ++kt)
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = (kt + u) * BK + kof;
+      const bool live = kt + u < kt1 && k < p.n;
+      x[u] = live ? Xt[(kt + u) * B_PIECE] : 0.0;
+      d[u] = live ? Dt[(kt + u) * B_PIECE] : 0.0;
+    }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int64_t k = kt * BK + kof[j];
-      if (k >= p.n) continue;
-      const double x = Xt[kt * B_PIECE + tid + 256 * j];
-      const double d = Dt[kt * B_PIECE + tid + 256 * j];
+    for (int u = 0; u < 4; ++u) {
+      const int64_t k = (kt + u) * BK + kof;
+      if (kt + u >= kt1 || k >= p.n) continue;
       for (int64_t blk = 0; blk < p.blocks; ++blk) {
         const int64_t r = blk * p.n + k;
         const double cf = __ldg(p.coef + r);
         // -(x c) + b and d c, one rounding each (sampler.cpp:168-170; no FMA
         // contraction, so the bounds equal the one-term dot products')
-        const double sl = __dsub_rn(__ldg(p.b + r), __dmul_rn(x, cf));
-        viol[j] = fmax(viol[j], -sl);
-        if (p.bounds) scan_row(sl, __dmul_rn(d, cf), p.eps_dir, hi[j], lo[j], sd[j]);
+        const double sl = __dsub_rn(__ldg(p.b + r), __dmul_rn(x[u], cf));
+        viol = fmax(viol, -sl);
+        if (p.bounds) scan_row(sl, __dmul_rn(d[u], cf), p.eps_dir, ehi, elo, sd);
       }
     }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const long long vk = dkey(viol[j]);
-    if (vk > s_viol[wl[j]]) atomicMax(&s_viol[wl[j]], vk);
-    if (p.bounds) {
-      const long long hk = dkey(hi[j]), lk = dkey(lo[j]);
-      if (hk < s_hi[wl[j]]) atomicMin(&s_hi[wl[j]], hk);
-      if (lk > s_lo[wl[j]]) atomicMax(&s_lo[wl[j]], lk);
-      if (sd[j]) atomicOr(&s_sd[wl[j]], sd[j]);
-    }
+  }
+  const int wl = (int)wc;
+  const long long vk = dkey(viol);
+  if (vk > s_viol[wl]) atomicMax(&s_viol[wl], vk);
+  if (p.bounds) {
+    const long long hk = dkey(ehi), lk = dkey(elo);
+    if (hk < s_hi[wl]) atomicMin(&s_hi[wl], hk);
+    if (lk > s_lo[wl]) atomicMax(&s_lo[wl], lk);
+    if (sd) atomicOr(&s_sd[wl], sd);
   }
   __syncthreads();
   if (tid < BC) {

@@ -112,6 +112,7 @@ __global__ void fill_keys_kernel(long long* hi, long long* lo, long long* viol, 
 struct RngParams {
   uint64_t seed;
   uint64_t iterate;       // global iterate counter (Philox key)
+  const unsigned long long* iter_dev = nullptr;  // graph replays: the counter in device memory
   int64_t chain_offset;   // global id of local walk 0
   int64_t n, z, KT;
   int mode;               // 0 Philox, 1 reference SplitMix streams
@@ -131,7 +132,8 @@ __global__ void normals_kernel(const RngParams rp, double* __restrict__ H,
     double u1, u2;
     if (rp.mode == 0) {
       uint64_t a, b;
-      philox_u64x2(rp.seed, (uint32_t)pidx, (uint64_t)(rp.chain_offset + c), rp.iterate, 0,
+      philox_u64x2(rp.seed, (uint32_t)pidx, (uint64_t)(rp.chain_offset + c),
+                   rp.iter_dev ? (uint64_t)*rp.iter_dev : rp.iterate, 0,
                    kDomNormal, &a, &b);
       u1 = u01_open_closed(a);
       u2 = u01_closed_open(b);
@@ -312,6 +314,7 @@ struct RedrawParams {
   unsigned long long* redraw_total;
   unsigned long long* err;
   uint64_t seed, iterate;
+  const unsigned long long* iter_dev = nullptr;  // graph replays: the counter in device memory
   int64_t chain_offset;
   uint64_t* col_state;    // reference mode
   int mode;
@@ -371,7 +374,8 @@ __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
         double u1, u2;
         if (rp.mode == 0) {
           uint64_t a, b;
-          philox_u64x2(rp.seed, (uint32_t)pidx, (uint64_t)(rp.chain_offset + c), rp.iterate,
+          philox_u64x2(rp.seed, (uint32_t)pidx, (uint64_t)(rp.chain_offset + c),
+                       rp.iter_dev ? (uint64_t)*rp.iter_dev : rp.iterate,
                        (uint32_t)(attempt + 1), kDomNormal, &a, &b);
           u1 = u01_open_closed(a);
           u2 = u01_closed_open(b);
@@ -473,6 +477,7 @@ struct ThetaParams {
   double* theta;
   const unsigned long long* err;
   uint64_t seed, iterate;
+  const unsigned long long* iter_dev = nullptr;  // graph replays: the counter in device memory
   int64_t chain_offset, z;
   int mode;
   uint64_t* theta_state;  // reference mode (device scalar)
@@ -503,7 +508,8 @@ __global__ void theta_kernel(const ThetaParams tp) {
     int r = 0;
     for (; r < kMaxThetaRejects; ++r) {
       uint64_t a, b;
-      philox_u64x2(tp.seed, (uint32_t)r, (uint64_t)(tp.chain_offset + c), tp.iterate, 0,
+      philox_u64x2(tp.seed, (uint32_t)r, (uint64_t)(tp.chain_offset + c),
+                   tp.iter_dev ? (uint64_t)*tp.iter_dev : tp.iterate, 0,
                    kDomTheta, &a, &b);
       th = chord_point(u01_closed_open(a), lo, hi);
       if (th > lo && th < hi) break;
@@ -632,5 +638,9 @@ __global__ void contains_kernel(const double* __restrict__ viol, const double* _
     if (set_error) atomicMin(err, error_word(PH_COLLECT, c, ST_NUMERICAL));
   }
 }
+
+// the device copy of the iterate counter (CUDA-graph replays of an iterate)
+__global__ void iter_set_kernel(unsigned long long* it, unsigned long long v) { *it = v; }
+__global__ void iter_inc_kernel(unsigned long long* it) { *it += 1ull; }
 
 }  // namespace mhar_dev
