@@ -92,14 +92,16 @@ typedef struct {
   double eps_feas;       /* SamplerConfig::eps_feas (1e-9) */
   int rng;               /* MHAR_RNG_* */
   int slack_mode;        /* MHAR_SLACK_* */
-  int64_t refresh_every; /* incremental mode: fused refresh cadence (0 = default 64) */
+  int64_t refresh_every; /* incremental mode: fused refresh cadence (0 = default 128) */
   int device;            /* CUDA ordinal */
   int small_path;        /* 1 (default): bodies whose A_I, P, A_E fit in shared memory run
                             all iterates of a batch in one walk-resident launch (Philox only) */
-  int precision;         /* 64 (default): fp64 DMMA.  32: the fp32 variant -- A_I rounded to
-                            fp32, rates A_I d on tcgen05 tensor cores (3xTF32, fp32 accuracy),
-                            fp64 slack/state, chords of {A_I x <= b_I - fp32_margin} */
-  double fp32_margin;    /* precision 32: slack margin mu (0 = default 1e-6) */
+  int precision;         /* 64 (default): fp64 DMMA.  32: the fp32 variant -- rates A_I d on
+                            tcgen05 tensor cores with fp32 accuracy (kind::f16 with per-row /
+                            per-walk power-of-two scales, A_I as two halves; MHAR_TC_F16=0:
+                            kind::tf32 hi/lo split), fp64 slack/state, chords of
+                            {A_I x <= b_I - fp32_margin} */
+  double fp32_margin;    /* precision 32: slack margin mu (0 = default 2e-5) */
   int f64_engine;        /* precision 64 only.  MHAR_F64_DMMA (default): A_I d on the fp64
                             tensor cores (DMMA).  MHAR_F64_INT8: A_I d formed exactly from
                             53-bit fixed-point operands split into int8 slices on the
