@@ -24,7 +24,7 @@
 // hold all 256 rows for their own walks, so each epilogue thread still owns
 // one walk and reduces its 256 rows in registers.
 //
-// Warp roles (192 threads per CTA): warp 0 lane 0 = bulk-copy producer (its
+// Warp roles (320 threads per CTA): warp 0 lane 0 = bulk-copy producer (its
 // CTA's pieces); warp 1 = TMEM allocation (both CTAs), lane 0 = MMA issuer
 // in the even CTA and the "stage landed" relay in the odd one (waits its
 // CTA's full barrier, arrives remotely on the leader's peer barrier); warps
