@@ -472,7 +472,7 @@ int launch_normals(mhar_ctx* c, double* out) {
   rp.KT = c->KT;
   rp.mode = c->opt.rng;
   rp.col_state = c->col_state;
-  const int64_t work = ((c->n + 1) / 2) * c->z;
+  const int64_t work = c->ct64 * c->KT * 16 * 32;
   normals_kernel<<<blocks_for(work, 256, c->num_sms * 16), 256, 0, c->stream>>>(rp, out, c->err);
   LAUNCH_OK(c, "normals_kernel");
   return 0;

@@ -125,10 +125,20 @@ __global__ void normals_kernel(const RngParams rp, double* __restrict__ H,
                                const unsigned long long* err) {
   if (*err != kNoError) return;
   const int64_t ppc = (rp.n + 1) / 2;
-  const int64_t total = ppc * rp.z;
+  // thread order follows the packed layout: a warp fills one (walk tile, k
+  // tile, k8, column group) block of 8 walks x 8 coordinates -- 512
+  // contiguous bytes -- one pair per thread
+  const int64_t ct64 = (rp.z + BC - 1) / BC;
+  const int64_t total = ct64 * rp.KT * 16 * 32;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = t / ppc, pidx = t % ppc;
+    const int64_t blk = t >> 5;
+    const int tl = (int)(t & 31);
+    const int64_t cg = blk & 7, k8 = (blk >> 3) & 1, kt = (blk >> 4) % rp.KT,
+                  ct = (blk >> 4) / rp.KT;
+    const int64_t c = ct * BC + cg * 8 + (tl >> 2);
+    const int64_t pidx = (kt * BK + k8 * 8) / 2 + (tl & 3);
+    if (c >= rp.z || pidx >= ppc) continue;
     double u1, u2;
     if (rp.mode == 0) {
       uint64_t a, b;
