@@ -45,7 +45,10 @@ constexpr int TC_M = 128;             // walks per CTA (per unit: 2 x 128)
 constexpr int TC_N = 256;             // rows per unit
 constexpr int TC_NH = 128;            // rows staged by each CTA of the pair
 constexpr int TC_BK = 16;             // k per stage
-constexpr int TC_STAGES = 8;
+#ifndef MHAR_TC_STAGES
+#define MHAR_TC_STAGES 8
+#endif
+constexpr int TC_STAGES = MHAR_TC_STAGES;
 constexpr int TC_D_PIECE = TC_M * TC_BK;   // floats per D stage piece (8 KB)
 constexpr int TC_A_PIECE = TC_NH * TC_BK;  // floats per A_hi (or A_lo) half piece (8 KB)
 constexpr int TC_STAGE_FLOATS = TC_D_PIECE + 2 * TC_A_PIECE;  // 24 KB
