@@ -155,6 +155,13 @@ int mhar_sync(mhar_ctx* ctx);
  * streams carry per-walk state instead: INVALID_ARGUMENT there. */
 int mhar_get_iteration(mhar_ctx* ctx, int64_t* iteration);
 int mhar_set_iteration(mhar_ctx* ctx, int64_t iteration);
+/* WalkRng state (rng.hpp:42-55) of a reference-stream context: the z column
+ * stream states and the shared theta stream state, exactly the uint64
+ * counters RngStream holds (rng.hpp:16-33).  Moving them to another context
+ * continues the same streams (a rebind to another polytope, or checkpoint /
+ * resume in MHAR_RNG_REFERENCE mode).  INVALID_ARGUMENT on a Philox context. */
+int mhar_get_streams(mhar_ctx* ctx, uint64_t* col_states, uint64_t* theta_state);
+int mhar_set_streams(mhar_ctx* ctx, const uint64_t* col_states, const uint64_t* theta_state);
 /* mhar_step bracketed by CUDA events on the context's stream; *device_ms is
  * the device time of the `iters` iterates (synchronises). */
 int mhar_step_timed(mhar_ctx* ctx, int64_t iters, int64_t reproject_every, double* device_ms);

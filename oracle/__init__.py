@@ -101,6 +101,15 @@ def lib():
         L.orc_run.restype = C.c_int
         L.orc_run.argtypes = [_dp, _dp, _i64, _dp, _dp, _i64, _i64, C.POINTER(RunConfig), _dp,
                               _dp, C.POINTER(RunStats)]
+        _u32p = C.POINTER(C.c_uint32)
+        L.orc_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
+        L.orc_philox_u64x2.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
+                                       C.c_uint32, C.c_uint32, _u64p, _u64p]
+        L.orc_philox_normals.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32, _dp,
+                                         _i64]
+        L.orc_step_philox.restype = C.c_int
+        L.orc_step_philox.argtypes = [_dp, _dp, _i64, _i64, _dp, C.c_double, C.c_uint64, _i64,
+                                      C.c_uint64, _dp, _i64, _i64p, _i64p]
         _i32p = C.POINTER(C.c_int32)
         L.orc_minimum_spanning_tree.restype = C.c_int
         L.orc_minimum_spanning_tree.argtypes = [_dp, _i64, _i64, _i32p, _i32p, _dp]
@@ -266,6 +275,37 @@ def step(A, b, P, eps_dir, rng: WalkRng, X):
     st = lib().orc_step(_d(A), _d(b), A.shape[0], A.shape[1], _d(Pf), eps_dir,
                         rng.cols.ctypes.data_as(_u64p), rng.theta.ctypes.data_as(_u64p), _d(X),
                         X.shape[1], C.byref(red), C.byref(err))
+    return st, red.value, err.value
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 of a 4-word counter under a 2-word key (4 uint32)."""
+    c = (C.c_uint32 * 4)(*ctr)
+    k = (C.c_uint32 * 2)(*key)
+    o = (C.c_uint32 * 4)()
+    lib().orc_philox4x32_10(c, k, o)
+    return list(o)
+
+
+def philox_normals(seed, walk, iterate, attempt, n):
+    out = np.empty(n)
+    lib().orc_philox_normals(seed & (2**64 - 1), walk, iterate, attempt, _d(out), n)
+    return out
+
+
+def step_philox(A, b, P, eps_dir, seed, chain_offset, iterate, X):
+    """One reference iterate in place on X (Fortran n x z) with the engine's
+    Philox draws for (seed, global walk chain_offset + k, iterate).  Returns
+    (status, redraws, err_chain)."""
+    A = _f(A)
+    b = np.ascontiguousarray(b, dtype=np.float64)
+    Pf = None if P is None else _f(P)
+    assert X.flags.f_contiguous and X.dtype == np.float64
+    red = C.c_int64(0)
+    err = C.c_int64(-1)
+    st = lib().orc_step_philox(_d(A), _d(b), A.shape[0], A.shape[1], _d(Pf), eps_dir,
+                               seed & (2**64 - 1), chain_offset, iterate, _d(X), X.shape[1],
+                               C.byref(red), C.byref(err))
     return st, red.value, err.value
 
 

@@ -812,3 +812,166 @@ out:
   free(Ginv);
   return st;
 }
+
+/* ======================================================================== */
+/* Production-mode draws: the engine's Philox4x32-10 keying                  */
+/* ======================================================================== */
+/*
+ * The reference draws from SplitMix streams (restated above); the engine's
+ * production mode draws the same uniforms' roles from Philox4x32-10 (Salmon,
+ * Moraes, Dror, Shaw, "Parallel random numbers: as easy as 1, 2, 3", SC'11 --
+ * the published algorithm, pinned below to its authors' known-answer vectors
+ * in tests/test_oracle_kats.py), keyed on (seed, global walk, iterate,
+ * attempt, domain) as include/mhar_b200.h documents.  orc_step_philox is the
+ * reference step (sampler.cpp:235-272) driven by those draws, so the
+ * engine's default path can be compared with the reference algorithm
+ * iterate by iterate.  Test infrastructure only.
+ */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+  for (int round = 0; round < 10; ++round) {
+    const uint64_t p0 = (uint64_t)M0 * c0, p1 = (uint64_t)M1 * c2;
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c1 ^ k0;
+    const uint32_t n2 = (uint32_t)(p0 >> 32) ^ c3 ^ k1;
+    c1 = (uint32_t)p1;
+    c3 = (uint32_t)p0;
+    c0 = n0;
+    c2 = n2;
+    k0 += W0;
+    k1 += W1;
+  }
+  out[0] = c0;
+  out[1] = c1;
+  out[2] = c2;
+  out[3] = c3;
+}
+
+/* Two 64-bit words for (seed; index, walk, iterate, attempt, domain):
+ * counter (index, walk lo32, iterate lo32, iterate bits 32..47 | attempt
+ * (6 bits) << 16 | walk bits 32..39 << 22 | domain << 30), key = seed. */
+void orc_philox_u64x2(uint64_t seed, uint32_t index, uint64_t walk, uint64_t iterate,
+                      uint32_t attempt, uint32_t domain, uint64_t* a, uint64_t* b) {
+  const uint32_t ctr[4] = {index, (uint32_t)walk, (uint32_t)iterate,
+                           ((uint32_t)(iterate >> 32) & 0xFFFFu) | ((attempt & 0x3Fu) << 16) |
+                               (((uint32_t)(walk >> 32) & 0xFFu) << 22) | (domain << 30)};
+  const uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t r[4];
+  orc_philox4x32_10(ctr, key, r);
+  *a = ((uint64_t)r[0] << 32) | r[1];
+  *b = ((uint64_t)r[2] << 32) | r[3];
+}
+
+enum { kDomNormal = 0, kDomTheta = 1 };
+
+/* Column of standard normals for (walk, iterate, attempt): pair p from
+ * Philox index p -- u1 = open (0,1] from word a, u2 = [0,1) from word b --
+ * then the reference's Box-Muller (rng.cpp:115-124), odd n dropping the
+ * last sine (rng.hpp:57-64). */
+void orc_philox_normals(uint64_t seed, uint64_t walk, uint64_t iterate, uint32_t attempt,
+                        double* out, int64_t n) {
+  for (int64_t p = 0; 2 * p < n; ++p) {
+    uint64_t a, b;
+    orc_philox_u64x2(seed, (uint32_t)p, walk, iterate, attempt, kDomNormal, &a, &b);
+    const double u1 = (double)((a >> 11) + 1) * 0x1.0p-53;
+    const double u2 = (double)(b >> 11) * 0x1.0p-53;
+    double c, s;
+    orc_box_muller(u1, u2, &c, &s);
+    out[2 * p] = c;
+    if (2 * p + 1 < n) out[2 * p + 1] = s;
+  }
+}
+
+/* draw_theta (sampler.cpp:95-101) with rejection draw r from Philox index r
+ * of the theta domain. */
+static double draw_theta_philox(uint64_t seed, uint64_t walk, uint64_t iterate, double lower,
+                                double upper, int* midpoint) {
+  for (int r = 0; r < kMaxThetaRejects; ++r) {
+    uint64_t a, b;
+    orc_philox_u64x2(seed, (uint32_t)r, walk, iterate, 0, kDomTheta, &a, &b);
+    const double theta = chord_point((double)(a >> 11) * 0x1.0p-53, lower, upper);
+    if (theta > lower && theta < upper) return theta;
+  }
+  *midpoint = 1;
+  return chord_point(0.5, lower, upper);
+}
+
+int orc_step_philox(const double* A, const double* b, int64_t m, int64_t n, const double* P,
+                    double eps_dir, uint64_t seed, int64_t chain_offset, uint64_t iterate,
+                    double* X, int64_t z, int64_t* redraws, int64_t* err_chain) {
+  const size_t nz = (size_t)(n * z);
+  double* h = (double*)malloc(sizeof(double) * nz);
+  double* d = (double*)malloc(sizeof(double) * nz);
+  double* lo = (double*)malloc(sizeof(double) * (size_t)z);
+  double* hi = (double*)malloc(sizeof(double) * (size_t)z);
+  uint8_t* degen = (uint8_t*)malloc((size_t)z);
+  uint8_t* collapsed = (uint8_t*)calloc((size_t)z, 1);
+  int st = ST_OK;
+
+  for (int64_t k = 0; k < z; ++k)
+    orc_philox_normals(seed, (uint64_t)(chain_offset + k), iterate, 0, h + k * n, n);
+  if (P) {
+    orc_gemm(n, n, z, P, h, d);
+    for (int64_t k = 0; k < z; ++k)
+      if (col_norm(d + k * n, n) <= kNearZeroDirection) collapsed[k] = 1;
+  } else {
+    memcpy(d, h, sizeof(double) * nz);
+  }
+  st = orc_lambda_intervals(A, b, m, n, X, d, z, eps_dir, lo, hi, degen, NULL, err_chain);
+  if (st != ST_OK) goto done;
+  for (int64_t k = 0; k < z; ++k)
+    if (collapsed[k]) degen[k] = 1;
+  /* redraw_column (sampler.cpp:105-123): attempt a of walk k draws from
+   * Philox attempt a + 1 */
+  for (int64_t k = 0; k < z && st == ST_OK; ++k) {
+    if (!degen[k]) continue;
+    int ok = 0;
+    for (int attempt = 0; attempt < kMaxDirectionRetries; ++attempt) {
+      ++*redraws;
+      double* hk = (P ? h : d) + k * n;
+      double* dk = d + k * n;
+      orc_philox_normals(seed, (uint64_t)(chain_offset + k), iterate, (uint32_t)(attempt + 1),
+                         hk, n);
+      if (P) {
+        orc_gemm(n, n, 1, P, hk, dk);
+        if (col_norm(dk, n) <= kNearZeroDirection) continue;
+      }
+      double l, u;
+      int dg;
+      const int cs = column_interval(A, b, m, n, X + k * n, dk, eps_dir, &l, &u, &dg);
+      if (cs != ST_OK) {
+        st = cs;
+        if (err_chain) *err_chain = k;
+        break;
+      }
+      if (!dg) {
+        lo[k] = l;
+        hi[k] = u;
+        degen[k] = 0;
+        ok = 1;
+        break;
+      }
+    }
+    if (st == ST_OK && !ok) {
+      st = ST_RETRY_EXHAUSTED;
+      if (err_chain) *err_chain = k;
+    }
+  }
+  if (st != ST_OK) goto done;
+  for (int64_t k = 0; k < z; ++k) {
+    int mid = 0;
+    const double theta =
+        draw_theta_philox(seed, (uint64_t)(chain_offset + k), iterate, lo[k], hi[k], &mid);
+    double* xk = X + k * n;
+    const double* dk = d + k * n;
+    for (int64_t i = 0; i < n; ++i) xk[i] = xk[i] + theta * dk[i];
+  }
+done:
+  free(h);
+  free(d);
+  free(lo);
+  free(hi);
+  free(degen);
+  free(collapsed);
+  return st;
+}

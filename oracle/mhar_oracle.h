@@ -90,6 +90,25 @@ int orc_step_injected(const double* A, const double* b, int64_t m, int64_t n,
                       const double* H, const double* U, double* lower, double* upper,
                       double* theta, uint8_t* flags, int64_t* err_chain);
 
+/* ---- production-mode draws: the engine's Philox4x32-10 keying -----------
+ * Philox4x32-10 (Salmon et al., SC'11), counter ctr, key key -> out.  Draw
+ * (a, b) for (seed; index, walk, iterate, attempt, domain) as the engine
+ * keys it (include/mhar_b200.h MHAR_RNG_PHILOX).  orc_philox_normals fills
+ * one walk's column (pair p from index p, Box-Muller as rng.cpp:115-124).
+ * orc_step_philox is orc_step (sampler.cpp:235-272) with these draws: the
+ * first direction from attempt 0, redraw a from attempt a + 1, theta
+ * rejection r from index r of the theta domain.  No projector
+ * factoring and no walk interaction: the reference algorithm, only the
+ * random source differs. */
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+void orc_philox_u64x2(uint64_t seed, uint32_t index, uint64_t walk, uint64_t iterate,
+                      uint32_t attempt, uint32_t domain, uint64_t* a, uint64_t* b);
+void orc_philox_normals(uint64_t seed, uint64_t walk, uint64_t iterate, uint32_t attempt,
+                        double* out, int64_t n);
+int orc_step_philox(const double* A, const double* b, int64_t m, int64_t n, const double* P,
+                    double eps_dir, uint64_t seed, int64_t chain_offset, uint64_t iterate,
+                    double* X, int64_t z, int64_t* redraws, int64_t* err_chain);
+
 /* ---- full run with warm start: proj/src/sampler.cpp:274-335 --------------
  * x0 (n) replaces chebyshev_center (sampler.cpp:276); cfg already resolved.
  * samples: (windows*z) x n row-major, collection order. */

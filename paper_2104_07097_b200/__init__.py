@@ -134,7 +134,7 @@ EXPORTED_SYMBOLS = [
     "mhar_flops_per_iterate", "mhar_last_error", "mhar_version", "mhar_device_count",
     "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
     "mhar_select_points", "mhar_chebyshev_center", "mhar_debug_last_iterate",
-    "mhar_get_iteration", "mhar_set_iteration",
+    "mhar_get_iteration", "mhar_set_iteration", "mhar_get_streams", "mhar_set_streams",
 ]
 
 
@@ -176,6 +176,11 @@ def lib():
     L.mhar_get_iteration.restype = C.c_int
     L.mhar_set_iteration.argtypes = [C.c_void_p, C.c_int64]
     L.mhar_set_iteration.restype = C.c_int
+    _u64p = C.POINTER(C.c_uint64)
+    L.mhar_get_streams.argtypes = [C.c_void_p, _u64p, _u64p]
+    L.mhar_get_streams.restype = C.c_int
+    L.mhar_set_streams.argtypes = [C.c_void_p, _u64p, _u64p]
+    L.mhar_set_streams.restype = C.c_int
     L.mhar_debug_last_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
     L.mhar_debug_last_iterate.restype = C.c_int
     L.mhar_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -415,6 +420,7 @@ class Engine:
         opt.f64_engine = {"dmma": F64_DMMA, "int8": F64_INT8}[f64_engine]
         self.precision = int(precision)
         self.f64_engine = f64_engine
+        self.rng = rng
         P = G = None
         if projector is not None:
             P = _f(projector.p)
@@ -523,14 +529,39 @@ class Engine:
     def iteration(self, value: int):
         _check(lib().mhar_set_iteration(self._h, int(value)))
 
+    def get_streams(self):
+        """Reference-stream mode: (z column stream states, theta stream state),
+        the WalkRng counters (rng.hpp:42-55)."""
+        cols = np.empty(self.z, np.uint64)
+        th = np.empty(1, np.uint64)
+        _u64p = C.POINTER(C.c_uint64)
+        _check(lib().mhar_get_streams(self._h, cols.ctypes.data_as(_u64p), th.ctypes.data_as(_u64p)))
+        return cols, int(th[0])
+
+    def set_streams(self, cols, theta):
+        cols = np.ascontiguousarray(cols, dtype=np.uint64)
+        if cols.shape != (self.z,):
+            raise MharError(ErrorCode.dimension_mismatch,
+                            f"set_streams: {cols.shape[0]} column streams for {self.z} walks")
+        th = np.array([theta], dtype=np.uint64)
+        _u64p = C.POINTER(C.c_uint64)
+        _check(lib().mhar_set_streams(self._h, cols.ctypes.data_as(_u64p), th.ctypes.data_as(_u64p)))
+
     def checkpoint(self):
-        """(X, iteration): everything a Philox walk needs to resume."""
+        """Everything a walk set needs to resume: (X, iteration) with Philox
+        directions, (X, (column streams, theta stream)) on the reference
+        streams."""
+        if self.rng == "reference":
+            return self.get_state(), self.get_streams()
         return self.get_state(), self.iteration
 
     def restore(self, checkpoint):
-        X, it = checkpoint
+        X, key = checkpoint
         self.set_state(X)
-        self.iteration = it
+        if isinstance(key, tuple):
+            self.set_streams(*key)
+        else:
+            self.iteration = key
 
     def debug_last_iterate(self):
         """Test hook: (D n x z, lower, upper, theta) of the last iterate."""
@@ -550,6 +581,10 @@ class Engine:
             collect: bool = True):
         cfg = _RunConfig(int(phi), int(windows), int(burn_in), int(reproject_every))
         x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        if x0.shape != (self.n,):
+            # mhar_run reads exactly n doubles from x0
+            raise MharError(ErrorCode.dimension_mismatch,
+                            f"run: x0 has shape {x0.shape}, expected ({self.n},)")
         samples = np.empty((windows * self.z, self.n)) if collect else None
         st = _RunStats()
         _check(lib().mhar_run(self._h, C.byref(cfg), _d(x0), _d(samples), C.byref(st)))
@@ -639,22 +674,31 @@ def run(p: Polytope, cfg: SamplerConfig, x0=None, rng: str = "philox", slack: st
     """run() (sampler.cpp:274-335) on one B200.  Without x0 the start is the
     Chebyshev centre (sampler.cpp:276), computed before the clock starts as
     in the reference; with x0 that warm start replaces it (start_radius 0).
-    `clock` (the reference's ClockFn, sampler.cpp:278-282) is read once
-    before the projector is built and once after the last collection; by
-    default the engine's own run timer supplies `seconds`."""
+    `clock` (the reference's ClockFn, sampler.cpp:278-282; default the host's
+    monotonic clock) is read once before the projector is built and once
+    after the last collection, so `seconds` spans projector construction,
+    the context (polytope upload and packing) and every iterate, as the
+    reference's window does (sampler.cpp:284-335)."""
+    import time
     rc = resolve(cfg, p)
     radius = 0.0
     if x0 is None:
         center = chebyshev_center(p, device=device)
         x0, radius = center.x, center.radius
-    t0 = clock() if clock is not None else None
+    x0 = np.ascontiguousarray(x0, dtype=np.float64)
+    if x0.shape != (p.dim(),):
+        raise MharError(ErrorCode.dimension_mismatch,
+                        f"run: x0 has shape {x0.shape}, expected ({p.dim()},)")
+    if clock is None:
+        clock = time.perf_counter
+    t0 = clock()
     projector = compute_projection(p.a_eq) if p.num_equalities() > 0 else None
     windows = (rc.t_target + rc.z - 1) // rc.z
     with Engine(p, rc.z, seed=rc.seed, projector=projector, eps_dir=rc.eps_dir,
                 eps_feas=rc.eps_feas, rng=rng, slack=slack, device=device) as eng:
         samples, st = eng.run(x0, rc.phi, windows, rc.burn_in,
                               rc.reproject_every if projector is not None else 0)
-    seconds = st.seconds if clock is None else clock() - t0
+    seconds = clock() - t0
     return SampleSet(samples=samples, config=rc, start=np.asarray(x0, dtype=np.float64),
                      start_radius=radius, seconds=seconds, iterate_count=st.iterate_count,
                      windows=st.windows, redraw_count=st.redraw_count)

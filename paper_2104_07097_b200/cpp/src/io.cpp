@@ -3,29 +3,42 @@
 // nlohmann::json::dump(2) with sorted keys.
 #include "mhar/io.hpp"
 
+#include <algorithm>
+#include <cerrno>
 #include <charconv>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
-#include <sstream>
+#include <string_view>
 #include <vector>
 
 namespace mhar {
 namespace {
 
-void write_text(const std::string& path, const std::string& text) {
-  std::ofstream out(path, std::ios::binary);
-  if (!out) raise(ErrorCode::io_failure, "cannot open " + path + " for writing");
-  out << text;
-  if (!out) raise(ErrorCode::io_failure, "write failed for " + path);
+// Whole-file output through C stdio; any short write or close failure is an
+// IO_FAILURE naming the path and the errno text.
+void save_bytes(const std::string& path, std::string_view bytes) {
+  std::FILE* f = std::fopen(path.c_str(), "wb");
+  if (!f) raise(ErrorCode::io_failure, path + ": open for writing: " + std::strerror(errno));
+  const size_t put = bytes.empty() ? 0 : std::fwrite(bytes.data(), 1, bytes.size(), f);
+  const int closed = std::fclose(f);
+  if (put != bytes.size() || closed != 0)
+    raise(ErrorCode::io_failure, path + ": short write (" + std::to_string(put) + " of " +
+                                     std::to_string(bytes.size()) + " bytes)");
 }
 
-double parse_double(const std::string& token, const std::string& where) {
-  double value = 0.0;
-  const auto r = std::from_chars(token.data(), token.data() + token.size(), value);
-  if (r.ec != std::errc{} || r.ptr != token.data() + token.size())
-    raise(ErrorCode::io_failure, "bad number '" + token + "' in " + where);
-  return value;
+std::string load_bytes(const std::string& path) {
+  std::FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) raise(ErrorCode::io_failure, path + ": open for reading: " + std::strerror(errno));
+  std::string data;
+  char chunk[1 << 16];
+  size_t got = 0;
+  while ((got = std::fread(chunk, 1, sizeof(chunk), f)) > 0) data.append(chunk, got);
+  const bool bad = std::ferror(f) != 0;
+  std::fclose(f);
+  if (bad) raise(ErrorCode::io_failure, path + ": read error");
+  return data;
 }
 
 // JSON number for a double: shortest round trip, with ".0" on integral
@@ -53,65 +66,92 @@ std::string json_string(const std::string& s) {
   return out + "\"";
 }
 
+// Appends the shortest round-trip text of v (std::to_chars without a format
+// argument is specified to produce exactly that).
+void append_number(std::string& out, double v) {
+  char buf[32];
+  char* end = std::to_chars(buf, buf + sizeof(buf), v).ptr;
+  out.append(buf, end);
+}
+
 }  // namespace
 
 std::string format_double(double value) {
-  char buffer[32];
-  const auto result = std::to_chars(buffer, buffer + sizeof(buffer), value);
-  return std::string(buffer, result.ptr);
+  std::string s;
+  append_number(s, value);
+  return s;
 }
 
+// Header "x1,...,xn", then one line per collected point, cells separated by
+// commas, numbers in shortest round-trip form.  Byte-identical output for
+// identical matrices is what makes reruns comparable with cmp (acceptance #9).
 std::string sample_csv_string(const Matrix& samples) {
-  std::string out;
-  out.reserve(static_cast<size_t>(samples.size()) * 20 + 16);
-  for (Index j = 0; j < samples.cols(); ++j) {
-    if (j > 0) out += ',';
-    out += 'x';
-    out += std::to_string(j + 1);
+  const Index rows = samples.rows(), cols = samples.cols();
+  std::string text;
+  text.reserve(static_cast<size_t>(rows * cols) * 20 + static_cast<size_t>(cols) * 6 + 1);
+  for (Index j = 1; j <= cols; ++j) {
+    text += j == 1 ? "x" : ",x";
+    text += std::to_string(j);
   }
-  out += '\n';
-  for (Index i = 0; i < samples.rows(); ++i) {
-    for (Index j = 0; j < samples.cols(); ++j) {
-      if (j > 0) out += ',';
-      out += format_double(samples(i, j));
+  text.push_back('\n');
+  for (Index i = 0; i < rows; ++i) {
+    for (Index j = 0; j < cols; ++j) {
+      if (j) text.push_back(',');
+      append_number(text, samples(i, j));
     }
-    out += '\n';
+    text.push_back('\n');
   }
-  return out;
+  return text;
 }
 
 void write_sample_csv(const std::string& path, const Matrix& samples) {
-  write_text(path, sample_csv_string(samples));
+  save_bytes(path, sample_csv_string(samples));
 }
 
+// One pass over the file image: the header fixes the column count, every
+// non-empty line after it must carry exactly that many numbers that parse
+// completely (from_chars) -- else IO_FAILURE with the 1-based line number.
 Matrix read_sample_csv(const std::string& path) {
-  std::ifstream in(path, std::ios::binary);
-  if (!in) raise(ErrorCode::io_failure, "cannot open " + path);
-  std::string line;
-  if (!std::getline(in, line)) raise(ErrorCode::io_failure, path + ": missing header");
-  Index cols = 1;
-  for (char c : line)
-    if (c == ',') ++cols;
-  std::vector<double> data;
-  Index rows = 0;
-  while (std::getline(in, line)) {
-    if (line.empty()) continue;
-    std::stringstream ss(line);
-    std::string token;
-    Index seen = 0;
-    while (std::getline(ss, token, ',')) {
-      data.push_back(parse_double(token, path + " row " + std::to_string(rows)));
-      ++seen;
+  const std::string text = load_bytes(path);
+  const char* cur = text.data();
+  const char* const stop = cur + text.size();
+  const char* eol = static_cast<const char*>(std::memchr(cur, '\n', text.size()));
+  const char* header_end = eol ? eol : stop;
+  if (header_end == cur) raise(ErrorCode::io_failure, path + ": no header line");
+  const Index width = 1 + std::count(cur, header_end, ',');
+  cur = eol ? eol + 1 : stop;
+  std::vector<double> cells;
+  Index line_no = 1;
+  while (cur < stop) {
+    ++line_no;
+    const char* line_end = static_cast<const char*>(std::memchr(cur, '\n', stop - cur));
+    if (!line_end) line_end = stop;
+    if (line_end != cur) {
+      Index fields = 0;
+      const char* field = cur;
+      for (;;) {
+        const char* comma = std::find(field, line_end, ',');
+        double v = 0.0;
+        const auto r = std::from_chars(field, comma, v);
+        if (r.ec != std::errc{} || r.ptr != comma || field == comma)
+          raise(ErrorCode::io_failure, path + ":" + std::to_string(line_no) + ": '" +
+                                           std::string(field, comma) + "' is not a number");
+        cells.push_back(v);
+        ++fields;
+        if (comma == line_end) break;
+        field = comma + 1;
+      }
+      if (fields != width)
+        raise(ErrorCode::io_failure, path + ":" + std::to_string(line_no) + ": " +
+                                         std::to_string(fields) + " values where the header names " +
+                                         std::to_string(width) + " columns");
     }
-    if (seen != cols)
-      raise(ErrorCode::io_failure, path + ": row " + std::to_string(rows) + " has " +
-                                       std::to_string(seen) + " fields, header has " +
-                                       std::to_string(cols));
-    ++rows;
+    cur = line_end == stop ? stop : line_end + 1;
   }
-  Matrix out(rows, cols);
+  const Index rows = static_cast<Index>(cells.size()) / width;
+  Matrix out(rows, width);
   for (Index i = 0; i < rows; ++i)
-    for (Index j = 0; j < cols; ++j) out(i, j) = data[static_cast<size_t>(i * cols + j)];
+    for (Index j = 0; j < width; ++j) out(i, j) = cells[static_cast<size_t>(i * width + j)];
   return out;
 }
 
@@ -145,7 +185,7 @@ std::string manifest_string(const SampleSet& set, const std::string& polytope_so
 
 void write_manifest(const std::string& path, const SampleSet& set,
                     const std::string& polytope_source, const std::string& samples_path) {
-  write_text(path, manifest_string(set, polytope_source, samples_path));
+  save_bytes(path, manifest_string(set, polytope_source, samples_path));
 }
 
 void write_sample_bin(const std::string& path, const Matrix& samples) {
@@ -197,7 +237,7 @@ std::string bench_csv_string(const std::vector<BenchRecord>& records) {
 }
 
 void write_bench_csv(const std::string& path, const std::vector<BenchRecord>& records) {
-  write_text(path, bench_csv_string(records));
+  save_bytes(path, bench_csv_string(records));
 }
 
 std::string bench_json_string(const std::vector<BenchRecord>& records) {
@@ -231,7 +271,7 @@ std::string bench_json_string(const std::vector<BenchRecord>& records) {
 }
 
 void write_bench_json(const std::string& path, const std::vector<BenchRecord>& records) {
-  write_text(path, bench_json_string(records));
+  save_bytes(path, bench_json_string(records));
 }
 
 }  // namespace mhar

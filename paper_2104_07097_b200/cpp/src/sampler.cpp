@@ -4,7 +4,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../../include/mhar_b200.h"
 
@@ -109,6 +111,15 @@ class Engine {
   ~Engine() { mhar_ctx_destroy(ctx_); }
   mhar_ctx* ctx() { return ctx_; }
   double eps_dir() const { return eps_dir_; }
+  // What the context was built from (step() rebinds when any of it changes).
+  uint64_t fingerprint = 0;
+  // The reference streams continue across a rebind, as one WalkRng's do.
+  void take_streams_from(Engine& other, int z) {
+    std::vector<uint64_t> cols(static_cast<size_t>(z));
+    uint64_t theta = 0;
+    check(mhar_get_streams(other.ctx(), cols.data(), &theta));
+    check(mhar_set_streams(ctx_, cols.data(), &theta));
+  }
   long long redraws() {
     mhar_ctx_stats s;
     check(mhar_get_stats(ctx_, &s));
@@ -119,6 +130,50 @@ class Engine {
   mhar_ctx* ctx_ = nullptr;
   double eps_dir_ = 0.0;
 };
+
+namespace {
+// 64-bit content hash (four interleaved multiply-xorshift lanes over 8-byte
+// words, ~10 GB/s on one core): a polytope rebuilt at the same address with
+// other rows must not reuse the old device copy.
+uint64_t hash_words(const double* v, Index count, uint64_t h) {
+  uint64_t lane[4] = {h ^ 0x9E3779B97F4A7C15ULL, h + 0xBF58476D1CE4E5B9ULL,
+                      h ^ 0x94D049BB133111EBULL, h + 0x2545F4914F6CDD1DULL};
+  auto mix = [](uint64_t x) {
+    x ^= x >> 31;
+    x *= 0x7FB5D329728EA185ULL;
+    x ^= x >> 27;
+    x *= 0x81DADEF4BC2DD44DULL;
+    return x ^ (x >> 33);
+  };
+  Index i = 0;
+  uint64_t w[4];
+  for (; i + 4 <= count; i += 4) {
+    std::memcpy(w, v + i, sizeof(w));
+    for (int l = 0; l < 4; ++l) lane[l] = mix(lane[l] ^ w[l]) + 0x632BE59BD9B4E019ULL;
+  }
+  for (; i < count; ++i) {
+    std::memcpy(w, v + i, 8);
+    lane[0] = mix(lane[0] ^ w[0]);
+  }
+  return mix(lane[0] ^ mix(lane[1] ^ mix(lane[2] ^ mix(lane[3] ^ (uint64_t)count))));
+}
+
+uint64_t engine_fingerprint(const Polytope& p, const ProjectionOperator* projector,
+                            const SamplerConfig& cfg) {
+  uint64_t h = (uint64_t)p.dim() * 0x100000001B3ULL ^ (uint64_t)p.num_inequalities() << 20 ^
+               (uint64_t)p.num_equalities();
+  h = hash_words(p.a_in.data(), p.a_in.size(), h);
+  h = hash_words(p.b_in.data(), p.b_in.size(), h);
+  h = hash_words(p.a_eq.data(), p.a_eq.size(), h);
+  h = hash_words(p.b_eq.data(), p.b_eq.size(), h);
+  if (projector) {
+    h = hash_words(projector->p.data(), projector->p.size(), h ^ 0x5bd1e995ULL);
+    h = hash_words(projector->gram_inverse.data(), projector->gram_inverse.size(), h);
+  }
+  const double eps[2] = {cfg.eps_dir, cfg.eps_feas};
+  return hash_words(eps, 2, h);
+}
+}  // namespace
 
 // ---------------------------------------------------------------- sampler --
 SamplerConfig resolve(const SamplerConfig& cfg, const Polytope& p) {
@@ -215,10 +270,17 @@ void step(const Polytope& p, const ProjectionOperator* projector, const SamplerC
   if (state.x.cols() != rng.width() || state.x.rows() != p.dim())
     raise(ErrorCode::dimension_mismatch, "step: state does not match the rng width / polytope");
   // The walks' streams live with the device context: created on the first
-  // step for this polytope, reused while the caller keeps stepping it.
-  if (!rng.engine_ || rng.bound_ != &p || rng.engine_->eps_dir() != cfg.eps_dir) {
-    rng.engine_ = std::make_unique<Engine>(p, projector, rng.width(), rng.seed(), cfg.eps_dir,
-                                           cfg.eps_feas, MHAR_RNG_REFERENCE);
+  // step for this polytope, reused while the caller keeps stepping the same
+  // body (contents, projector and tolerances -- not just its address).  A
+  // rebind hands the streams over, so they continue exactly as one WalkRng's
+  // do in the reference (rng.hpp:42-55).
+  const uint64_t fp = engine_fingerprint(p, projector, cfg);
+  if (!rng.engine_ || rng.bound_ != &p || rng.engine_->fingerprint != fp) {
+    auto fresh = std::make_unique<Engine>(p, projector, rng.width(), rng.seed(), cfg.eps_dir,
+                                          cfg.eps_feas, MHAR_RNG_REFERENCE);
+    if (rng.engine_) fresh->take_streams_from(*rng.engine_, rng.width());
+    fresh->fingerprint = fp;
+    rng.engine_ = std::move(fresh);
     rng.bound_ = &p;
   }
   mhar_ctx* ctx = rng.engine_->ctx();

@@ -247,6 +247,52 @@ int main() {
     }
   });
 
+  run_case("a body rebuilt at the same address is sampled, not the old one", [] {
+    auto cfg = mhar::resolve(mhar::SamplerConfig{}, mhar::make_hypercube(3));
+    mhar::WalkRng rng(cfg.seed, 8);
+    mhar::WalkState state;
+    state.x = Matrix::Zero(3, 8);
+    mhar::Polytope body = mhar::make_hypercube(3);
+    for (int it = 0; it < 5; ++it) mhar::step(body, nullptr, cfg, rng, state);
+    // same object, same address, rows now bound the box at 1e-3
+    body = mhar::Polytope(mhar::make_hypercube(3).a_in, Vector::Constant(6, 1e-3));
+    state.x = Matrix::Zero(3, 8);
+    for (int it = 0; it < 5; ++it) mhar::step(body, nullptr, cfg, rng, state);
+    for (int k = 0; k < 8; ++k) CHECK(mhar::contains(body, state.x.col(k), 1e-15));
+    // and a changed eps_feas / projector also rebinds (no stale context)
+    cfg.eps_feas = 2e-9;
+    mhar::step(body, nullptr, cfg, rng, state);
+    for (int k = 0; k < 8; ++k) CHECK(mhar::contains(body, state.x.col(k), 1e-15));
+  });
+
+  run_case("streams continue across generate_directions and a rebind to the body", [] {
+    // the reference's WalkRng keeps its streams across calls: directions drawn
+    // before the first step are not replayed by it
+    const auto cube = mhar::make_hypercube(4);
+    const auto cfg = mhar::resolve(mhar::SamplerConfig{}, cube);
+    const int z = 5;
+    const uint64_t seed = 31;
+    mhar::WalkRng rng(seed, z);
+    const Matrix h = mhar::generate_directions(rng, 4);
+    mhar::WalkState state;
+    state.x = Matrix::Zero(4, z);
+    mhar::step(cube, nullptr, cfg, rng, state);
+    mhar::step(cube, nullptr, cfg, rng, state);
+    std::vector<uint64_t> cols(z);
+    for (int k = 0; k < z; ++k) cols[k] = orc_stream_init(seed, (uint64_t)k);
+    uint64_t th = orc_stream_init(seed, ~0ULL);
+    std::vector<double> hr(4 * z), xr(4 * z, 0.0);
+    orc_fill_standard_normal_matrix(cols.data(), z, hr.data(), 4);
+    for (int i = 0; i < 4 * z; ++i) CHECK(std::fabs(hr[i] - h.data()[i]) <= 1e-15);
+    int64_t red = 0, err = -1;
+    for (int it = 0; it < 2; ++it)
+      CHECK(orc_step(cube.a_in.data(), cube.b_in.data(), 8, 4, nullptr, cfg.eps_dir, cols.data(),
+                     &th, xr.data(), z, &red, &err) == 0);
+    double worst = 0.0;
+    for (int i = 0; i < 4 * z; ++i) worst = std::fmax(worst, std::fabs(xr[i] - state.x.data()[i]));
+    CHECK(worst <= 1e-14);
+  });
+
   run_case("format_double is the shortest round trip (io.hpp:13)", [] {
     CHECK(mhar::format_double(0.1) == "0.1");
     CHECK(mhar::format_double(2.0) == "2");
@@ -286,6 +332,22 @@ int main() {
     CHECK(slurp(dir + "/a.csv") == slurp(dir + "/b.csv"));
     CHECK(slurp(dir + "/a.csv").rfind("x1,x2,x3\n", 0) == 0);
     CHECK(mhar::read_sample_csv(dir + "/a.csv") == a.samples);
+    // test_io.cpp:94-108: ragged rows, bad tokens, a missing header, no file
+    auto bad_file = [&](const std::string& text) {
+      const std::string f = dir + "/bad.csv";
+      std::ofstream(f, std::ios::binary) << text;
+      expect_error(mhar::ErrorCode::io_failure, [&] { mhar::read_sample_csv(f); });
+    };
+    bad_file("x1,x2\n1,2\n3\n");
+    bad_file("x1,x2\n1,banana\n");
+    bad_file("x1,x2\n1,,2\n");
+    bad_file("");
+    expect_error(mhar::ErrorCode::io_failure, [&] { mhar::read_sample_csv(dir + "/none.csv"); });
+    {
+      std::ofstream(dir + "/empty_rows.csv", std::ios::binary) << "x1,x2\n1.5,-2\n\n3,4e-3";
+      const Matrix r = mhar::read_sample_csv(dir + "/empty_rows.csv");
+      CHECK(r.rows() == 2 && r.cols() == 2 && r(0, 0) == 1.5 && r(1, 1) == 4e-3);
+    }
     mhar::write_sample_bin(dir + "/a.bin", a.samples);
     CHECK(mhar::read_sample_bin(dir + "/a.bin") == a.samples);
     const std::string man = mhar::manifest_string(a, "hypercube:3", dir + "/a.csv");

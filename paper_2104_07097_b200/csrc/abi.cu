@@ -814,6 +814,13 @@ int read_error(mhar_ctx* c, int64_t* walk) {
   CK(cudaStreamSynchronize(c->stream));
   if (c->timing) harvest_timing(c);
   if (w == kNoError) return 0;
+  // The failing iterate may have written S_t / R_t (chord kernel) while theta
+  // and X stayed at t-1 (theta/axpy return early on the error word): the
+  // incremental cache no longer describes X, so the next pass refreshes it
+  // from a fresh product, and the captured graph (which assumes a valid
+  // cache) is dropped.
+  c->slack_valid = false;
+  drop_graph(c);
   const int status = (int)(w & 0xFF);
   const int64_t k = (int64_t)((w >> 8) & ((1ULL << 48) - 1));
   if (walk) *walk = k;
@@ -838,6 +845,20 @@ int read_error(mhar_ctx* c, int64_t* walk) {
 int clear_error(mhar_ctx* c) {
   CK(cudaMemsetAsync(c->err, 0xFF, sizeof(unsigned long long), c->stream));
   return 0;
+}
+
+// A caught device error (read_error) invalidated the slack cache there; an
+// error word cleared without being read (set_state after a failed step whose
+// status the caller ignored) must not leave a stale cache either.
+int clear_error_and_cache(mhar_ctx* c) {
+  unsigned long long w = kNoError;
+  CK(cudaMemcpyAsync(&w, c->err, sizeof(w), cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  if (w != kNoError) {
+    c->slack_valid = false;
+    drop_graph(c);
+  }
+  return clear_error(c);
 }
 
 int upload_state_host(mhar_ctx* c, const double* x_host, double* dst) {
@@ -1316,7 +1337,7 @@ int mhar_set_state(mhar_ctx* c, const double* x) {
   LAUNCH_OK(c, "differs_kernel");
   int differs = 1;
   CK(cudaMemcpyAsync(&differs, c->first_bad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
-  if ((s = clear_error(c))) return s;
+  if ((s = clear_error_and_cache(c))) return s;
   CK(cudaStreamSynchronize(c->stream));
   if (differs) {
     std::swap(c->X, c->Xtmp);
@@ -1382,6 +1403,36 @@ int mhar_set_iteration(mhar_ctx* c, int64_t iteration) {
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
   c->iterations = iteration;
+  return 0;
+}
+
+int mhar_get_streams(mhar_ctx* c, uint64_t* col_states, uint64_t* theta_state) {
+  if (!c || !col_states || !theta_state)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "get_streams: null argument");
+  if (c->opt.rng != MHAR_RNG_REFERENCE)
+    return fail(MHAR_ERR_INVALID_ARGUMENT,
+                "get_streams: Philox draws are keyed on the iterate counter (mhar_get_iteration)");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(col_states, c->col_state, sizeof(uint64_t) * c->z, cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaMemcpyAsync(theta_state, c->theta_state, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
+  return 0;
+}
+
+int mhar_set_streams(mhar_ctx* c, const uint64_t* col_states, const uint64_t* theta_state) {
+  if (!c || !col_states || !theta_state)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "set_streams: null argument");
+  if (c->opt.rng != MHAR_RNG_REFERENCE)
+    return fail(MHAR_ERR_INVALID_ARGUMENT,
+                "set_streams: Philox draws are keyed on the iterate counter (mhar_set_iteration)");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->col_state, col_states, sizeof(uint64_t) * c->z, cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaMemcpyAsync(c->theta_state, theta_state, sizeof(uint64_t), cudaMemcpyHostToDevice,
+                     c->stream));
+  CK(cudaStreamSynchronize(c->stream));
   return 0;
 }
 

@@ -75,22 +75,53 @@ def reduce_diagnostics(redraws: int, max_violation: float, max_eq: float, rows, 
 def gather_rows(local_rows, z_counts, dst: int = 0):
     """Gather every rank's (z_local x n) sample rows to rank `dst` in global
     walk order (rank-major = walk-id order, since shards are contiguous).
-    Uses all_gather (NCCL has no gather): ragged shards are padded to the
-    largest.  Returns the (sum z) x n tensor on dst, None elsewhere."""
+    A true gather: only `dst` receives (torch's NCCL gather is a grouped
+    ncclSend / ncclRecv; gloo has its own), so at 8 ranks and config 5 each
+    rank sends its 65.5 MB once instead of receiving 524 MB.  Ragged shards
+    are padded to the largest.  Returns the (sum z) x n tensor on dst, None
+    elsewhere."""
     import torch
     import torch.distributed as dist
     if not dist.is_initialized():
         return local_rows
     zmax = max(z_counts)
     n = local_rows.shape[1]
-    padded = torch.zeros((zmax, n), dtype=local_rows.dtype, device=local_rows.device)
-    padded[: local_rows.shape[0]] = local_rows
-    out = torch.empty((len(z_counts) * zmax, n), dtype=local_rows.dtype, device=local_rows.device)
-    dist.all_gather_into_tensor(out, padded)
-    if dist.get_rank() != dst:
+    if local_rows.shape[0] == zmax:
+        padded = local_rows.contiguous()
+    else:
+        padded = torch.zeros((zmax, n), dtype=local_rows.dtype, device=local_rows.device)
+        padded[: local_rows.shape[0]] = local_rows
+    rank = dist.get_rank()
+    bufs = None
+    if rank == dst:
+        bufs = [torch.empty((zmax, n), dtype=local_rows.dtype, device=local_rows.device)
+                for _ in z_counts]
+    dist.gather(padded, gather_list=bufs, dst=dst)
+    if rank != dst:
         return None
-    parts = [out[r * zmax: r * zmax + z] for r, z in enumerate(z_counts)]
-    return torch.cat(parts, 0)
+    return torch.cat([b[:z] for b, z in zip(bufs, z_counts)], 0)
+
+
+def first_failure(local_bad: int, offset: int, device=None) -> int:
+    """Global id of the lowest walk that failed containment on any rank, or
+    -1: the reference's run() raises NUMERICAL_FAILURE naming the first
+    failing walk (sampler.cpp:319-324), so every rank learns it."""
+    import torch
+    import torch.distributed as dist
+    big = float(2 ** 62)
+    v = float(local_bad + offset) if local_bad >= 0 else big
+    if not dist.is_initialized():
+        return -1 if v == big else int(v)
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    v = float(t.item())
+    return -1 if v == big else int(v)
+
+
+def _backend_is_device() -> bool:
+    """True when the process group's collectives take CUDA tensors (NCCL)."""
+    import torch.distributed as dist
+    return not dist.is_initialized() or dist.get_backend() != "gloo"
 
 
 class ShardedSampler:
@@ -117,16 +148,25 @@ class ShardedSampler:
         self.engine.set_state(X)
 
     def window(self, phi: int, reproject_every: int = 0, gather: bool = True):
-        """phi iterates on every rank, containment check, gather to rank 0."""
+        """phi iterates on every rank, containment check of every walk, gather
+        to rank 0.  Raises MharError(NUMERICAL_FAILURE) on every rank, naming
+        the lowest global walk outside the body, like the reference's run()
+        (sampler.cpp:319-324), before anything is gathered."""
         import torch
+        from . import ErrorCode, MharError
         self.engine.step(phi, reproject_every)
         bad, viol, eqv = self.engine.check_state(self.engine.eps_feas)
         rows = torch.empty((self.z, self.n), dtype=torch.float64, device=f"cuda:{self.device}")
         self.engine.state_rows_to_device(rows.data_ptr())
+        dev = rows.device if _backend_is_device() else "cpu"
+        failed = first_failure(bad, self.offset, device=dev)
+        if failed >= 0:
+            raise MharError(ErrorCode.numerical_failure,
+                            f"NUMERICAL_FAILURE: walk {failed} left the polytope at a collection")
         diag = reduce_diagnostics(self.engine.stats()["redraw_count"], float(viol.max()),
-                                  float(eqv.max()), rows, device=rows.device)
-        full = gather_rows(rows, self.z_counts) if gather else None
-        return full, diag, bad
+                                  float(eqv.max()), rows, device=dev)
+        full = gather_rows(rows if dev != "cpu" else rows.cpu(), self.z_counts) if gather else None
+        return full, diag
 
     def close(self):
         self.engine.close()

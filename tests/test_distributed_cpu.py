@@ -10,8 +10,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2104_07097_b200.distributed import gather_rows, max_over_ranks, reduce_diagnostics, \
-    shard_walks
+from paper_2104_07097_b200.distributed import first_failure, gather_rows, max_over_ranks, \
+    reduce_diagnostics, shard_walks
 
 
 def test_shard_walks_cover_exactly():
@@ -47,8 +47,11 @@ def _worker(rank, world, port, z_total, n, q):
         diag = reduce_diagnostics(redraws=rank + 1, max_violation=-1.0 - rank, max_eq=rank * 1e-12,
                                   rows=rows)
         t = max_over_ranks(1.5 + rank)
+        # containment failure: rank 1's local walk 2 is the only one outside
+        bad = first_failure(2 if rank == 1 else -1, off)
+        none = first_failure(-1, off)
         q.put((rank, None if full is None else full.numpy(), diag.redraws, diag.max_violation,
-               diag.max_eq_residual, diag.count, diag.coord_sum.tolist(), t))
+               diag.max_eq_residual, diag.count, diag.coord_sum.tolist(), t, bad, none, off))
     finally:
         dist.destroy_process_group()
 
@@ -74,7 +77,9 @@ def test_gather_and_reduce_world2(z_total):
     assert np.array_equal(full[:, 0], np.arange(z_total))
     assert res[1][1] is None
     for r in range(world):
-        _, _, red, mv, meq, cnt, csum, t = res[r]
+        _, _, red, mv, meq, cnt, csum, t, bad, none, _ = res[r]
         assert red == 3 and mv == -1.0 and meq == 1e-12 and cnt == z_total
         assert csum[0] == sum(range(z_total))
         assert t == 2.5
+        # every rank learns the global id of the failing walk (sampler.cpp:319-324)
+        assert bad == res[1][10] + 2 and none == -1

@@ -1,6 +1,6 @@
 """The multi-GPU plumbing through real NCCL on the one GPU a test box has:
-a world-size-1 process group runs the same collectives (all_gather of the
-collected rows device to device, all_reduce of the diagnostics, max of the
+a world-size-1 process group runs the same collectives (gather of the
+collected rows to rank 0 device to device, the containment-failure min, all_reduce of the diagnostics, max of the
 timers) the N-GPU bench runs, on rows the engine writes straight into device
 memory.  The multi-rank logic itself is covered on gloo
 (tests/test_distributed_cpu.py)."""
@@ -35,8 +35,8 @@ def test_nccl_window_gather_matches_the_engine():
         z = 300
         sh = ShardedSampler(p, z, seed=5)
         sh.set_start(np.zeros(40))
-        full, diag, bad = sh.window(12)
-        assert bad == -1 and diag.count == z and diag.max_violation <= 1e-9
+        full, diag = sh.window(12)
+        assert diag.count == z and diag.max_violation <= 1e-9
         got = full.cpu().numpy()
         sh.close()
         with mh.Engine(p, z, seed=5) as eng:

@@ -81,3 +81,41 @@ def test_all_rows_skipped_is_degenerate(orc, kw):
     w = hir - lor
     assert np.all(np.abs(lo - lor)[ok] <= tol * w[ok])
     assert np.all(np.abs(hi - hir)[ok] <= tol * w[ok])
+
+
+def _quadrant_path(slack, **kw):
+    # Half the directions are one-sided on the quadrant {x >= 0}
+    # (UNBOUNDED), so errors are frequent; after each, the caller hands back
+    # the unchanged state, as the reference's loop would (WalkState is
+    # untouched on a throw, sampler.cpp:235-272).
+    n, z = 2, 1
+    quadrant = mh.Polytope(-np.eye(n), np.zeros(n))
+    errors = 0
+    with mh.Engine(quadrant, z, seed=17, slack=slack, refresh_every=1000, small_path=False,
+                   **kw) as eng:
+        x = np.ones((n, z))
+        eng.set_state(x)
+        traj = []
+        for _ in range(60):
+            try:
+                eng.step(1)
+            except mh.MharError as e:
+                assert e.code == mh.ErrorCode.unbounded_polytope
+                errors += 1
+                eng.set_state(x)
+            x = eng.get_state()
+            assert x.min() >= -1e-12  # inside the quadrant
+            traj.append(x.copy())
+    assert 5 < errors < 55
+    return np.array(traj)
+
+
+@pytest.mark.parametrize("kw", [dict(), dict(f64_engine="int8")], ids=["dmma", "int8"])
+def test_caught_error_then_same_state_refreshes_the_slack_cache(kw):
+    # A failed iterate has already written the chord kernel's S_t / R_t while
+    # theta and X stayed at t-1: the incremental cache must not be reused
+    # when the same state comes back.  The incremental run equals
+    # the fresh-product (recompute) run.
+    ref = _quadrant_path("recompute")
+    got = _quadrant_path("incremental", **kw)
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)

@@ -424,3 +424,40 @@ def test_simplex_moments_and_drift(orc):
     st, S, _ = orc.run(A, b, np.full(8, 1 / 8), z=20, phi=50, t_target=500, burn_in=50,
                        reproject_every=50, seed=14, AE=AE, bE=bE)
     assert st == 0 and np.abs(S.sum(1) - 1.0).max() <= 1e-9
+
+
+def test_philox4x32_10_known_answers(orc):
+    # Philox4x32-10 (Salmon, Moraes, Dror, Shaw, SC'11): the authors'
+    # published known-answer vectors (Random123 kat_vectors, philox4x32 10
+    # rounds).  The engine's production-mode draws and oracle.step_philox
+    # rest on this function.
+    assert orc.philox4x32_10([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C,
+                                                       0x9B00DBD8]
+    assert orc.philox4x32_10([0xFFFFFFFF] * 4, [0xFFFFFFFF] * 2) == [0x408F276D, 0x41C83B0E,
+                                                                     0xA20BC7C6, 0x6D5451FD]
+    assert orc.philox4x32_10([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344],
+                             [0xA4093822, 0x299F31D0]) == [0xD16CFE09, 0x94FDCCEB, 0x5001E420,
+                                                           0x24126EA1]
+
+
+def test_philox_step_is_the_reference_step_on_philox_draws(orc):
+    # orc_step_philox == orc_step_injected fed the same Philox normals and
+    # the first theta draw (no redraws / rejections on this body): only the
+    # random source differs from the reference step
+    import numpy as np
+    from paper_2104_07097_b200 import workloads
+    p = workloads.random_polytope(9, 60, seed=3)
+    z, seed, off, it = 7, 5, 11, 3
+    X = np.zeros((9, z), order="F")
+    H = np.stack([orc.philox_normals(seed, off + k, it, 0, 9) for k in range(z)], 1)
+    import ctypes as C
+    U = np.empty(z)
+    for k in range(z):
+        a, b = C.c_uint64(), C.c_uint64()
+        orc.lib().orc_philox_u64x2(seed, 0, off + k, it, 0, 1, C.byref(a), C.byref(b))
+        U[k] = (a.value >> 11) * 2.0 ** -53
+    st, Xi, *_ = orc.step_injected(p.a_in, p.b_in, None, 1e-11, X, H, U)
+    Xp = X.copy(order="F")
+    st2, red, _ = orc.step_philox(p.a_in, p.b_in, None, 1e-11, seed, off, it, Xp)
+    assert st == 0 and st2 == 0 and red == 0
+    assert np.array_equal(Xi, Xp)
