@@ -46,7 +46,29 @@ def fp64_peak():
     return best
 
 
-NCU_FILE = os.path.join(ROOT, "profiles", "ncu_full_r01.json")
+def _latest_ncu_file():
+    """The newest committed `ncu --set full` summary (profiles/ncu_full_rNN.json)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_full_r*.json")))
+    return files[-1] if files else os.path.join(ROOT, "profiles", "ncu_full_r01.json")
+
+
+NCU_FILE = _latest_ncu_file()
+
+
+def ncu_source() -> str:
+    """Where roofline.traffic comes from: the capture file and, when it
+    records them, the capture date and the commit of the captured kernels
+    (traffic is not measured inside this run: ncu replays each kernel)."""
+    name = os.path.relpath(NCU_FILE, ROOT)
+    try:
+        with open(NCU_FILE) as f:
+            meta = json.load(f).get("_meta", {})
+    except (OSError, ValueError):
+        meta = {}
+    if meta:
+        return f"{name} (captured {meta.get('captured', '?')}, kernels at {meta.get('commit', '?')})"
+    return f"{name} (round-1 capture, kernels of that round)"
 
 
 def ncu_traffic(capture: str):
@@ -377,6 +399,43 @@ def run_sweep(args):
     return out
 
 
+def timed_cycle(eng, steps: int, reproject: int, refresh_every: int, incremental: bool,
+                world: int, clock_device=None):
+    """The timed region of one engine: a refresh pass (the fresh fused / A x
+    product that rebuilds the incremental slack cache) followed by steps - 1
+    incremental iterates, each part bracketed by CUDA events on the engine's
+    stream.  Returns the refresh-amortized device time per iterate,
+    (t_refresh + (R - 1) t_incremental) / R with R = refresh_every -- the
+    long-run cost of an iterate in a run() -- plus the per-part stats of the
+    chord kernels and the clocks sampled during the region."""
+    eng.request_refresh()
+    eng.reset_stats()
+    eng.set_timing(True)
+    barrier(world)
+    clk = ClockSampler(clock_device) if clock_device is not None else None
+    if clk:
+        clk.__enter__()
+    ms_ref = eng.step_timed(1, reproject)
+    s_ref = eng.stats()
+    eng.reset_stats()
+    ms_rest = eng.step_timed(max(steps - 1, 1), reproject)
+    if clk:
+        clk.__exit__(None, None, None)
+    eng.set_timing(False)
+    s_rest = eng.stats()
+    ms_ref = max_over_ranks(ms_ref, world)
+    ms_rest = max_over_ranks(ms_rest, world)
+    t_inc = ms_rest / max(steps - 1, 1)
+    if incremental:
+        amortized = (ms_ref + (refresh_every - 1) * t_inc) / refresh_every
+    else:
+        amortized = (ms_ref + ms_rest) / (1 + max(steps - 1, 1))
+    return {"ms_per_iterate": amortized, "ms_refresh": ms_ref, "ms_incremental": t_inc,
+            "ms_region": ms_ref + ms_rest, "stats_refresh": s_ref, "stats": s_rest,
+            "launches": s_ref["kernel_launches"] + s_rest["kernel_launches"],
+            "clocks": clk.summary() if clk else None}
+
+
 def run_engine(args, world, rank, local):
     import paper_2104_07097_b200 as mh
     from paper_2104_07097_b200 import workloads
@@ -396,50 +455,61 @@ def run_engine(args, world, rank, local):
     total_walks = args.strong if args.strong else z * world
     if offset is None:
         offset = rank * z
-    # the committed ncu captures (profiles/ncu_full_r01.json) are of this workload
+    # the committed ncu captures (NCU_FILE) are of this workload
     captured = args.config == 5 and z == 4096
+    traffic = {k: ncu_traffic(k) for k in ("chord2_full", "tc32_full", "i8_full")}
+    traffic_source = ncu_source()
     projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
     reproject = args.reproject if p.num_equalities() else 0
     eng = mh.Engine(p, z, seed=args.seed, projector=projector, slack=args.slack,
                     refresh_every=args.refresh, device=local, chain_offset=offset,
-                    precision=args.precision, f64_engine=args.f64_engine)
+                    precision=args.precision, f64_engine=args.f64_engine,
+                    fp32_direction=args.fp32_direction)
     X0 = np.zeros((p.dim(), z), order="F")
     X0[:] = w.x0[:, None]
     eng.set_state(X0)
 
     # warm-up; the first iterate after set_state is the fused refresh pass
     # (A_I [X | D] + slack cache), which recurs every --refresh iterates
-    ms_refresh = eng.step_timed(1, reproject)
-    eng.step_timed(args.warmup - 1, reproject)
+    eng.step_timed(args.warmup, reproject)
 
-    # timed, device-resident inputs
-    eng.reset_stats()
-    eng.set_timing(True)
-    barrier(world)
-    with ClockSampler(local) as clk:
-        ms = eng.step_timed(args.steps, reproject)
-    eng.set_timing(False)
-    st = eng.stats()
-    ms = max_over_ranks(ms, world)
-    value = total_walks * args.steps / (ms * 1e-3)
+    # timed, device-resident inputs: one refresh pass + K - 1 incremental
+    # iterates; value is the refresh-amortized rate
+    incremental = args.slack == "incremental"
+    cyc = timed_cycle(eng, args.steps, reproject, args.refresh, incremental, world, local)
+    st = cyc["stats"]
+    ms = cyc["ms_per_iterate"] * args.steps
+    value = total_walks / (cyc["ms_per_iterate"] * 1e-3)
 
     # e2e: the reference-facing call with HOST buffers every step, as the
     # reference's own loop `step(p, op, cfg, rng, state)` does: the walk state
-    # goes host -> device (pinned), one iterate, device -> host.
+    # goes host -> device (pinned), one iterate, device -> host.  Two forms:
+    # the caller hands back the state unchanged (the reference's loop; the
+    # slack cache survives) and the caller edits X before every step (each
+    # step then pays the refresh pass).
     import torch
     pinned = torch.empty((z, p.dim()), dtype=torch.float64, pin_memory=True).numpy()
     Xh = pinned.T  # (n, z) column-major view of pinned memory
     eng.get_state(out=Xh)
-    barrier(world)
-    t_e2e = []
-    for i in range(args.e2e_steps):
-        t0 = time.perf_counter()
-        eng.set_state(Xh)
-        eng.step(1, reproject)
-        eng.get_state(out=Xh)
-        t_e2e.append(time.perf_counter() - t0)
-    e2e_s = max_over_ranks(sum(t_e2e), world)
+
+    def e2e_loop(steps, mutate):
+        barrier(world)
+        t = 0.0
+        for i in range(steps):
+            if mutate:
+                Xh[0, :] *= 1.0 - 1e-12  # an edit the cache cannot survive
+            t0 = time.perf_counter()
+            eng.set_state(Xh)
+            eng.step(1, reproject)
+            eng.get_state(out=Xh)
+            t += time.perf_counter() - t0
+        return max_over_ranks(t, world)
+
+    e2e_s = e2e_loop(args.e2e_steps, False)
     e2e_value = total_walks * args.e2e_steps / e2e_s
+    e2e_mut_steps = max(3, args.e2e_steps // 4)
+    e2e_mut_s = e2e_loop(e2e_mut_steps, True)
+    e2e_mut_value = total_walks * e2e_mut_steps / e2e_mut_s
     bytes_state = p.dim() * z * 8
 
     # one collection window (outside the timed region): containment of every
@@ -469,11 +539,9 @@ def run_engine(args, world, rank, local):
                        device=local, chain_offset=rank * z, f64_engine="int8")
         e8.set_state(X0)
         e8.step_timed(args.warmup, reproject)
-        e8.reset_stats()
-        e8.set_timing(True)
-        barrier(world)
-        ms8 = max_over_ranks(e8.step_timed(args.steps, reproject), world)
-        s8 = e8.stats()
+        c8 = timed_cycle(e8, args.steps, reproject, args.refresh, True, world)
+        ms8 = c8["ms_per_iterate"] * args.steps
+        s8 = c8["stats"]
         bad8, viol8, _ = e8.check_state(e8.eps_feas)
         e8.close()
         alg8 = s8["chord_flops"] / max(s8["chord_ms"] * 1e-3, 1e-30) / 1e12
@@ -487,36 +555,49 @@ def run_engine(args, world, rank, local):
               "fp64_equivalent_tflops": alg8, "fp64_equivalent_frac_of_dmma_peak": alg8 / peak,
               "roofline": {"bound": "tensor", "achieved": ops8, "peak": i8_peak,
                            "unit": "TOPS (int8 executed)", "frac": ops8 / i8_peak,
-                           "traffic": ncu_traffic("i8_full") if captured else None,
+                           "traffic": traffic["i8_full"] if captured else None,
                            "peak_source": "tcgen05 kind::i8 microbench, profiles/tensor_probe_r01.jsonl"},
               "all_inside_eps_feas": bool(bad8 == -1)}
 
     # the north star's fp32 variant on the same workload (A_I rounded to fp32,
     # rates on tcgen05 tensor cores): same timing protocol, reported beside
-    fp32 = None
-    if args.precision == 64 and not args.no_fp32:
+    def fp32_line(direction):
+        """The north star's fp32 variant on the same workload, same timing
+        protocol.  direction "split": the walk moves along its fp64
+        direction, the tensor cores see it as two operands (3 MMAs per k
+        step); "rounded": the fast form, the direction rounded to one
+        operand and moved along (2 MMAs)."""
         e32 = mh.Engine(p, z, seed=args.seed, projector=projector, refresh_every=args.refresh,
-                        device=local, chain_offset=rank * z, precision=32)
+                        device=local, chain_offset=rank * z, precision=32,
+                        fp32_direction=direction)
         e32.set_state(X0)
         e32.step_timed(args.warmup, reproject)
-        e32.reset_stats()
-        e32.set_timing(True)
-        barrier(world)
-        ms32 = max_over_ranks(e32.step_timed(args.steps, reproject), world)
-        s32 = e32.stats()
+        c32 = timed_cycle(e32, args.steps, reproject, args.refresh, True, world)
+        s32 = c32["stats"]
         bad32, viol32, _ = e32.check_state(e32.eps_feas)
         e32.close()
-        tc_exec = 2.0 * s32["chord_flops"] / max(s32["chord_ms"] * 1e-3, 1e-30) / 1e12
+        mmas = 3.0 if (direction == "split" or p.num_equalities()) else 2.0
+        tc_exec = mmas * s32["chord_flops"] / max(s32["chord_ms"] * 1e-3, 1e-30) / 1e12
         tc_peak, tc_unit, tc_kernel, tc_dtype, tc_src = tc_roofline_terms()
-        fp32 = {"value": total_walks * args.steps / (ms32 * 1e-3), "unit": "chain-steps/s",
-                "ms_per_step": ms32 / args.steps, "form": tc_form(), "dtype": tc_dtype,
-                "kernel": tc_kernel,
+        return {"value": total_walks / (c32["ms_per_iterate"] * 1e-3), "unit": "chain-steps/s",
+                "ms_per_step": c32["ms_per_iterate"], "form": tc_form(), "direction": direction,
+                "dtype": tc_dtype + ("; direction split into two operands, walk moves along "
+                                     "its fp64 direction" if direction == "split" else
+                                     "; direction rounded to one operand and moved along"),
+                "kernel": tc_kernel, "mmas_per_kstep": mmas,
                 "roofline": {"bound": "tensor", "achieved": tc_exec, "peak": tc_peak,
                              "unit": tc_unit, "frac": tc_exec / tc_peak,
-                             "traffic": ncu_traffic("tc32_full") if captured else None,
+                             "traffic": traffic["tc32_full"] if captured else None,
                              "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
+                             "avg_launch_ms": s32["chord_ms"] / max(s32["chord_timed"], 1),
                              "peak_source": tc_src},
-                "all_inside_eps_feas": bool(bad32 == -1)}
+                "all_inside_eps_feas": bool(bad32 == -1),
+                "containment_body": "caller's fp64 A_I (fresh DMMA product)"}
+
+    fp32 = fp32r = None
+    if args.precision == 64 and not args.no_fp32:
+        fp32 = fp32_line("split")
+        fp32r = fp32_line("rounded")
 
     if rank != 0:
         return
@@ -550,24 +631,36 @@ def run_engine(args, world, rank, local):
                    "l2": "inputs larger than L2 (A_I is %.1f GB)" % (p.a_in.nbytes / 1e9)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None,
-                     "traffic": ncu_traffic("chord2_full") if captured else None,
-                     "traffic_unit": "GB DRAM read+write per launch (ncu --set full, "
-                                     "profiles/ncu_full_r01.json)",
+                     "traffic": traffic["chord2_full"] if captured else None,
+                     "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
+                     "traffic_source": traffic_source,
                      "algorithmic_bytes_GB": (p.a_in.nbytes + 4 * 8 * z * p.num_inequalities()
                                               + 8 * z * p.dim()) / 1e9,
-                     "kernel": "chord_kernel (DMMA A_I [X|D] / A_I D + fused chord reduce)",
+                     "kernel": "chord2_kernel<INCREMENTAL> (DMMA A_I D + streamed slack cache, "
+                               "fused chord reduce)",
                      "avg_launch_ms": chord_avg_ms, "launches": st["chord_timed"],
-                     "peak_source": "fp64 DMMA microbench, profiles/fp64_peaks_r01.json"},
+                     "peak_source": "fp64 DMMA microbench, profiles/fp64_peaks_r01.json",
+                     "peak_note": "builder-measured mma.sync.m8n8k4.f64 throughput on this pool's "
+                                  "B200 (MEASURED_PEAKS.json has no fp64 entry; cuBLAS DGEMM "
+                                  "reaches 35.5 TFLOP/s on the same box)"},
         "reference_equivalent_tflops": value * fpi / z / 1e12 / world,
-        "refresh": {"every": args.refresh, "ms": ms_refresh,
-                    "amortized_value": total_walks * args.refresh /
-                    ((ms / args.steps * (args.refresh - 1) + ms_refresh) * 1e-3),
-                    "note": "value is the steady incremental iterate; amortized_value adds one "
-                            "fused refresh pass per `every` iterates"},
+        "refresh": {"every": args.refresh, "ms_refresh_pass": cyc["ms_refresh"],
+                    "ms_incremental_iterate": cyc["ms_incremental"],
+                    "steady_value": total_walks / (cyc["ms_incremental"] * 1e-3),
+                    "note": "the timed region is one refresh pass + K-1 incremental iterates; "
+                            "value = walks / ((t_refresh + (every-1) t_incremental) / every), the "
+                            "long-run rate with one refresh per `every` iterates"},
         "e2e": {"value": e2e_value, "unit": "chain-steps/s", "h2d_bytes_per_step": bytes_state,
-                "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps},
-        "gpu_launches": st["kernel_launches"],
-        "clocks": clk.summary(),
+                "d2h_bytes_per_step": bytes_state, "steps": args.e2e_steps,
+                "note": "host state in, one iterate, host state out per step (the reference's "
+                        "step(p, op, cfg, rng, state) loop, state handed back unchanged)"},
+        "e2e_mutated": {"value": e2e_mut_value, "unit": "chain-steps/s",
+                        "h2d_bytes_per_step": bytes_state, "d2h_bytes_per_step": bytes_state,
+                        "steps": e2e_mut_steps,
+                        "note": "the host edits X before every step: each step pays the refresh "
+                                "pass"},
+        "gpu_launches": cyc["launches"],
+        "clocks": cyc["clocks"],
         "checks": {"walks_gathered_on_rank0": int(gathered.shape[0]),
                    "max_violation": diag.max_violation, "max_eq_residual": diag.max_eq_residual,
                    "all_inside_eps_feas": bool(diag.max_violation <= 1e-9 and
@@ -578,14 +671,17 @@ def run_engine(args, world, rank, local):
         line["cpu_baseline"] = cpu
     if fp32:
         line["fp32_variant"] = fp32
+    if fp32r:
+        line["fp32_variant_rounded_direction"] = fp32r
     if i8:
         line["fp64_int8_variant"] = i8
     if args.precision == 32:
         tc_peak, tc_unit, tc_kernel, tc_dtype, tc_src = tc_roofline_terms()
         line["dtype"] = "f32 rates (" + tc_dtype + ")"
-        line["roofline"].update({"achieved": 2.0 * achieved, "peak": tc_peak, "unit": tc_unit,
-                                 "frac": 2.0 * achieved / tc_peak, "kernel": tc_kernel,
-                                 "traffic": ncu_traffic("tc32_full") if captured else None,
+        mm = 3.0 if args.fp32_direction == "split" or p.num_equalities() else 2.0
+        line["roofline"].update({"achieved": mm * achieved, "peak": tc_peak, "unit": tc_unit,
+                                 "frac": mm * achieved / tc_peak, "kernel": tc_kernel,
+                                 "traffic": traffic["tc32_full"] if captured else None,
                                  "peak_source": tc_src})
     print(json.dumps(line), flush=True)
 
@@ -604,7 +700,7 @@ def main():
     ap.add_argument("--slack", default="incremental", choices=["incremental", "recompute"])
     ap.add_argument("--refresh", type=int, default=128)
     ap.add_argument("--reproject", type=int, default=1000)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-walks", type=int, default=256)
     ap.add_argument("--cpu-iters", type=int, default=24)
     ap.add_argument("--cpu-walks-1core", type=int, default=32)
@@ -618,6 +714,9 @@ def main():
                     help="comma-separated walk counts: padding sweep instead of the bench line")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 32],
                     help="32: the fp32 variant (tcgen05 3xTF32 rates, fp64 state)")
+    ap.add_argument("--fp32-direction", default="split", choices=["split", "rounded"],
+                    help="--precision 32: split (default, north-star parity) or rounded "
+                         "(fast form) direction")
     ap.add_argument("--paper", action="store_true",
                     help="run the paper's hypercube/simplex table (PAPER.md:845-887) instead")
     args = ap.parse_args()

@@ -100,14 +100,24 @@ typedef struct {
                             tcgen05 tensor cores with fp32 accuracy (kind::f16 with per-row /
                             per-walk power-of-two scales, A_I as two halves; MHAR_TC_F16=0:
                             kind::tf32 hi/lo split), fp64 slack/state, chords of
-                            {A_I x <= b_I - fp32_margin} */
+                            {A_I x <= b_I - fp32_margin}; the slack refresh and every
+                            containment check use the caller's fp64 A_I */
   double fp32_margin;    /* precision 32: slack margin mu (0 = default 2e-5) */
   int f64_engine;        /* precision 64 only.  MHAR_F64_DMMA (default): A_I d on the fp64
                             tensor cores (DMMA).  MHAR_F64_INT8: A_I d formed exactly from
                             53-bit fixed-point operands split into int8 slices on the
                             tcgen05 int8 tensor cores (Ozaki scheme, fp64-accurate rates,
                             n <= 4608); refreshes and containment checks stay on DMMA */
+  int fp32_direction;    /* precision 32 only.  MHAR_FP32_DIR_SPLIT (default): the walk moves
+                            along its fp64 direction; the tensor cores see it split into two
+                            operands (~22 bits).  MHAR_FP32_DIR_ROUNDED: the fast form -- the
+                            direction is rounded to one fp16 (per-walk scale) / TF32 operand
+                            and the walk moves along that rounded direction (one MMA fewer
+                            per k step); bodies with equalities always split */
 } mhar_options;
+
+#define MHAR_FP32_DIR_SPLIT 0
+#define MHAR_FP32_DIR_ROUNDED 1
 
 #define MHAR_F64_DMMA 0
 #define MHAR_F64_INT8 1
@@ -155,6 +165,10 @@ int mhar_sync(mhar_ctx* ctx);
  * streams carry per-walk state instead: INVALID_ARGUMENT there. */
 int mhar_get_iteration(mhar_ctx* ctx, int64_t* iteration);
 int mhar_set_iteration(mhar_ctx* ctx, int64_t iteration);
+/* Incremental slack mode: the next iterate recomputes the slack cache from a
+ * fresh product (the refresh pass that otherwise recurs every refresh_every
+ * iterates), e.g. to time a whole refresh cycle. */
+int mhar_request_refresh(mhar_ctx* ctx);
 /* WalkRng state (rng.hpp:42-55) of a reference-stream context: the z column
  * stream states and the shared theta stream state, exactly the uint64
  * counters RngStream holds (rng.hpp:16-33).  Moving them to another context

@@ -99,7 +99,7 @@ class _Options(C.Structure):
                 ("eps_dir", C.c_double), ("eps_feas", C.c_double), ("rng", C.c_int),
                 ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int),
                 ("small_path", C.c_int), ("precision", C.c_int), ("fp32_margin", C.c_double),
-                ("f64_engine", C.c_int)]
+                ("f64_engine", C.c_int), ("fp32_direction", C.c_int)]
 
 
 class _RunConfig(C.Structure):
@@ -135,6 +135,7 @@ EXPORTED_SYMBOLS = [
     "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
     "mhar_select_points", "mhar_chebyshev_center", "mhar_debug_last_iterate",
     "mhar_get_iteration", "mhar_set_iteration", "mhar_get_streams", "mhar_set_streams",
+    "mhar_request_refresh",
 ]
 
 
@@ -181,6 +182,8 @@ def lib():
     L.mhar_get_streams.restype = C.c_int
     L.mhar_set_streams.argtypes = [C.c_void_p, _u64p, _u64p]
     L.mhar_set_streams.restype = C.c_int
+    L.mhar_request_refresh.argtypes = [C.c_void_p]
+    L.mhar_request_refresh.restype = C.c_int
     L.mhar_debug_last_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
     L.mhar_debug_last_iterate.restype = C.c_int
     L.mhar_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -382,13 +385,18 @@ class Engine:
     (default, fp64 tensor cores) or "int8" (A_I d formed exactly from 53-bit
     fixed-point operands split into int8 slices on the tcgen05 int8 tensor
     cores -- the Ozaki scheme; n <= 4608; refreshes and checks stay DMMA).
+    fp32_direction (precision 32): "split" (default; the walk moves along its
+    fp64 direction, the tensor cores see it as two operands) or "rounded"
+    (the fast form: the direction is rounded to one operand and the walk
+    moves along the rounded direction).
     """
 
     def __init__(self, p: Polytope, z: int, seed: int = 0, projector: Optional[ProjectionOperator] = None,
                  eps_dir: float = 1e-11, eps_feas: float = 1e-9, rng: str = "philox",
                  slack: str = "incremental", refresh_every: int = 128, device: int = 0,
                  chain_offset: int = 0, small_path: bool = True, precision: int = 64,
-                 fp32_margin: float = 0.0, f64_engine: str = "dmma"):
+                 fp32_margin: float = 0.0, f64_engine: str = "dmma",
+                 fp32_direction: str = "split"):
         L = lib()
         self.p = p
         self.n = p.dim()
@@ -418,6 +426,7 @@ class Engine:
         opt.precision = int(precision)
         opt.fp32_margin = float(fp32_margin)
         opt.f64_engine = {"dmma": F64_DMMA, "int8": F64_INT8}[f64_engine]
+        opt.fp32_direction = {"split": 0, "rounded": 1}[fp32_direction]
         self.precision = int(precision)
         self.f64_engine = f64_engine
         self.rng = rng
@@ -474,6 +483,11 @@ class Engine:
 
     def sync(self):
         _check(lib().mhar_sync(self._h))
+
+    def request_refresh(self):
+        """The next iterate recomputes the incremental slack cache (the
+        refresh pass of every refresh_every iterates)."""
+        _check(lib().mhar_request_refresh(self._h))
 
     def step_timed(self, iters: int = 1, reproject_every: int = 0) -> float:
         """Iterates bracketed by CUDA events on the engine's stream; device ms."""

@@ -973,6 +973,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   if (opt->precision != 0 && opt->precision != 32 && opt->precision != 64)
     return fail(MHAR_ERR_INVALID_ARGUMENT, "options: precision must be 64 or 32");
 
+  if (opt->fp32_direction != MHAR_FP32_DIR_SPLIT && opt->fp32_direction != MHAR_FP32_DIR_ROUNDED)
+    return fail(MHAR_ERR_INVALID_ARGUMENT, "options: unknown fp32_direction");
   if (opt->f64_engine != MHAR_F64_DMMA && opt->f64_engine != MHAR_F64_INT8)
     return fail(MHAR_ERR_INVALID_ARGUMENT, "options: unknown f64_engine");
   if (opt->f64_engine == MHAR_F64_INT8 && opt->precision != 32 && round_up(p->n, I8_BK) > I8_MAX_K)
@@ -1117,8 +1119,14 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     if (fp32) {
       // A_I rounded to fp32 and split for 3xTF32; the fp64 copy becomes A_hi + A_lo
       const size_t an = (size_t)c->m_pad * c->n_pad, dn = (size_t)c->z_pad * c->n_pad;
+      // the direction reaches the tensor cores split d = d_hi + d_lo (default:
+      // the walk moves along its fp64 direction, the rates carry ~22 bits of
+      // it) or rounded to one operand (MHAR_FP32_DIR_ROUNDED, the fast form:
+      // the walk moves along the rounded direction); bodies with equalities
+      // always split, the rounded direction would leave the null space of A_E
+      const bool split_d = p->m_eq > 0 || opt->fp32_direction != MHAR_FP32_DIR_ROUNDED;
       if ((st = dalloc(c, &c->Ahi, an)) || (st = dalloc(c, &c->Alo, an)) ||
-          (st = dalloc(c, &c->Dhi, dn)) || (p->m_eq > 0 && (st = dalloc(c, &c->Dlo, dn)))) {
+          (st = dalloc(c, &c->Dhi, dn)) || (split_d && (st = dalloc(c, &c->Dlo, dn)))) {
         cudaFree(tmp);
         return bail(st);
       }
@@ -1130,11 +1138,11 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         }
         tc16_split_a_kernel<<<blocks_for(c->m_pad, 128, c->num_sms * 8), 128, 0, c->stream>>>(
             tmp, c->m, c->n, c->m_pad, c->tc_kt, reinterpret_cast<__half*>(c->Ahi),
-            reinterpret_cast<__half*>(c->Alo), c->tc_rsc, c->A, c->KT);
+            reinterpret_cast<__half*>(c->Alo), c->tc_rsc, nullptr, c->KT);
       } else {
         c->tc_kt = c->KT;
         tc_split_a_kernel<<<blocks_for(total, 256, c->num_sms * 32), 256, 0, c->stream>>>(
-            tmp, c->m, c->n, c->m_pad, c->KT, c->Ahi, c->Alo, c->A, c->KT);
+            tmp, c->m, c->n, c->m_pad, c->KT, c->Ahi, c->Alo, nullptr, c->KT);
       }
       ++c->launches;
       cudaMemsetAsync(c->Dhi, 0, dn * sizeof(float), c->stream);
@@ -1403,6 +1411,12 @@ int mhar_set_iteration(mhar_ctx* c, int64_t iteration) {
   CK(cudaSetDevice(c->device));
   CK(cudaStreamSynchronize(c->stream));
   c->iterations = iteration;
+  return 0;
+}
+
+int mhar_request_refresh(mhar_ctx* c) {
+  if (!c) return fail(MHAR_ERR_INVALID_ARGUMENT, "request_refresh: null context");
+  c->slack_valid = false;
   return 0;
 }
 

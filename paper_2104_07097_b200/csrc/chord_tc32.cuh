@@ -547,8 +547,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// fp64 polytope rows -> (A_hi, A_lo) with A_used = A_hi + A_lo written back
-// into the packed fp64 A (the fp32 variant's body is A rounded to fp32).
+// fp64 polytope rows -> (A_hi, A_lo); with Apk, A_used = A_hi + A_lo is also
+// written into a packed fp64 copy (a debugging aid: the engine keeps the
+// caller's A_I pristine for the slack refresh and containment).
 __global__ void tc_split_a_kernel(const double* __restrict__ Acm, int64_t m, int64_t n,
                                   int64_t m_pad, int64_t KT, float* __restrict__ Ahi,
                                   float* __restrict__ Alo, double* __restrict__ Apk,
@@ -563,7 +564,7 @@ __global__ void tc_split_a_kernel(const double* __restrict__ Acm, int64_t m, int
     const int64_t ti = tc_a_index(r, k, KT);
     Ahi[ti] = h;
     Alo[ti] = l;
-    if (r < m && k < n) Apk[a_index(r, k, KT64)] = (double)h + (double)l;
+    if (Apk && r < m && k < n) Apk[a_index(r, k, KT64)] = (double)h + (double)l;
   }
 }
 
@@ -605,8 +606,8 @@ __device__ inline __half tc16_half(double v) {
   return fabs((double)__half2float(h)) < 6.103515625e-05 ? __float2half(0.0f) : h;
 }
 
-// per-row exponents of A_I (column-major m x n), the split, and A_used back
-// into the packed fp64 copy: one thread per row
+// per-row exponents of A_I (column-major m x n) and the split (A_used into
+// Apk when given): one thread per row
 __global__ void tc16_split_a_kernel(const double* __restrict__ Acm, int64_t m, int64_t n,
                                     int64_t m_pad, int64_t KT16, __half* __restrict__ Ahi,
                                     __half* __restrict__ Alo, float* __restrict__ rsc,
@@ -626,7 +627,7 @@ __global__ void tc16_split_a_kernel(const double* __restrict__ Acm, int64_t m, i
       const int64_t ti = tc_a_index16(r, k, KT16);
       Ahi[ti] = h;
       Alo[ti] = l;
-      if (r < m && k < n)
+      if (Apk && r < m && k < n)
         Apk[a_index(r, k, KT64)] =
             ((double)__half2float(h) + (double)__half2float(l)) * ldexp(1.0, e - 14);
     }

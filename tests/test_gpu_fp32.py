@@ -1,8 +1,12 @@
-"""The fp32 variant (precision=32): A_I rounded to fp32, rates on tcgen05
-tensor cores in 3xTF32 (csrc/chord_tc32.cuh), fp64 slack/state, chords of
-{A x <= b - mu}.  North-star bar: one iterate within 1e-4 relative of the
-reference step on the same (fp32-rounded) body; every emitted sample exactly
-feasible; moments within Monte-Carlo error."""
+"""The fp32 variant (precision=32): the rates A_I d on tcgen05 tensor cores
+with fp32 accuracy (csrc/chord_tc32.cuh; kind::f16 with per-row / per-walk
+scales, or kind::tf32 under MHAR_TC_F16=0), fp64 slack/state from the
+caller's A_I, chords of {A x <= b - mu}.  North-star bar: one iterate within
+1e-4 relative of the reference step on the fp32 body with the injected
+direction; every emitted sample exactly inside the caller's body; moments
+within Monte-Carlo error.  The fast form (fp32_direction="rounded") moves
+along a rounded direction and is tested against the reference step with that
+direction."""
 import numpy as np
 import pytest
 
@@ -40,17 +44,6 @@ def _f16_split(x, axis):
     return h / s, (h + lo) / s
 
 
-def split_used(a, form="tf32"):
-    """The A_I the tensor cores see: tf32 hi + tf32 lo of fp32(a), or the
-    per-row-scaled half pair."""
-    if form == "f16":
-        return _f16_split(np.asarray(a, dtype=np.float64), 1)[1]
-    a32 = np.asarray(a, dtype=np.float32)
-    hi = _tf32(a32)
-    lo = _tf32((a32 - hi).astype(np.float32))
-    return hi.astype(np.float64) + lo.astype(np.float64)
-
-
 def dir_used(H, form="tf32"):
     """The direction moved along: TF32-rounded, or the per-walk-scaled half."""
     if form == "f16":
@@ -66,6 +59,11 @@ def _interior(p, z, rng, shrink=0.4):
 
 @pytest.mark.parametrize("n,m,z", [(16, 300, 128), (37, 1000, 200), (500, 20000, 256)])
 def test_fp32_injected_step_parity(orc, form, n, m, z):
+    # north star: one iterate within 1e-4 of the reference step on the same
+    # fp32 body with the injected (un-quantised) direction.  The default
+    # (split-direction) variant differs from the fp64 path only in the
+    # products A_I d (sampler.cpp:174-176): the walk moves along the fp64
+    # direction, the slack comes from the caller's A_I.
     p = workloads.random_polytope(n, m, seed=n)
     rng = np.random.default_rng(m)
     X = _interior(p, z, rng)
@@ -75,30 +73,61 @@ def test_fp32_injected_step_parity(orc, form, n, m, z):
         eng.set_state(X)
         lo, hi, th, fl = eng.step_injected(H, U)
         Xg = eng.get_state()
-    A_used = np.asfortranarray(split_used(p.a_in, form))
-    D_used = np.asfortranarray(dir_used(H, form))  # the direction moved along
-    st, Xr, lor, hir, thr, flr, _ = orc.step_injected(A_used, p.b_in, None, 1e-11, X, D_used, U)
+        bad, viol, _ = eng.check_state(0.0)  # fresh fp64 product on the caller's A_I
+    A32 = np.asfortranarray(np.asarray(p.a_in, dtype=np.float32).astype(np.float64))
+    st, Xr, lor, hir, thr, flr, _ = orc.step_injected(A32, p.b_in, None, 1e-11, X, H, U)
     assert st == 0
     assert np.array_equal(fl & mh.FLAG_DEGENERATE, flr & mh.FLAG_DEGENERATE)
     w = hir - lor
     assert np.all(np.abs(lo - lor) <= RTOL32 * w)
     assert np.all(np.abs(hi - hir) <= RTOL32 * w)
-    # the margin only ever shrinks the chord
-    assert np.all(hi <= hir + 1e-12 * w) and np.all(lo >= lor - 1e-12 * w)
+    assert np.all(np.abs(th - thr) <= RTOL32 * w)
     assert np.abs(Xg - Xr).max() <= RTOL32 * np.abs(Xr).max()
+    # every walk strictly inside the caller's body (not a perturbed copy)
+    assert bad == -1 and viol.max() < 0.0
+    assert (p.a_in @ Xg - p.b_in[:, None]).max() < 0.0
 
 
-def test_fp32_walks_stay_exactly_feasible(form):
+@pytest.mark.parametrize("n,m,z", [(16, 300, 128), (500, 20000, 256)])
+def test_fp32_rounded_direction_form(orc, form, n, m, z):
+    # the fast form (fp32_direction="rounded"): the direction is rounded to
+    # one operand and the walk moves along that rounded direction; against
+    # the reference step on the same body with that direction injected
+    p = workloads.random_polytope(n, m, seed=n)
+    rng = np.random.default_rng(m)
+    X = _interior(p, z, rng)
+    H = np.asfortranarray(rng.standard_normal((n, z)))
+    U = rng.uniform(0.05, 0.95, z)
+    with mh.Engine(p, z, precision=32, fp32_direction="rounded") as eng:
+        eng.set_state(X)
+        lo, hi, th, fl = eng.step_injected(H, U)
+        Xg = eng.get_state()
+        bad, viol, _ = eng.check_state(0.0)
+    D_used = np.asfortranarray(dir_used(H, form))  # the direction moved along
+    A32 = np.asfortranarray(np.asarray(p.a_in, dtype=np.float32).astype(np.float64))
+    st, Xr, lor, hir, thr, flr, _ = orc.step_injected(A32, p.b_in, None, 1e-11, X, D_used, U)
+    assert st == 0
+    w = hir - lor
+    assert np.all(np.abs(lo - lor) <= RTOL32 * w)
+    assert np.all(np.abs(hi - hir) <= RTOL32 * w)
+    # the margin only ever shrinks the chord (to fp32 accuracy of the rates)
+    assert np.all(hi <= hir + 1e-6 * w) and np.all(lo >= lor - 1e-6 * w)
+    assert np.abs(Xg - Xr).max() <= RTOL32 * np.abs(Xr).max()
+    assert bad == -1 and viol.max() < 0.0
+
+
+@pytest.mark.parametrize("direction", ["split", "rounded"])
+def test_fp32_walks_stay_exactly_feasible(form, direction):
     p = workloads.random_polytope(64, 4000, seed=3)
-    with mh.Engine(p, 256, seed=4, precision=32, refresh_every=64) as eng:
+    with mh.Engine(p, 256, seed=4, precision=32, refresh_every=64,
+                   fp32_direction=direction) as eng:
         eng.set_state(np.zeros((64, 256)))
         for _ in range(5):
             eng.step(60)
-            bad, viol, _ = eng.check_state(1e-9)   # fresh fp64 product on A_used
+            bad, viol, _ = eng.check_state(1e-9)   # fresh fp64 product on the caller's A_I
             assert bad == -1 and viol.max() <= 0.0
         X = eng.get_state()
-    A_used = split_used(p.a_in, form)
-    assert (A_used @ X - p.b_in[:, None]).max() <= 1e-9
+    assert (p.a_in @ X - p.b_in[:, None]).max() <= 0.0
     assert np.abs(X).max() > 0.1
 
 
