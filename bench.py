@@ -436,6 +436,56 @@ def timed_cycle(eng, steps: int, reproject: int, refresh_every: int, incremental
             "clocks": clk.summary() if clk else None}
 
 
+def run_group(args):
+    """--driver group: one process drives --gpus N devices through the C
+    ABI's multi-device group (mhar_group_*; one host thread and stream per
+    device, walks sharded by global id, windows gathered to device 0 over
+    NCCL).  Same workload per device as the torchrun path; the timed region
+    is a group step of K iterates bracketed by a host clock after a device
+    sync on every GPU (the group step returns only when all shards are done),
+    and the chord kernels' CUDA-event times per device are reported beside."""
+    import paper_2104_07097_b200 as mh
+    from paper_2104_07097_b200 import workloads
+    import torch
+    ndev = args.gpus
+    devices = list(range(ndev)) if torch.cuda.device_count() >= ndev else [0] * ndev
+    w = workloads.config(args.config, z=args.z)
+    p = w.polytope
+    z_total = w.z * ndev
+    projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
+    reproject = args.reproject if p.num_equalities() else 0
+    g = mh.Group(p, z_total, devices, seed=args.seed, projector=projector,
+                 refresh_every=args.refresh)
+    X0 = np.empty((p.dim(), z_total), order="F")
+    X0[:] = w.x0[:, None]
+    g.set_state(X0)
+    g.step(args.warmup, reproject)
+    t0 = time.perf_counter()
+    g.step(args.steps, reproject)
+    secs = time.perf_counter() - t0
+    value = z_total * args.steps / secs
+    # one collection window through run(): rows of every shard on device 0,
+    # then on the host (the samples of a window, 65.5 MB per shard at config 5)
+    t1 = time.perf_counter()
+    S, st = g.run(w.x0, phi=args.steps, windows=1, burn_in=0, reproject_every=reproject)
+    run_s = time.perf_counter() - t1
+    info = g.info()
+    g.close()
+    line = {"metric": METRIC, "value": value, "unit": "chain-steps/s", "n_gpus": ndev,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded unit-norm Gaussian rows, BASELINE config %d)" % args.config,
+            "config": {"workload": w.name, "walks_per_gpu": w.z, "walks_total": z_total,
+                       "driver": "mhar_group (one process, one thread per device)",
+                       "devices": devices, "uses_nccl": info["uses_nccl"]},
+            "timing": "host clock around a group step that synchronises every device",
+            "run_one_window": {"value": z_total * args.steps / run_s, "seconds": run_s,
+                               "samples_rows": int(S.shape[0]),
+                               "max_violation": info["last_max_violation"]}}
+    print(json.dumps(line), flush=True)
+
+
 def run_engine(args, world, rank, local):
     import paper_2104_07097_b200 as mh
     from paper_2104_07097_b200 import workloads
@@ -717,6 +767,9 @@ def main():
     ap.add_argument("--fp32-direction", default="split", choices=["split", "rounded"],
                     help="--precision 32: split (default, north-star parity) or rounded "
                          "(fast form) direction")
+    ap.add_argument("--driver", default="ranks", choices=["ranks", "group"],
+                    help="ranks: one process per GPU (torchrun); group: this process drives "
+                         "--gpus devices through the C ABI's mhar_group")
     ap.add_argument("--paper", action="store_true",
                     help="run the paper's hypercube/simplex table (PAPER.md:845-887) instead")
     args = ap.parse_args()
@@ -726,6 +779,9 @@ def main():
         # ranks exit 0 without work; no process group, no device touched
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")),
                       int(os.environ.get("RANK", "0")))
+        return
+    if args.driver == "group":
+        run_group(args)
         return
     world, rank, local = dist_setup(args)
     if args.paper:

@@ -29,7 +29,8 @@
  * status: MHAR_OK (0) or 1 + the reference ErrorCode ordinal; MHAR_ERR_CUDA
  * for a device/runtime failure, which the reference has no code for.
  * mhar_last_error() returns the thread-local message of the last failure.
- * A context is bound to one CUDA device and is not thread-safe.
+ * A context is bound to one CUDA device and is not thread-safe; a group
+ * (mhar_group_*) drives several devices from one process.
  */
 #ifndef MHAR_B200_H
 #define MHAR_B200_H
@@ -262,6 +263,54 @@ int mhar_reset_stats(mhar_ctx* ctx);
 /* Algorithmic flops of one iterate of this context's walks (4 m n z, + 2 n^2 z
  * with equalities) and of its dominant chord launch. */
 double mhar_flops_per_iterate(mhar_ctx* ctx);
+
+/* ---- several GPUs driven by one host process ---------
+ * run() / step() over z_total walks split into contiguous shards across
+ * `devices` (the first z_total % ndev shards one walk larger), A_I, b_I and
+ * P replicated on every device.  Walk k of the whole set draws on global id
+ * opt->chain_offset + k, so samples, states and errors are identical
+ * whatever the device list (Philox; the reference streams cannot be sharded:
+ * one theta stream is shared by every walk, rng.hpp:42-55, so ndev > 1 with
+ * MHAR_RNG_REFERENCE is INVALID_ARGUMENT).  One host thread per device
+ * issues its shard's iterates; nothing moves between GPUs per iterate.  At
+ * every collection window the shards' rows are gathered to devices[0] with
+ * grouped ncclSend / ncclRecv and the diagnostics (worst containment slack,
+ * redraw count) all-reduced with ncclAllReduce over NVLink; with one device,
+ * a device listed twice, or no libnccl.so.2, the gather is a peer copy into
+ * the root's window buffer (MHAR_GROUP_NCCL=0 forces that, =1 uses NCCL even
+ * for one device).  Replaces the single-process multi-GPU loop around
+ * mhar::run (sampler.cpp:274-335).  opt->z = z_total; opt->device ignored. */
+typedef struct mhar_group mhar_group;
+#define MHAR_GROUP_MAX_DEV 16
+typedef struct {
+  int ndev;
+  int uses_nccl;              /* 1: NCCL gather + all-reduce; 0: peer copies */
+  int64_t z_total;
+  int devices[MHAR_GROUP_MAX_DEV];
+  int64_t z[MHAR_GROUP_MAX_DEV];       /* walks per shard */
+  int64_t offset[MHAR_GROUP_MAX_DEV];  /* global id of each shard's first walk */
+  double last_max_violation;  /* max_k max_i (A x - b)_i of the last collection, all shards */
+  int64_t last_redraws;       /* redraw attempts of the last run, all shards */
+} mhar_group_info_t;
+
+int mhar_group_create(const mhar_polytope* p, const double* projector, const double* gram_inverse,
+                      const mhar_options* opt, const int* devices, int ndev, mhar_group** out);
+int mhar_group_destroy(mhar_group* g);
+int mhar_group_info(mhar_group* g, mhar_group_info_t* info);
+/* Shard i's single-device context (stats, timing); NULL when out of range. */
+mhar_ctx* mhar_group_context(mhar_group* g, int i);
+/* n x z_total column-major, like mhar_set_state / mhar_get_state. */
+int mhar_group_set_state(mhar_group* g, const double* x);
+int mhar_group_get_state(mhar_group* g, double* x);
+/* `iters` iterates of every walk on every device, then waits for all. */
+int mhar_group_step(mhar_group* g, int64_t iters, int64_t reproject_every);
+/* run() with warm start x0 over all shards; samples ((windows*z_total) x n
+ * row-major, collection order, walks in global order) assembled on
+ * devices[0] and streamed to the host overlapped with the next window.
+ * stats->seconds is host wall time of the whole run; err_walk the lowest
+ * failing global walk. */
+int mhar_group_run(mhar_group* g, const mhar_run_config* cfg, const double* x0, double* samples,
+                   mhar_run_stats* stats);
 
 /* ---- two-sample uniformity test ----------------------
  * minimum_spanning_tree (stats.hpp:31, stats.cpp:50-91): Prim over N points

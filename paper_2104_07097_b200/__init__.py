@@ -21,7 +21,7 @@ import numpy as np
 
 __all__ = [
     "MharError", "ErrorCode", "Polytope", "SamplerConfig", "ProjectionOperator", "SampleSet",
-    "LambdaIntervals", "Engine", "WalkState", "resolve", "compute_projection", "run", "step",
+    "LambdaIntervals", "Engine", "Group", "WalkState", "resolve", "compute_projection", "run", "step",
     "make_hypercube", "make_simplex", "contains", "library_path", "FLAG_DEGENERATE",
     "FLAG_HAS_UPPER", "FLAG_HAS_LOWER", "FLAG_COLLAPSED", "FLAG_THETA_MIDPOINT",
     "kDegenerateWidth", "kMaxDirectionRetries", "kNearZeroDirection",
@@ -135,7 +135,9 @@ EXPORTED_SYMBOLS = [
     "mhar_minimum_spanning_tree", "mhar_friedman_rafsky", "mhar_generate_directions",
     "mhar_select_points", "mhar_chebyshev_center", "mhar_debug_last_iterate",
     "mhar_get_iteration", "mhar_set_iteration", "mhar_get_streams", "mhar_set_streams",
-    "mhar_request_refresh",
+    "mhar_request_refresh", "mhar_group_create", "mhar_group_destroy", "mhar_group_info",
+    "mhar_group_context", "mhar_group_set_state", "mhar_group_get_state", "mhar_group_step",
+    "mhar_group_run",
 ]
 
 
@@ -143,6 +145,16 @@ class _FrResult(C.Structure):
     _fields_ = [("cross_edges", C.c_int64), ("expected_cross", C.c_double),
                 ("variance_cross", C.c_double), ("z_value", C.c_double),
                 ("shared_end_pairs", C.c_int64), ("pooled_size", C.c_int64)]
+
+MHAR_GROUP_MAX_DEV = 16
+
+
+class _GroupInfo(C.Structure):
+    _fields_ = [("ndev", C.c_int), ("uses_nccl", C.c_int), ("z_total", C.c_int64),
+                ("devices", C.c_int * MHAR_GROUP_MAX_DEV), ("z", C.c_int64 * MHAR_GROUP_MAX_DEV),
+                ("offset", C.c_int64 * MHAR_GROUP_MAX_DEV), ("last_max_violation", C.c_double),
+                ("last_redraws", C.c_int64)]
+
 
 class _LpStats(C.Structure):
     _fields_ = [("rounds", C.c_int32), ("reserved", C.c_int32), ("pivots", C.c_int64),
@@ -184,6 +196,24 @@ def lib():
     L.mhar_set_streams.restype = C.c_int
     L.mhar_request_refresh.argtypes = [C.c_void_p]
     L.mhar_request_refresh.restype = C.c_int
+    L.mhar_group_create.argtypes = [C.POINTER(_Polytope), _dp, _dp, C.POINTER(_Options),
+                                    C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_void_p)]
+    L.mhar_group_create.restype = C.c_int
+    L.mhar_group_destroy.argtypes = [C.c_void_p]
+    L.mhar_group_destroy.restype = C.c_int
+    L.mhar_group_info.argtypes = [C.c_void_p, C.POINTER(_GroupInfo)]
+    L.mhar_group_info.restype = C.c_int
+    L.mhar_group_context.argtypes = [C.c_void_p, C.c_int]
+    L.mhar_group_context.restype = C.c_void_p
+    L.mhar_group_set_state.argtypes = [C.c_void_p, _dp]
+    L.mhar_group_set_state.restype = C.c_int
+    L.mhar_group_get_state.argtypes = [C.c_void_p, _dp]
+    L.mhar_group_get_state.restype = C.c_int
+    L.mhar_group_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+    L.mhar_group_step.restype = C.c_int
+    L.mhar_group_run.argtypes = [C.c_void_p, C.POINTER(_RunConfig), _dp, _dp,
+                                 C.POINTER(_RunStats)]
+    L.mhar_group_run.restype = C.c_int
     L.mhar_debug_last_iterate.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
     L.mhar_debug_last_iterate.restype = C.c_int
     L.mhar_step.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
@@ -373,6 +403,43 @@ class SampleSet:
 
 # ------------------------------------------------------------- engine ------
 
+def _context_args(p, z, seed, projector, eps_dir, eps_feas, rng, slack, refresh_every, device,
+                  chain_offset, small_path, precision, fp32_margin, f64_engine, fp32_direction):
+    """(polytope struct, options struct, P, G) for mhar_ctx_create /
+    mhar_group_create; the returned arrays back the struct pointers."""
+    L = lib()
+    poly = _Polytope()
+    poly.n = p.dim()
+    poly.m_in = p.num_inequalities()
+    poly.m_eq = p.num_equalities()
+    poly.a_in = _d(p.a_in)
+    poly.b_in = _d(p.b_in)
+    if poly.m_eq > 0:
+        poly.a_eq = _d(p.a_eq)
+        poly.b_eq = _d(p.b_eq)
+    opt = _Options()
+    L.mhar_default_options(C.byref(opt))
+    opt.z = int(z)
+    opt.chain_offset = int(chain_offset)
+    opt.seed = int(seed) & (2**64 - 1)
+    opt.eps_dir = eps_dir
+    opt.eps_feas = eps_feas
+    opt.rng = {"philox": RNG_PHILOX, "reference": RNG_REFERENCE}[rng]
+    opt.slack_mode = {"recompute": SLACK_RECOMPUTE, "incremental": SLACK_INCREMENTAL}[slack]
+    opt.refresh_every = int(refresh_every)
+    opt.device = int(device)
+    opt.small_path = 1 if small_path else 0
+    opt.precision = int(precision)
+    opt.fp32_margin = float(fp32_margin)
+    opt.f64_engine = {"dmma": F64_DMMA, "int8": F64_INT8}[f64_engine]
+    opt.fp32_direction = {"split": 0, "rounded": 1}[fp32_direction]
+    P = G = None
+    if projector is not None:
+        P = _f(projector.p)
+        G = _f(projector.gram_inverse)
+    return poly, opt, P, G
+
+
 class Engine:
     """One device context: the polytope resident in HBM plus z walks.
 
@@ -402,42 +469,17 @@ class Engine:
         self.n = p.dim()
         self.z = int(z)
         self._keep = []
-        poly = _Polytope()
-        poly.n = self.n
-        poly.m_in = p.num_inequalities()
-        poly.m_eq = p.num_equalities()
-        poly.a_in = _d(p.a_in)
-        poly.b_in = _d(p.b_in)
-        if poly.m_eq > 0:
-            poly.a_eq = _d(p.a_eq)
-            poly.b_eq = _d(p.b_eq)
-        opt = _Options()
-        L.mhar_default_options(C.byref(opt))
-        opt.z = self.z
-        opt.chain_offset = int(chain_offset)
-        opt.seed = int(seed) & (2**64 - 1)
-        opt.eps_dir = eps_dir
-        opt.eps_feas = eps_feas
-        opt.rng = {"philox": RNG_PHILOX, "reference": RNG_REFERENCE}[rng]
-        opt.slack_mode = {"recompute": SLACK_RECOMPUTE, "incremental": SLACK_INCREMENTAL}[slack]
-        opt.refresh_every = int(refresh_every)
-        opt.device = int(device)
-        opt.small_path = 1 if small_path else 0
-        opt.precision = int(precision)
-        opt.fp32_margin = float(fp32_margin)
-        opt.f64_engine = {"dmma": F64_DMMA, "int8": F64_INT8}[f64_engine]
-        opt.fp32_direction = {"split": 0, "rounded": 1}[fp32_direction]
+        poly, opt, P, G = _context_args(p, z, seed, projector, eps_dir, eps_feas, rng, slack,
+                                        refresh_every, device, chain_offset, small_path,
+                                        precision, fp32_margin, f64_engine, fp32_direction)
         self.precision = int(precision)
         self.f64_engine = f64_engine
         self.rng = rng
-        P = G = None
-        if projector is not None:
-            P = _f(projector.p)
-            G = _f(projector.gram_inverse)
         h = C.c_void_p()
         _check(L.mhar_ctx_create(C.byref(poly), _d(P), _d(G), C.byref(opt), C.byref(h)))
         self._h = h
         self.eps_feas = eps_feas
+        self._args = (poly, P, G)  # keep the arrays the structs point to alive
 
     def close(self):
         if getattr(self, "_h", None):
@@ -617,6 +659,98 @@ class Engine:
 
     def flops_per_iterate(self) -> float:
         return lib().mhar_flops_per_iterate(self._h)
+
+
+class Group:
+    """Several GPUs driven from this process (mhar_group_*): z_total walks in
+    contiguous shards over `devices` keyed on their global ids (the samples
+    do not depend on the device list), the polytope replicated, one host
+    thread per device; collection windows gathered to devices[0] with NCCL
+    (peer copies when a device is listed twice or NCCL is absent)."""
+
+    def __init__(self, p: Polytope, z_total: int, devices, seed: int = 0,
+                 projector: Optional[ProjectionOperator] = None, eps_dir: float = 1e-11,
+                 eps_feas: float = 1e-9, slack: str = "incremental", refresh_every: int = 128,
+                 chain_offset: int = 0, small_path: bool = True, precision: int = 64,
+                 fp32_margin: float = 0.0, f64_engine: str = "dmma",
+                 fp32_direction: str = "split", rng: str = "philox"):
+        L = lib()
+        self.p = p
+        self.n = p.dim()
+        self.z = int(z_total)
+        self.devices = [int(d) for d in devices]
+        poly, opt, P, G = _context_args(p, z_total, seed, projector, eps_dir, eps_feas, rng,
+                                        slack, refresh_every, self.devices[0], chain_offset,
+                                        small_path, precision, fp32_margin, f64_engine,
+                                        fp32_direction)
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        _check(L.mhar_group_create(C.byref(poly), _d(P), _d(G), C.byref(opt), devs,
+                                   len(self.devices), C.byref(h)))
+        self._h = h
+        self._args = (poly, P, G)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().mhar_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def info(self) -> dict:
+        gi = _GroupInfo()
+        _check(lib().mhar_group_info(self._h, C.byref(gi)))
+        nd = gi.ndev
+        return {"ndev": nd, "uses_nccl": bool(gi.uses_nccl), "z_total": gi.z_total,
+                "devices": list(gi.devices[:nd]), "z": list(gi.z[:nd]),
+                "offset": list(gi.offset[:nd]), "last_max_violation": gi.last_max_violation,
+                "last_redraws": gi.last_redraws}
+
+    def set_state(self, x):
+        x = _f(x)
+        if x.shape != (self.n, self.z):
+            raise MharError(ErrorCode.dimension_mismatch,
+                            f"set_state: x is {x.shape}, expected {(self.n, self.z)}")
+        _check(lib().mhar_group_set_state(self._h, _d(x)))
+
+    def get_state(self) -> np.ndarray:
+        x = np.empty((self.n, self.z), order="F")
+        _check(lib().mhar_group_get_state(self._h, _d(x)))
+        return x
+
+    def step(self, iters: int = 1, reproject_every: int = 0):
+        _check(lib().mhar_group_step(self._h, int(iters), int(reproject_every)))
+
+    def run(self, x0, phi: int, windows: int, burn_in: int = 0, reproject_every: int = 0,
+            collect: bool = True):
+        x0 = np.ascontiguousarray(x0, dtype=np.float64)
+        if x0.shape != (self.n,):
+            raise MharError(ErrorCode.dimension_mismatch,
+                            f"run: x0 has shape {x0.shape}, expected ({self.n},)")
+        cfg = _RunConfig(int(phi), int(windows), int(burn_in), int(reproject_every))
+        samples = np.empty((windows * self.z, self.n)) if collect else None
+        st = _RunStats()
+        _check(lib().mhar_group_run(self._h, C.byref(cfg), _d(x0), _d(samples), C.byref(st)))
+        return samples, st
+
+    def context_stats(self, i: int) -> dict:
+        """Shard i's single-device counters (mhar_get_stats)."""
+        h = lib().mhar_group_context(self._h, int(i))
+        if not h:
+            raise MharError(ErrorCode.invalid_argument, f"group has no shard {i}")
+        s = _CtxStats()
+        _check(lib().mhar_get_stats(C.c_void_p(h), C.byref(s)))
+        return {f[0]: getattr(s, f[0]) for f in s._fields_}
 
 
 # ------------------------------------------------ reference-style calls ----

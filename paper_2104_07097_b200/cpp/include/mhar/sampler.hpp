@@ -241,9 +241,16 @@ inline constexpr double kMinInteriorRadius = 1e-10;
 ChebyshevCenter chebyshev_center(const Polytope& p);
 
 /// run() with a warm start x0 in place of the Chebyshev centre.  Samples are
-/// collected on the device.
+/// collected on the device.  One GPU and the reference's own streams, or --
+/// with MHAR_DEVICES="0,1,..." in the environment -- the devices overload.
 SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0,
               const ClockFn& clock = {});
+
+/// run() over several GPUs of this process (the C ABI's mhar_group): walks
+/// sharded by global id with Philox draws, so the samples are identical for
+/// every device list; windows gathered to devices[0] over NVLink (NCCL).
+SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0,
+              const std::vector<int>& devices, const ClockFn& clock = {});
 
 /// run() (sampler.hpp:93-97): starts every walk at the Chebyshev centre
 /// (sampler.cpp:276), computed before the clock starts.

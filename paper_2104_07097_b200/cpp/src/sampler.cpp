@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -294,7 +295,76 @@ void step(const Polytope& p, const ProjectionOperator* projector, const SamplerC
   ++state.j;
 }
 
+namespace {
+// MHAR_DEVICES="0,1,2,3": run() shards its walks over these GPUs.
+std::vector<int> devices_from_env() {
+  std::vector<int> out;
+  const char* e = std::getenv("MHAR_DEVICES");
+  if (!e) return out;
+  std::string s(e);
+  size_t pos = 0;
+  while (pos < s.size()) {
+    const size_t comma = s.find(',', pos);
+    const std::string tok = s.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+    if (!tok.empty()) out.push_back(std::atoi(tok.c_str()));
+    if (comma == std::string::npos) break;
+    pos = comma + 1;
+  }
+  return out;
+}
+}  // namespace
+
+SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0,
+              const std::vector<int>& devices, const ClockFn& clock) {
+  if (devices.empty()) raise(ErrorCode::invalid_argument, "run: empty device list");
+  const SamplerConfig rc = resolve(cfg, p);
+  if (x0.size() != p.dim()) raise(ErrorCode::dimension_mismatch, "run: x0 has the wrong size");
+  auto now = [&clock]() {
+    if (clock) return clock();
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+  };
+  const double t0 = now();
+  std::unique_ptr<ProjectionOperator> projector;
+  if (p.num_equalities() > 0)
+    projector = std::make_unique<ProjectionOperator>(compute_projection(p.a_eq));
+  const long long windows = (rc.t_target + rc.z - 1) / rc.z;
+  mhar_polytope poly{p.dim(), p.num_inequalities(), p.num_equalities(), p.a_in.data(),
+                     p.b_in.data(), p.num_equalities() ? p.a_eq.data() : nullptr,
+                     p.num_equalities() ? p.b_eq.data() : nullptr};
+  mhar_options opt;
+  mhar_default_options(&opt);
+  opt.z = rc.z;
+  opt.seed = rc.seed;
+  opt.eps_dir = rc.eps_dir;
+  opt.eps_feas = rc.eps_feas;
+  opt.rng = MHAR_RNG_PHILOX;  // walks keyed on global ids: shardable
+  mhar_group* g = nullptr;
+  check(mhar_group_create(&poly, projector ? projector->p.data() : nullptr,
+                          projector ? projector->gram_inverse.data() : nullptr, &opt,
+                          devices.data(), static_cast<int>(devices.size()), &g));
+  std::unique_ptr<mhar_group, int (*)(mhar_group*)> guard(g, mhar_group_destroy);
+  SampleSet out;
+  out.config = rc;
+  out.start = x0;
+  out.windows = windows;
+  out.samples = Matrix(windows * rc.z, p.dim());
+  std::vector<double> rows(static_cast<size_t>(windows * rc.z * p.dim()));
+  mhar_run_config rcfg{rc.phi, windows, rc.burn_in, projector ? rc.reproject_every : 0};
+  mhar_run_stats stats;
+  check(mhar_group_run(g, &rcfg, x0.data(), rows.data(), &stats));
+  const Index n = p.dim();
+  for (Index r = 0; r < windows * rc.z; ++r)
+    for (Index j = 0; j < n; ++j) out.samples(r, j) = rows[static_cast<size_t>(r * n + j)];
+  out.seconds = now() - t0;
+  out.iterate_count = stats.iterate_count;
+  out.redraw_count = stats.redraw_count;
+  return out;
+}
+
 SampleSet run(const Polytope& p, const SamplerConfig& cfg, const Vector& x0, const ClockFn& clock) {
+  const std::vector<int> devices = devices_from_env();
+  if (!devices.empty()) return run(p, cfg, x0, devices, clock);
   const SamplerConfig rc = resolve(cfg, p);
   if (x0.size() != p.dim()) raise(ErrorCode::dimension_mismatch, "run: x0 has the wrong size");
   auto now = [&clock]() {

@@ -162,6 +162,32 @@ int main() {
     CHECK(centred.samples == out.samples);
   });
 
+  run_case("multi-GPU run: samples identical for every device list (mhar_group)", [] {
+    const auto simplex = mhar::make_simplex(12);
+    mhar::SamplerConfig cfg;
+    cfg.z = 65;
+    cfg.phi = 9;
+    cfg.t_target = 65 * 3;
+    cfg.seed = 5;
+    const Vector x0 = Vector::Constant(12, 1.0 / 12);
+    const auto one = mhar::run(simplex, cfg, x0, std::vector<int>{0});
+    const auto three = mhar::run(simplex, cfg, x0, std::vector<int>{0, 0, 0});
+    CHECK(one.samples.rows() == 195 && one.windows == 3 && one.iterate_count == 65 * 9 * 3);
+    CHECK(one.samples == three.samples);
+    for (int r = 0; r < 195; ++r) {
+      double s = 0.0;
+      for (int j = 0; j < 12; ++j) s += one.samples(r, j);
+      CHECK(std::fabs(s - 1.0) <= 1e-9);
+    }
+    // the reference-facing overload takes the device list from MHAR_DEVICES
+    setenv("MHAR_DEVICES", "0,0", 1);
+    const auto env = mhar::run(simplex, cfg, x0);
+    unsetenv("MHAR_DEVICES");
+    CHECK(env.samples == one.samples);
+    expect_error(mhar::ErrorCode::invalid_argument,
+                 [&] { mhar::run(simplex, cfg, x0, std::vector<int>{}); });
+  });
+
   run_case("chebyshev centres: box exact, simplex barycentre, errors", [] {
     for (int n : {2, 10, 100}) {
       const auto c = mhar::chebyshev_center(mhar::make_hypercube(n));

@@ -22,6 +22,7 @@
 
 #include "../../include/mhar_b200.h"
 #include "chord_kernel.cuh"
+#include "engine_internal.h"
 #include "host_linalg.h"
 #include "lp.h"
 #include "step_kernels.cuh"
@@ -1947,3 +1948,67 @@ double mhar_flops_per_iterate(mhar_ctx* c) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Asynchronous building blocks of one context for the multi-device group
+// (engine_internal.h, group.cu).
+namespace mhar_internal {
+
+int device(const mhar_ctx* c) { return c->device; }
+cudaStream_t stream(const mhar_ctx* c) { return c->stream; }
+int64_t walks(const mhar_ctx* c) { return c->z; }
+int64_t dim(const mhar_ctx* c) { return c->n; }
+unsigned long long* redraw_counter(mhar_ctx* c) { return c->redraw_total; }
+std::string last_error() { return g_last_error; }
+int set_error(int code, const std::string& msg) { return fail(code, msg); }
+
+int run_begin(mhar_ctx* c, const double* x0) {
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->x0, x0, sizeof(double) * c->n, cudaMemcpyHostToDevice, c->stream));
+  const int64_t total = c->z_pad * c->KT * BK;
+  broadcast_state_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+      c->x0, c->n, c->z, c->z_pad, c->KT, c->X);
+  LAUNCH_OK(c, "broadcast_state_kernel");
+  int s = clear_error(c);
+  if (s) return s;
+  CK(cudaMemsetAsync(c->redraw_total, 0, sizeof(unsigned long long), c->stream));
+  c->slack_valid = false;
+  c->iterations = 0;
+  return reset_streams(c);  // synchronises (x0 is the caller's host memory)
+}
+
+int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
+  CK(cudaSetDevice(c->device));
+  return ::advance(c, iters, reproject_every);
+}
+
+int collect(mhar_ctx* c, double* dev_rows, double* dev_viol) {
+  CK(cudaSetDevice(c->device));
+  int s = enqueue_check(c);
+  if (s) return s;
+  CK(cudaMemsetAsync(c->first_bad, 0x7F, sizeof(int), c->stream));
+  contains_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(
+      c->viol, c->me > 0 ? c->eqviol : nullptr, c->z, c->opt.eps_feas, c->err, 1, c->first_bad);
+  LAUNCH_OK(c, "contains_kernel");
+  if (dev_viol) {
+    worst_violation_kernel<<<1, 1024, 0, c->stream>>>(c->viol, c->me > 0 ? c->eqviol : nullptr,
+                                                      c->z, dev_viol);
+    LAUNCH_OK(c, "worst_violation_kernel");
+  }
+  if (dev_rows) {
+    unpack_b_kernel<<<blocks_for(c->n * c->z, 256, c->num_sms * 16), 256, 0, c->stream>>>(
+        c->X, c->n, c->z, c->KT, dev_rows);
+    LAUNCH_OK(c, "unpack_b_kernel");
+  }
+  return 0;
+}
+
+int finish(mhar_ctx* c, int64_t* walk) {
+  CK(cudaSetDevice(c->device));
+  int64_t k = -1;
+  const int s = read_error(c, &k);
+  if (walk) *walk = s ? k + c->opt.chain_offset : -1;
+  return s;
+}
+
+}  // namespace mhar_internal

@@ -649,6 +649,26 @@ __global__ void contains_kernel(const double* __restrict__ viol, const double* _
   }
 }
 
+// worst containment slack of a collection: max over walks of
+// max(viol[c], eqv[c]) into *out (one block)
+__global__ void worst_violation_kernel(const double* __restrict__ viol,
+                                       const double* __restrict__ eqv, int64_t z, double* out) {
+  __shared__ double red[32];
+  double v = -INFINITY;
+  for (int64_t c = threadIdx.x; c < z; c += blockDim.x) {
+    v = fmax(v, viol[c]);
+    if (eqv) v = fmax(v, eqv[c]);
+  }
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : -INFINITY;
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    if (threadIdx.x == 0) *out = v;
+  }
+}
+
 // the device copy of the iterate counter (CUDA-graph replays of an iterate)
 __global__ void iter_set_kernel(unsigned long long* it, unsigned long long v) { *it = v; }
 __global__ void iter_inc_kernel(unsigned long long* it) { *it += 1ull; }

@@ -1,0 +1,114 @@
+"""Several devices behind the C ABI (mhar_group_*, csrc/group.cu): one host
+process, one thread and stream per device, walks sharded by global id, the
+collection windows gathered to devices[0].
+
+A test box has one GPU, so the multi-device logic runs with a device listed
+several times (every shard a separate context on GPU 0, the peer-copy
+gather) and the NCCL gather / all-reduce at world size 1
+(MHAR_GROUP_NCCL=1).  The bar: bit-identical to one context over all walks
+-- the sample set of the reference's run() (sampler.cpp:274-335) does not
+depend on how the walks are placed."""
+import numpy as np
+import pytest
+
+import paper_2104_07097_b200 as mh
+from paper_2104_07097_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+def _single(p, z, seed, steps, op=None, reproject=0, **kw):
+    with mh.Engine(p, z, seed=seed, projector=op, **kw) as eng:
+        eng.set_state(np.zeros((p.dim(), z)) if op is None else
+                      np.repeat(np.full((p.dim(), 1), 1.0 / p.dim()), z, 1))
+        eng.step(steps, reproject)
+        return eng.get_state()
+
+
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_group_step_equals_one_context(devices):
+    p = workloads.random_polytope(40, 900, seed=4)
+    z, seed = 301, 21  # ragged shards: 301 = 151 + 150, 101 + 100 + 100
+    ref = _single(p, z, seed, 12)
+    with mh.Group(p, z, devices, seed=seed) as g:
+        info = g.info()
+        assert info["ndev"] == len(devices) and sum(info["z"]) == z
+        assert info["offset"][0] == 0 and not info["uses_nccl"]
+        g.set_state(np.zeros((40, z)))
+        g.step(12)
+        got = g.get_state()
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0, 0]])
+def test_group_run_equals_one_context_with_equalities(devices):
+    # simplex with a collapsing-free projected walk and the reprojection
+    # cadence; samples in global walk order, every window
+    p = mh.make_simplex(30)
+    op = mh.compute_projection(p.a_eq)
+    z, seed = 203, 8
+    x0 = np.full(30, 1.0 / 30)
+    with mh.Engine(p, z, seed=seed, projector=op) as eng:
+        ref, rst = eng.run(x0, phi=7, windows=5, burn_in=10, reproject_every=7)
+    with mh.Group(p, z, devices, seed=seed, projector=op) as g:
+        got, st = g.run(x0, phi=7, windows=5, burn_in=10, reproject_every=7)
+        info = g.info()
+    assert np.array_equal(got, ref)
+    assert st.iterate_count == rst.iterate_count == z * 7 * 5
+    assert st.redraw_count == rst.redraw_count
+    assert info["last_max_violation"] <= 1e-9
+
+
+def test_group_run_large_body_multikernel_path():
+    # the tensor-core chord path (incremental slack, refresh cadence) per shard
+    p = workloads.random_polytope(300, 6000, seed=5)
+    z, seed = 512, 3
+    x0 = np.zeros(300)
+    with mh.Engine(p, z, seed=seed, refresh_every=16) as eng:
+        ref, _ = eng.run(x0, phi=20, windows=3)
+    with mh.Group(p, z, [0, 0], seed=seed, refresh_every=16) as g:
+        got, st = g.run(x0, phi=20, windows=3)
+        assert g.context_stats(0)["chord_launches"] > 0
+    assert np.array_equal(got, ref)
+
+
+def test_group_nccl_gather_at_world_one(monkeypatch):
+    # the NCCL path (grouped send/recv gather + all-reduce of diagnostics)
+    # through real NCCL on the one GPU
+    monkeypatch.setenv("MHAR_GROUP_NCCL", "1")
+    p = workloads.random_polytope(24, 400, seed=9)
+    z, seed = 130, 4
+    x0 = np.zeros(24)
+    with mh.Engine(p, z, seed=seed) as eng:
+        ref, rst = eng.run(x0, phi=9, windows=4)
+    with mh.Group(p, z, [0], seed=seed) as g:
+        assert g.info()["uses_nccl"]
+        got, st = g.run(x0, phi=9, windows=4)
+        info = g.info()
+    assert np.array_equal(got, ref)
+    assert info["last_redraws"] == rst.redraw_count
+    assert info["last_max_violation"] <= 1e-9
+
+
+def test_group_errors():
+    p = workloads.random_polytope(10, 60, seed=1)
+    with pytest.raises(mh.MharError) as e:
+        mh.Group(p, 64, [0, 0], rng="reference")
+    assert e.value.code == mh.ErrorCode.invalid_argument
+    with pytest.raises(mh.MharError) as e:
+        mh.Group(p, 1, [0, 0])
+    assert e.value.code == mh.ErrorCode.invalid_argument
+    with pytest.raises(mh.MharError):
+        mh.Group(p, 64, [0, 999])
+    # a device-side failure on a shard surfaces with the walk's global id
+    quadrant = mh.Polytope(-np.eye(2), np.zeros(2))
+    with mh.Group(quadrant, 40, [0, 0], seed=1, small_path=False) as g:
+        g.set_state(np.ones((2, 40)))
+        with pytest.raises(mh.MharError) as e:
+            g.step(1)
+    assert e.value.code == mh.ErrorCode.unbounded_polytope
+    with mh.Engine(quadrant, 40, seed=1, small_path=False) as eng:
+        eng.set_state(np.ones((2, 40)))
+        with pytest.raises(mh.MharError) as e1:
+            eng.step(1)
+    assert str(e.value) == str(e1.value)
