@@ -55,6 +55,9 @@ struct Ctl {
   int pad;
 };
 
+// Free columns (colfree[j] != 0, native free variables): priced by |d_j| and
+// entered in the direction of sign(d_j); once basic they never leave (their
+// rows are skipped by the ratio test).
 __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restrict__ T,
                                                           const double* __restrict__ b,
                                                           const double* __restrict__ cost,
@@ -62,7 +65,10 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
                                                           int cols, int limit_col, Ctl* ctl,
                                                           int* out /* entering, leaving */,
                                                           double* prow, double* fcol,
-                                                          double* pb /* [b_row/piv, cost_col] */) {
+                                                          double* pb /* [b_row/piv, cost_col,
+                                                                        leaving col, piv] */,
+                                                          const int* __restrict__ colfree,
+                                                          double* wbase, int wmode) {
   static_assert(kThreads == 1024, "one reduction partial per lane of warp 0");
   __shared__ double sv[kThreads / 32];
   __shared__ int si[kThreads / 32], sb[kThreads / 32];
@@ -80,18 +86,38 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
     return;
   }
   const int bland = ctl->bland;
-  // pricing
-  double bv = bland ? 0.0 : kReducedCostTol;
+  // wmode 1: Devex reference weights in wbase; 2: exact steepest edge, the
+  // squared tableau column norms accumulated by the previous pivot's update
+  // in wbase[(npiv & 1) * cols]; the other half is cleared for this pivot's
+  const double* dvx = nullptr;
+  double wadd = 0.0;
+  if (wmode == 1) dvx = wbase;
+  if (wmode == 2) {
+    const long long k = ctl->npiv;
+    dvx = wbase + (size_t)(k & 1) * cols;
+    double* nxt = wbase + (size_t)((k + 1) & 1) * cols;
+    for (int j = tid; j < cols; j += kThreads) nxt[j] = 0.0;
+    wadd = 1.0;  // gamma_j = 1 + |B^-1 a_j|^2
+  }
+  // pricing: Dantzig (largest reduced cost) or, with reference weights dvx,
+  // Devex (largest d_j^2 / w_j: an approximate steepest edge, far fewer
+  // pivots on the degenerate centring LP); Bland after a stall
+  double bv = -1.0;
   int bi = 0x7FFFFFFF;
   // (loops unrolled so each thread has its loads in flight together: this
   // single-CTA kernel is latency-bound)
 #pragma unroll 8
   for (int j = tid; j < limit_col; j += kThreads) {
-    const double c = cost[j];
+    double c = cost[j];
+    if (colfree && colfree[j]) c = fabs(c);
+    if (!(c > kReducedCostTol)) continue;
     if (bland) {
-      if (c > kReducedCostTol && j < bi) bi = j;
-    } else if (c > bv || (c == bv && c > kReducedCostTol && j < bi)) {
-      bv = c;
+      if (j < bi) bi = j;
+      continue;
+    }
+    const double sc = dvx ? c * c / (wadd + dvx[j]) : c;
+    if (sc > bv || (sc == bv && j < bi)) {
+      bv = sc;
       bi = j;
     }
   }
@@ -131,6 +157,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
   __syncthreads();
   const int e = s_enter;
   if (e < 0) return;
+  // a free column with a negative reduced cost enters decreasing
+  const double dir = (colfree && colfree[e] && cost[e] < 0.0) ? -1.0 : 1.0;
   // ratio test, pass 1: minimum ratio; the entering column (one strided
   // sector per row) is cached in fcol for the rank-1 update, and the first
   // kRegRows rows per thread keep their ratios in registers for pass 2
@@ -142,18 +170,20 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
     const int i = tid + q * kThreads;
     ra[q] = kInf;
     if (i < rows) {
-      const double a = T[(size_t)i * cols + e];
-      fcol[i] = a;
-      if (a > kPivotTol) {
+      const double t = T[(size_t)i * cols + e];
+      fcol[i] = t;
+      const double a = dir * t;
+      if (a > kPivotTol && !(colfree && colfree[basis[i]])) {
         ra[q] = b[i] / a;
         mr = fmin(mr, ra[q]);
       }
     }
   }
   for (int i = tid + kRegRows * kThreads; i < rows; i += kThreads) {
-    const double a = T[(size_t)i * cols + e];
-    fcol[i] = a;
-    if (a > kPivotTol) mr = fmin(mr, b[i] / a);
+    const double t = T[(size_t)i * cols + e];
+    fcol[i] = t;
+    const double a = dir * t;
+    if (a > kPivotTol && !(colfree && colfree[basis[i]])) mr = fmin(mr, b[i] / a);
   }
   for (int o = 16; o > 0; o >>= 1) mr = fmin(mr, __shfl_xor_sync(0xFFFFFFFFu, mr, o));
   if (lane == 0) sv[warp] = mr;
@@ -180,8 +210,9 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
       }
     }
     for (int i = tid + kRegRows * kThreads; i < rows; i += kThreads) {
-      const double a = fcol[i];
-      if (a > kPivotTol && b[i] / a <= lim && basis[i] < best_basic) {
+      const double a = dir * fcol[i];
+      if (a > kPivotTol && !(colfree && colfree[basis[i]]) && b[i] / a <= lim &&
+          basis[i] < best_basic) {
         best_basic = basis[i];
         best_row = i;
       }
@@ -240,6 +271,8 @@ __global__ void __launch_bounds__(kThreads) select_kernel(const double* __restri
   if (tid == 0) {
     pb[0] = b[row] / piv;
     pb[1] = cost[e];
+    pb[2] = (double)basis[row];  // the leaving variable
+    pb[3] = piv;
   }
 }
 
@@ -255,6 +288,8 @@ __global__ void capture_kernel(const double* __restrict__ T, const double* __res
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     pb[0] = b[row] / piv;
     pb[1] = 0.0;  // drive-out pivots run without a cost row
+    pb[2] = -1.0;
+    pb[3] = piv;
   }
 }
 
@@ -327,8 +362,11 @@ __global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
                                                          const int* __restrict__ done,
                                                          const double* __restrict__ prow,
                                                          const double* __restrict__ fcol,
-                                                         const double* pb) {
+                                                         const double* pb, double* wbase,
+                                                         int wmode,
+                                                         const long long* __restrict__ npiv) {
   if (*done) return;
+  double* dvx = wmode == 1 ? wbase : nullptr;
   const int col = sel[0], row = sel[1];
   const double brow = pb[0];
   const double cf = pb[1];
@@ -342,6 +380,10 @@ __global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
     q[v] = j < c2 ? __ldg(p2 + j) : make_double2(0.0, 0.0);
   }
   const int i0 = blockIdx.y * kPivRows;
+  const bool gam = wmode == 2;  // accumulate the updated columns' squared norms
+  double2 acc[kPivVec];
+#pragma unroll
+  for (int v = 0; v < kPivVec; ++v) acc[v] = make_double2(0.0, 0.0);
 #pragma unroll 2
   for (int r = 0; r < kPivRows; ++r) {
     const int i = i0 + r;
@@ -358,6 +400,25 @@ __global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
             cost[2 * j + 1] = c1;
           }
         }
+      if (dvx && pb[2] >= 0.0) {
+        // Devex reference weights (Forrest & Goldfarb): w_j = max(w_j,
+        // (a_rj / a_rq)^2 w_q) for the nonbasic columns, the leaving column
+        // max(w_q / a_rq^2, 1); prow holds a_rj / a_rq (0 on basic columns)
+        const double wq = dvx[col];
+        const int leave = (int)pb[2];
+        const double piv = pb[3];
+#pragma unroll
+        for (int v = 0; v < kPivVec; ++v) {
+          const int j = j0 + 256 * v;
+          if (j >= c2) continue;
+          for (int h = 0; h < 2; ++h) {
+            const int jj = 2 * j + h;
+            if (jj == col) continue;
+            const double a = h ? q[v].y : q[v].x;
+            dvx[jj] = jj == leave ? fmax(wq / (piv * piv), 1.0) : fmax(dvx[jj], a * a * wq);
+          }
+        }
+      }
       break;
     }
     double2* __restrict__ Ti = reinterpret_cast<double2*>(T + (size_t)i * cols);
@@ -365,7 +426,11 @@ __global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
 #pragma unroll
       for (int v = 0; v < kPivVec; ++v) {
         const int j = j0 + 256 * v;
-        if (j < c2) Ti[j] = q[v];
+        if (j < c2) {
+          Ti[j] = q[v];
+          acc[v].x = fma(q[v].x, q[v].x, acc[v].x);
+          acc[v].y = fma(q[v].y, q[v].y, acc[v].y);
+        }
       }
       if (blockIdx.x == 0 && threadIdx.x == 0) {
         b[i] = brow;
@@ -374,7 +439,7 @@ __global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
       continue;
     }
     const double f = fcol[i];
-    if (f == 0.0) continue;
+    if (f == 0.0 && !gam) continue;
     double2 t[kPivVec];
 #pragma unroll
     for (int v = 0; v < kPivVec; ++v) {
@@ -385,13 +450,41 @@ __global__ void __launch_bounds__(256) pivot_tile_kernel(double* __restrict__ T,
     for (int v = 0; v < kPivVec; ++v) {
       const int j = j0 + 256 * v;
       if (j < c2) {
-        t[v].x = fma(-f, q[v].x, t[v].x);
-        t[v].y = fma(-f, q[v].y, t[v].y);
-        Ti[j] = t[v];
+        if (f != 0.0) {
+          t[v].x = fma(-f, q[v].x, t[v].x);
+          t[v].y = fma(-f, q[v].y, t[v].y);
+          Ti[j] = t[v];
+        }
+        acc[v].x = fma(t[v].x, t[v].x, acc[v].x);
+        acc[v].y = fma(t[v].y, t[v].y, acc[v].y);
       }
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) b[i] -= f * brow;
+    if (f != 0.0 && blockIdx.x == 0 && threadIdx.x == 0) b[i] -= f * brow;
   }
+  if (gam) {
+    double* g = wbase + (size_t)((*npiv) & 1) * cols;
+#pragma unroll
+    for (int v = 0; v < kPivVec; ++v) {
+      const int j = j0 + 256 * v;
+      if (j < c2) {
+        atomicAdd(g + 2 * j, acc[v].x);
+        atomicAdd(g + 2 * j + 1, acc[v].y);
+      }
+    }
+  }
+}
+
+// squared column norms of the tableau (the steepest-edge weights of a phase's
+// first pivot) into g[0..cols)
+__global__ void colnorm_kernel(const double* __restrict__ T, int rows, int cols, double* g) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= cols) return;
+  double s = 0.0;
+  for (int i = 0; i < rows; ++i) {
+    const double t = T[(size_t)i * cols + j];
+    s = fma(t, t, s);
+  }
+  g[j] = s;
 }
 
 // v_i = a_i x + |a_i| r - b_i over all rows (A column-major m x n)
@@ -470,8 +563,8 @@ __global__ void __launch_bounds__(256) ws_argmax_kernel(const double* __restrict
 
 struct Dev {
   double *T = nullptr, *b = nullptr, *cost = nullptr, *prow = nullptr, *fcol = nullptr;
-  double *pb = nullptr, *ratio = nullptr;
-  int *basis = nullptr, *sel = nullptr, *zero = nullptr;
+  double *pb = nullptr, *ratio = nullptr, *dvx = nullptr;
+  int *basis = nullptr, *sel = nullptr, *zero = nullptr, *colfree = nullptr;
   Ctl* ctl = nullptr;
   cudaStream_t s = nullptr;
   ~Dev() {
@@ -482,9 +575,11 @@ struct Dev {
     cudaFree(fcol);
     cudaFree(pb);
     cudaFree(ratio);
+    cudaFree(dvx);
     cudaFree(basis);
     cudaFree(sel);
     cudaFree(zero);
+    cudaFree(colfree);
     cudaFree(ctl);
     if (s) cudaStreamDestroy(s);
   }
@@ -517,16 +612,21 @@ int err(std::string* msg, int code, const std::string& text) {
 // final basis is infeasible for the unperturbed rhs (retry with less).
 constexpr int kPerturbedOnly = 1000;
 
+// native_free: each free variable is ONE column that may enter in either
+// direction and never leaves once basic (no x+ / x- split, no l1 row; the
+// restricted LP may then report an unbounded ray, and the caller re-solves
+// with the split form, whose l1 row bounds it).
 int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::vector<double>& rhs,
             const std::vector<int>& is_eq, const std::vector<int>& is_free,
             const std::vector<double>& obj, int m, int nv, double perturb, double scale,
-            int l1_row, std::vector<double>* x, long* pivots, std::string* msg) {
+            int l1_row, bool native_free, std::vector<double>* x, long* pivots,
+            std::string* msg) {
   LpClock sclk;
   std::vector<int> var_col(nv);
   int ncols = 0;
   for (int v = 0; v < nv; ++v) {
     var_col[v] = ncols;
-    ncols += is_free[v] ? 2 : 1;
+    ncols += (is_free[v] && !native_free) ? 2 : 1;
   }
   int nslack = 0;
   for (int i = 0; i < m; ++i) nslack += is_eq[i] ? 0 : 1;
@@ -549,7 +649,8 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
     for (int v = 0; v < nv; ++v) {
       const double a = sgn[i] * Arow[(size_t)i * nv + v];
       row[var_col[v]] = a;
-      if (is_free[v]) row[var_col[v] + 1] = i == l1_row ? a : -a;  // l1: x+ + x- <= B
+      if (is_free[v] && !native_free)
+        row[var_col[v] + 1] = i == l1_row ? a : -a;  // l1: x+ + x- <= B
     }
     row[total] = sgn[i] * rhs[i];
     // golden-ratio sequence in [0.5, 1.5): distinct, deterministic per row
@@ -567,17 +668,25 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
       ++art;
     }
   }
+  std::vector<int> colfree(W, 0);
+  if (native_free)
+    for (int v = 0; v < nv; ++v)
+      if (is_free[v]) colfree[var_col[v]] = 1;
   Dev d;
   auto ok = [](cudaError_t e) { return e == cudaSuccess; };
   if (!ok(cudaStreamCreateWithFlags(&d.s, cudaStreamNonBlocking)) ||
       !ok(cudaMalloc(&d.T, sizeof(double) * T.size())) ||
       !ok(cudaMalloc(&d.b, sizeof(double) * m)) || !ok(cudaMalloc(&d.cost, sizeof(double) * W)) ||
       !ok(cudaMalloc(&d.prow, sizeof(double) * W)) ||
-      !ok(cudaMalloc(&d.fcol, sizeof(double) * m)) || !ok(cudaMalloc(&d.pb, 2 * sizeof(double))) ||
+      !ok(cudaMalloc(&d.fcol, sizeof(double) * m)) || !ok(cudaMalloc(&d.pb, 4 * sizeof(double))) ||
+      !ok(cudaMalloc(&d.dvx, 2 * sizeof(double) * W)) ||
       !ok(cudaMalloc(&d.zero, sizeof(int))) || !ok(cudaMalloc(&d.ctl, sizeof(Ctl))) ||
       !ok(cudaMalloc(&d.ratio, sizeof(double))) || !ok(cudaMalloc(&d.basis, sizeof(int) * m)) ||
-      !ok(cudaMalloc(&d.sel, sizeof(int) * 2)))
+      !ok(cudaMalloc(&d.sel, sizeof(int) * 2)) ||
+      (native_free && !ok(cudaMalloc(&d.colfree, sizeof(int) * W))))
     return err(msg, 100, "simplex: device allocation failed");
+  if (native_free)
+    cudaMemcpyAsync(d.colfree, colfree.data(), sizeof(int) * W, cudaMemcpyHostToDevice, d.s);
   cudaMemcpyAsync(d.T, T.data(), sizeof(double) * T.size(), cudaMemcpyHostToDevice, d.s);
   cudaMemcpyAsync(d.b, b.data(), sizeof(double) * m, cudaMemcpyHostToDevice, d.s);
   cudaMemcpyAsync(d.basis, basis.data(), sizeof(int) * m, cudaMemcpyHostToDevice, d.s);
@@ -591,20 +700,31 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
   const bool row_form = piv_env && !std::strcmp(piv_env, "row");
   const dim3 tile_grid((unsigned)((W / 2 + 256 * kPivVec - 1) / (256 * kPivVec)),
                        (unsigned)((rows + 1 + kPivRows - 1) / kPivRows));
-  auto pivot_launch = [&](const int* done) {
+  // Devex pricing with the tile update (MHAR_LP_PRICING=dantzig: the
+  // reference's rule throughout)
+  const char* pr_env = std::getenv("MHAR_LP_PRICING");
+  // exact steepest edge by default: the tile update accumulates the squared
+  // norms of the columns it rewrites, so the weights cost no extra pass; on
+  // the degenerate centring LP it needs 6x fewer pivots than Dantzig
+  // (config 5: 7.7K vs 47.9K).  MHAR_LP_PRICING=dantzig | devex | steepest
+  int wmode = row_form ? 0 : 2;
+  if (pr_env && !std::strcmp(pr_env, "dantzig")) wmode = 0;
+  if (!row_form && pr_env && !std::strcmp(pr_env, "devex")) wmode = 1;
+  auto pivot_launch = [&](const int* done, int wm) {
     if (row_form)
       pivot_kernel<<<rows + 1, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, d.sel, done,
                                                d.prow, d.fcol, d.pb);
     else
       pivot_tile_kernel<<<tile_grid, 256, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, d.sel,
-                                                    done, d.prow, d.fcol, d.pb);
+                                                    done, d.prow, d.fcol, d.pb, d.dvx, wm,
+                                                    &d.ctl->npiv);
   };
   // a host-chosen pivot (artificials driven out after phase one)
   auto pivot = [&](int row, int col) {
     set_sel_kernel<<<1, 1, 0, d.s>>>(d.sel, row, col);
     capture_kernel<<<std::max(1, std::min(1024, (std::max(rows, W) + 255) / 256)), 256, 0, d.s>>>(
         d.T, d.b, rows, W, row, col, d.prow, d.fcol, d.pb);
-    pivot_launch(d.zero);
+    pivot_launch(d.zero, 0);
     ++npiv;
   };
   const bool lp_trace = std::getenv("MHAR_LP_TRACE") != nullptr;  // one pivot per batch, logged
@@ -613,14 +733,23 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
     Ctl h{};
     h.budget = budget - npiv;
     h.stall_limit = rows + total;
+    if (const char* sl = std::getenv("MHAR_LP_STALL")) h.stall_limit = (int)(h.stall_limit * std::atof(sl));
     cudaMemcpyAsync(d.ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, d.s);
+    if (wmode == 1) {  // fresh reference framework: every weight 1
+      const std::vector<double> ones(W, 1.0);
+      cudaMemcpyAsync(d.dvx, ones.data(), sizeof(double) * W, cudaMemcpyHostToDevice, d.s);
+      cudaStreamSynchronize(d.s);  // `ones` is a local
+    } else if (wmode == 2) {  // exact weights of the phase's starting basis
+      colnorm_kernel<<<(W + 255) / 256, 256, 0, d.s>>>(d.T, rows, W, d.dvx);
+    }
     const char* bat_env = std::getenv("MHAR_LP_BATCH");
     int batch = bat_env ? std::max(1, std::atoi(bat_env)) : lp_trace ? 1 : 8;
     for (;;) {
       for (int k = 0; k < batch; ++k) {
         select_kernel<<<1, kThreads, 0, d.s>>>(d.T, d.b, d.cost, d.basis, rows, W, limit_col,
-                                               d.ctl, d.sel, d.prow, d.fcol, d.pb);
-        pivot_launch(&d.ctl->done);
+                                               d.ctl, d.sel, d.prow, d.fcol, d.pb, d.colfree,
+                                               d.dvx, wmode);
+        pivot_launch(&d.ctl->done, wmode);
       }
       cudaMemcpyAsync(&h, d.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, d.s);
       if (cudaStreamSynchronize(d.s) != cudaSuccess) return 100;
@@ -632,6 +761,9 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
       }
       if (h.done) {
         npiv += h.npiv;
+        if (sclk.on)
+          std::fprintf(stderr, "[lp profile]   phase: %lld pivots, bland %d, stall %d, status %d\n",
+                       h.npiv, h.bland, h.stall, h.status);
         return h.status;
       }
       if (!lp_trace && !bat_env) batch = std::min(batch * 2, 256);
@@ -706,7 +838,7 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
   std::vector<double> c2(W, 0.0);
   for (int v = 0; v < nv; ++v) {
     c2[var_col[v]] = obj[v];
-    if (is_free[v]) c2[var_col[v] + 1] = -obj[v];
+    if (is_free[v] && !native_free) c2[var_col[v] + 1] = -obj[v];
   }
   cudaMemcpyAsync(basis.data(), d.basis, sizeof(int) * rows, cudaMemcpyDeviceToHost, d.s);
   cudaStreamSynchronize(d.s);
@@ -735,12 +867,17 @@ int simplex(const std::vector<double>& Arow /* m x nv row-major */, const std::v
   if (cudaStreamSynchronize(d.s) != cudaSuccess) return err(msg, 100, "simplex: CUDA failure");
   std::vector<double> expanded(W, 0.0);
   for (int i = 0; i < rows; ++i) {
+    if (colfree[basis[i]]) {  // a basic free variable takes any sign
+      expanded[basis[i]] = orig[i];
+      continue;
+    }
     if (orig[i] < -1e-9 * scale) return kPerturbedOnly;
     expanded[basis[i]] = std::max(orig[i], 0.0);
   }
   x->assign(nv, 0.0);
   for (int v = 0; v < nv; ++v)
-    (*x)[v] = is_free[v] ? expanded[var_col[v]] - expanded[var_col[v] + 1] : expanded[var_col[v]];
+    (*x)[v] = (is_free[v] && !native_free) ? expanded[var_col[v]] - expanded[var_col[v] + 1]
+                                           : expanded[var_col[v]];
   return 0;
 }
 
@@ -823,6 +960,7 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
     ++rounds;
     const int nv = (int)n + 1;
     // + one l1 row sum(x+ + x-) <= box keeping the restricted LP bounded
+    // (split form only; the native-free form drops it)
     const int mw = (int)me + (int)work.size() + 1;
     std::vector<double> A((size_t)mw * nv, 0.0), rhs(mw);
     std::vector<int> is_eq(mw, 0), is_free(nv, 1);
@@ -844,12 +982,23 @@ int chebyshev_center(const double* a_in, const double* b_in, int64_t m, const do
     rhs[r] = box;
     std::vector<double> obj(nv, 0.0);
     obj[n] = 1.0;
-    // perturbed first; less (then none) if that basis misses the original
-    for (double eps : {1e-7, 1e-10, 0.0}) {
-      status = simplex(A, rhs, is_eq, is_free, obj, mw, nv, eps * scale, scale, l1_row, &xr,
-                       &pivots, msg);
-      clk.mark("simplex");
-      if (status != kPerturbedOnly) break;
+    // native free variables first (each x_k one column that never leaves the
+    // basis once in: a few pivots per coordinate instead of the x+ / x-
+    // swaps of the split form); the split form with its l1 row when that
+    // restricted LP is unbounded.  Perturbed first; less (then none) if that
+    // basis misses the original.
+    const char* lp_form = std::getenv("MHAR_LP_FORM");  // "split": the first round's form
+    const bool split_only = lp_form && !std::strcmp(lp_form, "split");
+    for (int form = split_only ? 1 : 0; form < 2; ++form) {
+      const bool native = form == 0;
+      const int rows_used = native ? mw - 1 : mw;  // the l1 row is the last
+      for (double eps : {1e-7, 1e-10, 0.0}) {
+        status = simplex(A, rhs, is_eq, is_free, obj, rows_used, nv, eps * scale, scale,
+                         native ? -1 : l1_row, native, &xr, &pivots, msg);
+        clk.mark(native ? "simplex (native free)" : "simplex (split)");
+        if (status != kPerturbedOnly) break;
+      }
+      if (!(native && status == 7)) break;
     }
     if (status) break;
     // violations over all rows on the GPU
