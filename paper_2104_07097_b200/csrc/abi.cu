@@ -99,9 +99,10 @@ struct mhar_ctx {
   int *redraw_list = nullptr, *redraw_count = nullptr, *attempts = nullptr;
   int *first_reject = nullptr, *first_bad = nullptr;
   unsigned long long *err = nullptr, *redraw_total = nullptr;
+  unsigned* sched = nullptr;  // chord2 unit tickets (chord_kernel.cuh next_unit)
   uint64_t *col_state = nullptr, *theta_state = nullptr;
   int redraw_grid = 1;
-  int group_m = 4;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
+  int group_m = 16;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
   int walk_band = 0;  // > 0: walk-tile bands (MHAR_WALK_BAND overrides)
   // walk-resident small-body path (small_kernel.cuh); Acm != null enables it
   double* Acm = nullptr;
@@ -255,6 +256,7 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   p.tc_walk_tiles = c->tc_walk_tiles;
   p.cache_rows = c->cache_rows;
   p.rate_f32 = c->Ahi != nullptr;
+  p.sched = c->sched;
   return p;
 }
 
@@ -1081,7 +1083,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       (st = dalloc(c, &c->first_bad, 1)) || (st = dalloc(c, &c->err, 1)) ||
       (st = dalloc(c, &c->redraw_total, 1)) || (st = dalloc(c, &c->col_state, c->z_pad)) ||
       (st = dalloc(c, &c->theta_state, 1)) || (st = dalloc(c, &c->x0, c->n)) ||
-      (st = dalloc(c, &c->injected_u, c->z_pad)))
+      (st = dalloc(c, &c->injected_u, c->z_pad)) || (st = dalloc(c, &c->sched, 2)))
     return bail(st);
   c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
   if (const char* g = std::getenv("MHAR_GROUP_M")) c->group_m = std::max(1, std::atoi(g));

@@ -64,7 +64,8 @@ constexpr int CHORD2_STAGES = MHAR_CHORD2_STAGES;  // 4 x 24 KB ring per CTA
 #endif
 constexpr int CHORD2_LAG = MHAR_CHORD2_LAG;
 constexpr int STAGE2_DOUBLES = A_PIECE + B_PIECE;
-constexpr size_t CHORD2_SMEM = (size_t)CHORD2_STAGES * STAGE2_DOUBLES * sizeof(double) + 256;
+constexpr int CHORD2_UQ = 8;  // announced-unit queue (> stages: the producer's lead in units)
+constexpr size_t CHORD2_SMEM = (size_t)CHORD2_STAGES * STAGE2_DOUBLES * sizeof(double) + 512;
 
 struct ChordParams {
   const double* A;  // packed A_I (a_index)
@@ -89,6 +90,7 @@ struct ChordParams {
   int64_t tc_walk_tiles;  // > 0: the slack cache uses a tcgen05 tile layout (tile_cache_index)
   int64_t cache_rows;     // its row tile: 256 (fp32 variant, fp32 rates) or 64 (int8 slices)
   int rate_f32;           // 1: the rate cache holds fp32 (fp32 variant)
+  unsigned* sched;        // chord2 unit tickets [next, finished CTAs]; zero between launches
 };
 
 // Slack-cache index for FUSED_STORE: the layout of whichever kernel consumes it.
@@ -346,6 +348,26 @@ __global__ void __launch_bounds__(CHORD_THREADS, 1) chord_kernel(const ChordPara
 // ===========================================================================
 // INCREMENTAL / CHECK: two CTAs per SM, tile 128 rows x 64 walks.
 // ===========================================================================
+// Units are handed out in order by a global ticket counter (p.sched) rather
+// than statically (CTA b taking b, b + grid, ...): CTAs that drift apart over
+// a few hundred units no longer spread the units in flight over many row
+// bands, so the band's A_I tiles and the direction tiles stay L2-resident
+// (DRAM traffic per launch was 70-150 GB against 29.5 GB algorithmic with
+// the static order, and varied from run to run with the drift).  Thread 0
+// draws the tickets as the producer and announces each unit (or the end,
+// -1) to the CTA through a small queue of (unit, mbarrier) slots.
+__device__ inline int64_t next_unit(const ChordParams& p, int64_t n_units) {
+  const int64_t u = (int64_t)atomicAdd(p.sched, 1u);
+  if (u < n_units) return u;
+  // this CTA's last ticket; the last CTA to get here rewinds the counter for
+  // the next launch (every other CTA has drawn its last ticket already)
+  if (atomicAdd(p.sched + 1, 1u) == gridDim.x - 1) {
+    p.sched[0] = 0u;
+    p.sched[1] = 0u;
+  }
+  return -1;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordParams p) {
   if (*p.err != kNoError) return;
@@ -354,12 +376,12 @@ __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordPar
   uint64_t* full =
       reinterpret_cast<uint64_t*>(smem_raw + (size_t)CHORD2_STAGES * STAGE2_DOUBLES * 8);
   uint64_t* empty = full + CHORD2_STAGES;
+  uint64_t* uready = empty + CHORD2_STAGES;  // [CHORD2_UQ] unit announced
+  long long* uq = reinterpret_cast<long long*>(uready + CHORD2_UQ);  // [CHORD2_UQ] the units
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;  // warp tile: 32 rows x 32 walks
   const int64_t n_units = p.m_tiles * p.col_tiles;
-  const int my_units =
-      (blockIdx.x < n_units) ? (int)((n_units - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int KT = (int)p.KT;
   const double* __restrict__ Bsrc = (MODE == INCREMENTAL) ? p.D : p.X;
 
@@ -368,40 +390,68 @@ __global__ void __launch_bounds__(CHORD_THREADS, 2) chord2_kernel(const ChordPar
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CHORD_THREADS / 32);
     }
+    for (int s = 0; s < CHORD2_UQ; ++s) mbar_init(&uready[s], 1);
     fence_barrier_init();
   }
   __syncthreads();
 
-  int l_ui = 0, l_kt = 0, l_stage = 0, l_round = 0;
-  int64_t l_mt = 0, l_ct = 0;
-  uint64_t keep_policy = 0;
-  auto producer_issue = [&]() {
-    if (l_ui >= my_units) return;
-    if (l_round > 0) mbar_wait(&empty[l_stage], (uint32_t)((l_round - 1) & 1));
-    double* st = ring + (size_t)l_stage * STAGE2_DOUBLES;
-    mbar_arrive_expect_tx(&full[l_stage], STAGE2_DOUBLES * 8);
-    bulk_g2s(st, p.A + (l_mt * p.KT + l_kt) * A_PIECE, A_PIECE * 8, &full[l_stage]);
-    bulk_g2s_hint(st + A_PIECE, Bsrc + (l_ct * p.KT + l_kt) * B_PIECE, B_PIECE * 8,
-                  &full[l_stage], keep_policy);
-    if (++l_stage == CHORD2_STAGES) {
-      l_stage = 0;
-      ++l_round;
+  // producer state (thread 0), kept in shared memory: in registers it would
+  // be allocated in every thread and push the 128-register accumulator
+  // tiles into spills
+  struct Producer {
+    const double* a;  // next A_I stage piece
+    const double* b;  // next B stage piece
+    int kt, stage, round, ann;
+    long long unit;
+  };
+  __shared__ Producer pr;
+  auto announce = [&](int64_t u) {  // unit u (or -1: no more) to the consumers
+    uq[pr.ann % CHORD2_UQ] = u;
+    mbar_arrive(&uready[pr.ann % CHORD2_UQ]);  // release: the uq write is visible
+    ++pr.ann;
+    pr.unit = u;
+    if (u >= 0) {
+      int64_t mt, ct;
+      unit_coords(u, p, &mt, &ct);
+      pr.a = p.A + mt * p.KT * A_PIECE;
+      pr.b = Bsrc + ct * p.KT * B_PIECE;
     }
-    if (++l_kt == KT) {
-      l_kt = 0;
-      if (++l_ui < my_units) unit_coords(blockIdx.x + (int64_t)l_ui * gridDim.x, p, &l_mt, &l_ct);
+  };
+  auto producer_issue = [&]() {
+    if (pr.unit < 0) return;
+    const int stage = pr.stage;
+    if (pr.round > 0) mbar_wait(&empty[stage], (uint32_t)((pr.round - 1) & 1));
+    double* st = ring + (size_t)stage * STAGE2_DOUBLES;
+    mbar_arrive_expect_tx(&full[stage], STAGE2_DOUBLES * 8);
+    bulk_g2s(st, pr.a, A_PIECE * 8, &full[stage]);
+    bulk_g2s_hint(st + A_PIECE, pr.b, B_PIECE * 8, &full[stage],
+                  MHAR_CHORD2_KEEP ? policy_evict_last() : policy_evict_normal());
+    pr.a += A_PIECE;
+    pr.b += B_PIECE;
+    if (stage + 1 == CHORD2_STAGES) {
+      pr.stage = 0;
+      ++pr.round;
+    } else {
+      pr.stage = stage + 1;
+    }
+    if (++pr.kt == KT) {
+      pr.kt = 0;
+      announce(next_unit(p, n_units));
     }
   };
   if (tid == 0) {
-    keep_policy = MHAR_CHORD2_KEEP ? policy_evict_last() : policy_evict_normal();
-    if (my_units > 0) unit_coords(blockIdx.x, p, &l_mt, &l_ct);
+    pr.kt = pr.stage = pr.round = pr.ann = 0;
+    announce(next_unit(p, n_units));
     for (int q = 0; q < CHORD2_STAGES - CHORD2_LAG; ++q) producer_issue();
   }
 
   int c_stage = 0, c_phase = 0;
-  for (int ui = 0; ui < my_units; ++ui) {
+  for (int ui = 0;; ++ui) {
+    mbar_wait(&uready[ui % CHORD2_UQ], (uint32_t)((ui / CHORD2_UQ) & 1));
+    const int64_t u = uq[ui % CHORD2_UQ];
+    if (u < 0) break;
     int64_t mt, ct;
-    unit_coords(blockIdx.x + (int64_t)ui * gridDim.x, p, &mt, &ct);
+    unit_coords(u, p, &mt, &ct);
     const int64_t cache_base = ((mt * p.col_tiles + ct) * 8 + warp) * S_WARP_BLOCK;
 
     double acc[4][4][2];
