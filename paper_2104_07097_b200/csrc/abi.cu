@@ -8,6 +8,7 @@
 //   -> redraw (slow path, usually empty) -> theta (+ fix-up) -> x += theta d
 //   -> [reprojection every reproject_every iterates]
 // All launches are queued on the context's stream without host syncs.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -114,6 +115,9 @@ struct mhar_ctx {
   bool tc_f16 = true;   // fp32 variant on kind::f16 with per-row / per-walk scales (MHAR_TC_F16=0: TF32)
   int64_t tc_kt = 0;    // k stages of the fp32 variant (16 floats or 32 halves each)
   float *tc_rsc = nullptr, *tc_csc = nullptr;
+  // tensor maps of the fp32 variant's operand arrays (2-CTA TMA loads)
+  CUtensorMap tm_ahi{}, tm_alo{}, tm_dhi{}, tm_dlo{};
+  bool tc_tma = false;
   int64_t cache_rows = 0;  // row tile of the tcgen05 cache layout (256 tc32, 64 int8)
   // int8-slice fp64 engine (chord_i8.cuh)
   uint8_t *A8 = nullptr, *D8 = nullptr;
@@ -190,6 +194,34 @@ inline int blocks_for(int64_t work, int threads, int cap) {
   if (b < 1) b = 1;
   if (b > cap) b = cap;
   return (int)b;
+}
+
+// A packed operand array of `floats` 4-byte words as a 2-D tensor of rows of
+// 64 words, boxes of 64 x 32 (one 8 KB stage piece); the driver entry point is
+// looked up at run time so the library needs no -lcuda.
+bool encode_piece_map(CUtensorMap* tm, const void* base, size_t floats) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode encode = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<Encode>(f);
+  }();
+  if (!encode || floats % 64 != 0) return false;
+  const cuuint64_t dims[2] = {64, floats / 64};
+  const cuuint64_t strides[1] = {256};
+  const cuuint32_t box[2] = {64, 32};
+  const cuuint32_t estride[2] = {1, 1};
+  return encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<void*>(base), dims, strides, box,
+                estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 int launch_check(mhar_ctx* c, const char* what) {
@@ -366,6 +398,11 @@ int launch_tc32(mhar_ctx* c) {
   p.group_n = c->tc_group_n;
   p.a_policy = c->tc_a_policy;
   p.prof = c->tc_prof;
+  p.tmAhi = c->tm_ahi;
+  p.tmAlo = c->tm_alo;
+  p.tmDhi = c->tm_dhi;
+  p.tmDlo = c->tm_dlo;
+  p.use_tma = c->tc_tma ? 1 : 0;
   if (c->tc_prof) cudaMemsetAsync(c->tc_prof, 0, kProfWords * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);  // (row tile, walk-tile pair)
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);  // CTA pairs
@@ -1150,6 +1187,14 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       ++c->launches;
       cudaMemsetAsync(c->Dhi, 0, dn * sizeof(float), c->stream);
       cudaStreamSynchronize(c->stream);
+      // 2-CTA TMA loads (MHAR_TC_TMA=0: plain bulk copies and the odd CTA's relay)
+      const char* tma_env = std::getenv("MHAR_TC_TMA");
+      c->tc_tma = !(tma_env && std::atoi(tma_env) == 0) &&
+                  encode_piece_map(&c->tm_ahi, c->Ahi, an) &&
+                  encode_piece_map(&c->tm_alo, c->Alo, an) &&
+                  encode_piece_map(&c->tm_dhi, c->Dhi, dn) &&
+                  (!c->Dlo || encode_piece_map(&c->tm_dlo, c->Dlo, dn));
+      if (!c->Dlo) c->tm_dlo = c->tm_dhi;
       cudaFuncSetAttribute(chord_tc32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TcCfg<false>::smem);
       cudaFuncSetAttribute(chord_tc32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -34,6 +34,7 @@
 // MMAs of the next.
 #pragma once
 
+#include <cuda.h>  // CUtensorMap
 #include <cuda_fp16.h>
 
 #include "chord_kernel.cuh"
@@ -245,7 +246,25 @@ struct TcParams {
   unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
   const float* rsc;  // fp16 form: per-row 2^s (rate = acc * rsc[r] * csc[c]), else null
   const float* csc;  // fp16 form: per-walk 2^t
+  // Tensor maps over the packed operand arrays viewed as rows of 64 4-byte
+  // words (one 8 KB piece = a 64 x 32 box): with them both CTAs of the pair
+  // load through cp.async.bulk.tensor ... cta_group::2, whose completion
+  // lands on the LEADER's full barrier -- no relay hop through the odd CTA.
+  CUtensorMap tmAhi, tmAlo, tmDhi, tmDlo;
+  int use_tma;
 };
+
+// one 8 KB piece (float offset `off`, a multiple of 2048) into this CTA's
+// smem, completing on the pair leader's barrier `bar_leader` (shared::cluster
+// address of CTA 0)
+__device__ inline void tma_piece_2cta(void* dst, const CUtensorMap* tm, int64_t off,
+                                      uint32_t bar_leader, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
+      "l"(tm), "r"(0), "r"((int)(off >> 6)), "r"(bar_leader), "l"(policy)
+      : "memory");
+}
 
 // unit u -> (row tile, walk-tile pair), banded over group_n row tiles
 __device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_t* wp) {
@@ -261,7 +280,7 @@ __device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_
 
 template <bool SPLIT_D, bool F16 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
-    chord_tc32_kernel(const TcParams p) {
+    chord_tc32_kernel(const __grid_constant__ TcParams p) {
   constexpr int kStages = TcCfg<SPLIT_D>::stages;
   constexpr int kStageFloats = TcCfg<SPLIT_D>::stage_floats;
   unsigned long long g_entry = 0;
@@ -333,16 +352,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           if (round > 0) mbar_wait(&empty[stage], (uint32_t)((round - 1) & 1));
           w_empty += clock64() - t0;
           float* st = ring + (size_t)stage * kStageFloats;
-          mbar_arrive_expect_tx(&full[stage], kStageFloats * 4);
           const int64_t doff = (wt * p.KT + kt) * TC_D_PIECE;
           const int64_t aoff = ((rt * p.KT + kt) * 2 + rank) * TC_A_PIECE;
-          bulk_g2s_hint(st, p.Dhi + doff, TC_D_PIECE * 4, &full[stage], keep);
-          bulk_g2s_hint(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage], apol);
-          bulk_g2s_hint(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4, &full[stage],
-                        apol);
-          if (SPLIT_D)
-            bulk_g2s_hint(st + TC_D_PIECE + 2 * TC_A_PIECE, p.Dlo + doff, TC_D_PIECE * 4,
-                          &full[stage], keep);
+          if (p.use_tma) {
+            // both CTAs' pieces complete on the leader's full barrier, which
+            // the leader arms with the bytes of the whole pair
+            uint32_t lb;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
+                         : "=r"(lb)
+                         : "r"(smem_u32(&full[stage])), "r"(0));
+            if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * kStageFloats * 4);
+            tma_piece_2cta(st, &p.tmDhi, doff, lb, keep);
+            tma_piece_2cta(st + TC_D_PIECE, &p.tmAhi, aoff, lb, apol);
+            tma_piece_2cta(st + TC_D_PIECE + TC_A_PIECE, &p.tmAlo, aoff, lb, apol);
+            if (SPLIT_D) tma_piece_2cta(st + TC_D_PIECE + 2 * TC_A_PIECE, &p.tmDlo, doff, lb, keep);
+          } else {
+            mbar_arrive_expect_tx(&full[stage], kStageFloats * 4);
+            bulk_g2s_hint(st, p.Dhi + doff, TC_D_PIECE * 4, &full[stage], keep);
+            bulk_g2s_hint(st + TC_D_PIECE, p.Ahi + aoff, TC_A_PIECE * 4, &full[stage], apol);
+            bulk_g2s_hint(st + TC_D_PIECE + TC_A_PIECE, p.Alo + aoff, TC_A_PIECE * 4,
+                          &full[stage], apol);
+            if (SPLIT_D)
+              bulk_g2s_hint(st + TC_D_PIECE + 2 * TC_A_PIECE, p.Dlo + doff, TC_D_PIECE * 4,
+                            &full[stage], keep);
+          }
           if (++stage == kStages) {
             stage = 0;
             ++round;
@@ -368,7 +401,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
           const long long t1 = clock64();
           mbar_wait(&full[stage], (uint32_t)phase);
           const long long t2 = clock64();
-          mbar_wait_relaxed(&peer_full[stage], (uint32_t)phase);
+          if (!p.use_tma) mbar_wait_relaxed(&peer_full[stage], (uint32_t)phase);
           w_full += t2 - t1;
           w_peer += clock64() - t2;
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -412,7 +445,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         pr[2] = (unsigned long long)w_full;
         pr[3] = (unsigned long long)w_peer;
       }
-    } else if (lane == 0) {
+    } else if (lane == 0 && !p.use_tma) {
       // ---------------- relay (odd CTA): my stage landed -> leader ----------------
       int stage = 0, phase = 0;
       for (int ui = 0; ui < my_units; ++ui)
