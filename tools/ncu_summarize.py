@@ -1,4 +1,4 @@
-"""Builds profiles/ncu_full_r01.json from the --set full captures of
+"""Builds profiles/ncu_full_rNN.json from the --set full captures of
 tools/ncu_capture.sh (gpurun_out/<name>.ncu-rep): the per-launch metrics
 bench.py's roofline reads (DRAM bytes), plus clock, tensor-pipe activity and
 L2 hit rate, and the derived DRAM GB/s."""
@@ -48,12 +48,23 @@ def summarize(rep):
 
 
 if __name__ == "__main__":
-    dest = sys.argv[1] if len(sys.argv) > 1 else "profiles/ncu_full_r01.json"
-    doc = {name: summarize(f"gpurun_out/{name}.ncu-rep")
-           for name in ("chord2_full", "tc32_full", "i8_full")}
+    import datetime
+    import os
+    dest = sys.argv[1] if len(sys.argv) > 1 else "profiles/ncu_full_r02.json"
+    names = [n for n in ("chord2_full", "tc32_full", "tc32r_full", "i8_full")
+             if os.path.exists(f"gpurun_out/{n}.ncu-rep")]
+    doc = {name: summarize(f"gpurun_out/{name}.ncu-rep") for name in names}
+    commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
+                            text=True).stdout.strip()
+    doc["_meta"] = {"captured": datetime.date.today().isoformat(), "commit": commit,
+                    "kernels": {"chord2_full": "chord2_kernel<INCREMENTAL> (DMMA headline)",
+                                "tc32_full": "chord_tc32_kernel, fp32 variant, split direction",
+                                "tc32r_full": "chord_tc32_kernel, fp32 variant, rounded direction",
+                                "i8_full": "chord_i8_kernel (int8-slice fp64 engine)"}}
     doc["_how"] = ("tools/ncu_capture.sh: ncu --set full --clock-control none --import-source on "
                    "-k <kernel> --launch-skip 1 -c 1 python bench.py ... (config 5, 4096 walks); "
                    "numbers per launch; summarised by tools/ncu_summarize.py")
     with open(dest, "w") as f:
         json.dump(doc, f, indent=1)
-    print(json.dumps({k: v["derived"] for k, v in doc.items() if k != "_how"}, indent=1))
+    print(json.dumps({k: v["derived"] for k, v in doc.items() if k not in ("_how", "_meta")},
+                     indent=1))
