@@ -111,6 +111,7 @@ struct mhar_ctx {
   float *Ahi = nullptr, *Alo = nullptr, *Dhi = nullptr, *Dlo = nullptr;
   int64_t tc_walk_tiles = 0, tc_row_tiles = 0;
   int tc_group_n = 1;   // tc32 rasterisation band (row tiles); MHAR_TC_GROUP overrides
+  int tc_walk_band = 0; // tc32 walk-pair bands for large z (MHAR_TC_WALK_BAND overrides)
   int tc_a_policy = 0;  // L2 policy of the tc32 A stream (evict_normal); MHAR_TC_APOL overrides
   bool tc_f16 = true;   // fp32 variant on kind::f16 with per-row / per-walk scales (MHAR_TC_F16=0: TF32)
   int64_t tc_kt = 0;    // k stages of the fp32 variant (16 floats or 32 halves each)
@@ -396,6 +397,7 @@ int launch_tc32(mhar_ctx* c) {
   p.eps_dir = c->opt.eps_dir;
   p.margin = c->opt.fp32_margin > 0 ? c->opt.fp32_margin : 2e-5;
   p.group_n = c->tc_group_n;
+  p.walk_band = c->tc_walk_band;
   p.a_policy = c->tc_a_policy;
   p.prof = c->tc_prof;
   p.tmAhi = c->tm_ahi;
@@ -1195,6 +1197,14 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
                   encode_piece_map(&c->tm_dhi, c->Dhi, dn) &&
                   (!c->Dlo || encode_piece_map(&c->tm_dlo, c->Dlo, dn));
       if (!c->Dlo) c->tm_dlo = c->tm_dhi;
+      {
+        // walk-pair bands once the direction operands outgrow a ~32 MB L2 share
+        const int64_t pair_bytes = 2 * c->tc_kt * (int64_t)TC_D_PIECE * 4 * (c->Dlo ? 2 : 1);
+        const int64_t pairs = c->tc_walk_tiles / 2;
+        const int64_t fit = std::max<int64_t>(1, (32ll << 20) / pair_bytes);
+        c->tc_walk_band = pairs > fit ? (int)fit : 0;
+        if (const char* g = std::getenv("MHAR_TC_WALK_BAND")) c->tc_walk_band = std::max(0, std::atoi(g));
+      }
       cudaFuncSetAttribute(chord_tc32_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)TcCfg<false>::smem);
       cudaFuncSetAttribute(chord_tc32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -242,6 +242,7 @@ struct TcParams {
   double eps_dir;
   double margin;       // mu: chords of {A x <= b - mu}
   int group_n;         // rasterisation band (row tiles)
+  int walk_band;       // > 0: bands of this many walk-tile pairs, row tiles inner (large z)
   int a_policy;        // L2 policy of the A_hi/A_lo stream: 0 normal, 1 evict_last, 2 evict_first
   unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
   const float* rsc;  // fp16 form: per-row 2^s (rate = acc * rsc[r] * csc[c]), else null
@@ -266,9 +267,23 @@ __device__ inline void tma_piece_2cta(void* dst, const CUtensorMap* tm, int64_t 
       : "memory");
 }
 
-// unit u -> (row tile, walk-tile pair), banded over group_n row tiles
+// unit u -> (row tile, walk-tile pair), banded over group_n row tiles; with
+// walk_band > 0 (direction operands larger than L2 can hold: z beyond ~4K at
+// n = 2000) bands of walk_band pairs sweep every row tile, so the band's
+// direction tiles stay L2-resident and A_I is streamed once per band instead
+// of every direction tile once per row tile
 __device__ inline void tc_unit(int64_t u, const TcParams& p, int64_t* rt, int64_t* wp) {
   const int64_t pairs = p.walk_tiles / 2;
+  if (p.walk_band > 0 && p.walk_band < pairs) {
+    const int64_t band_units = (int64_t)p.walk_band * p.row_tiles;
+    const int64_t band = u / band_units;
+    const int64_t in_band = u - band * band_units;
+    const int64_t start = band * p.walk_band;
+    const int64_t w = (pairs - start < p.walk_band) ? pairs - start : p.walk_band;
+    *wp = start + in_band % w;
+    *rt = in_band / w;
+    return;
+  }
   const int64_t band_units = (int64_t)p.group_n * pairs;
   const int64_t band = u / band_units;
   const int64_t in_band = u - band * band_units;
