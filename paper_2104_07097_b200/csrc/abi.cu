@@ -321,7 +321,12 @@ int launch_diag(mhar_ctx* c, int mode, const double* X) {
     ev = take_events(c);
     cudaEventRecord(ev.first, c->stream);
   }
-  diag_chord_kernel<<<grid, kDiagThreads, 0, c->stream>>>(p);
+  if (c->diag_blocks == 2)
+    diag_chord_kernel<2><<<grid, kDiagThreads, 0, c->stream>>>(p);
+  else if (c->diag_blocks == 1)
+    diag_chord_kernel<1><<<grid, kDiagThreads, 0, c->stream>>>(p);
+  else
+    diag_chord_kernel<0><<<grid, kDiagThreads, 0, c->stream>>>(p);
   LAUNCH_OK(c, "diag_chord_kernel");
   ++c->chord_launches;
   if (c->timing) {

@@ -41,6 +41,9 @@ struct DiagParams {
 // grid = (walk tiles of 64, coordinate splits); thread t owns packed element t
 // of every piece (B_PIECE = 1024 = blockDim), i.e. one (walk, k-offset) slot,
 // and walks its k tiles four at a time with all eight loads in flight.
+// BLOCKS > 0: the block count known at compile time (1: simplex -I, 2: the
+// hypercube's [I; -I]) so the row loop unrolls; 0: p.blocks at run time.
+template <int BLOCKS>
 __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagParams p) {
   if (*p.err != kNoError) return;
   __shared__ long long s_hi[BC], s_lo[BC], s_viol[BC];
@@ -63,27 +66,33 @@ __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagPara
   double ehi = __longlong_as_double(0x7FF0000000000000LL), elo = -ehi;
   double viol = __longlong_as_double((long long)0xFFF0000000000000ULL);
   unsigned sd = 0u;
-  for (int64_t kt = kt0; kt < kt1; kt += 4) {
+  // 32-bit coordinate / row arithmetic (m = blocks n < 2^31)
+  const int n32 = (int)p.n, nblk = BLOCKS > 0 ? BLOCKS : (int)p.blocks;
+  const int kof32 = (int)kof;
+  for (int kt = (int)kt0; kt < (int)kt1; kt += 4) {
     double x[4], d[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t k = (kt + u) * BK + kof;
-      const bool live = kt + u < kt1 && k < p.n;
-      x[u] = live ? Xt[(kt + u) * B_PIECE] : 0.0;
-      d[u] = live ? Dt[(kt + u) * B_PIECE] : 0.0;
+      const int k = (kt + u) * BK + kof32;
+      const bool live = kt + u < (int)kt1 && k < n32;
+      x[u] = live ? Xt[(int64_t)(kt + u) * B_PIECE] : 0.0;
+      d[u] = live ? Dt[(int64_t)(kt + u) * B_PIECE] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const int64_t k = (kt + u) * BK + kof;
-      if (kt + u >= kt1 || k >= p.n) continue;
-      for (int64_t blk = 0; blk < p.blocks; ++blk) {
-        const int64_t r = blk * p.n + k;
-        const double cf = __ldg(p.coef + r);
-        // -(x c) + b and d c, one rounding each (sampler.cpp:168-170; no FMA
-        // contraction, so the bounds equal the one-term dot products')
-        const double sl = __dsub_rn(__ldg(p.b + r), __dmul_rn(x[u], cf));
-        viol = fmax(viol, -sl);
-        if (p.bounds) scan_row(sl, __dmul_rn(d[u], cf), p.eps_dir, ehi, elo, sd);
+      const int k = (kt + u) * BK + kof32;
+      if (kt + u >= (int)kt1 || k >= n32) continue;
+#pragma unroll
+      for (int blk = 0; blk < (BLOCKS > 0 ? BLOCKS : 1); ++blk) {
+        for (int bb = blk; bb < (BLOCKS > 0 ? blk + 1 : nblk); ++bb) {
+          const int r = bb * n32 + k;
+          const double cf = __ldg(p.coef + r);
+          // -(x c) + b and d c, one rounding each (sampler.cpp:168-170; no FMA
+          // contraction, so the bounds equal the one-term dot products')
+          const double sl = __dsub_rn(__ldg(p.b + r), __dmul_rn(x[u], cf));
+          viol = fmax(viol, -sl);
+          if (p.bounds) scan_row(sl, __dmul_rn(d[u], cf), p.eps_dir, ehi, elo, sd);
+        }
       }
     }
   }

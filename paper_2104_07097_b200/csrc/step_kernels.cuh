@@ -130,14 +130,18 @@ __global__ void normals_kernel(const RngParams rp, double* __restrict__ H,
   // contiguous bytes -- one pair per thread
   const int64_t ct64 = (rp.z + BC - 1) / BC;
   const int64_t total = ct64 * rp.KT * 16 * 32;
+  const uint32_t KT32 = (uint32_t)rp.KT;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t blk = t >> 5;
     const int tl = (int)(t & 31);
-    const int64_t cg = blk & 7, k8 = (blk >> 3) & 1, kt = (blk >> 4) % rp.KT,
-                  ct = (blk >> 4) / rp.KT;
-    const int64_t c = ct * BC + cg * 8 + (tl >> 2);
-    const int64_t pidx = (kt * BK + k8 * 8) / 2 + (tl & 3);
+    // (walk tile, k tile) of the block: 32-bit division (ct64 * KT < 2^32);
+    // the 64-bit div/mod was a large share of this issue-bound kernel
+    const uint32_t q = (uint32_t)(blk >> 4);
+    const uint32_t kt = q % KT32, ct = q / KT32;
+    const int cg = (int)(blk & 7), k8 = (int)((blk >> 3) & 1);
+    const int64_t c = (int64_t)ct * BC + cg * 8 + (tl >> 2);
+    const int64_t pidx = (int64_t)(kt * BK + k8 * 8) / 2 + (tl & 3);
     if (c >= rp.z || pidx >= ppc) continue;
     double u1, u2;
     if (rp.mode == 0) {
@@ -154,8 +158,11 @@ __global__ void normals_kernel(const RngParams rp, double* __restrict__ H,
     }
     double cs, sn;
     box_muller(u1, u2, &cs, &sn);
-    H[b_index(c, 2 * pidx, rp.KT)] = cs;
-    if (2 * pidx + 1 < rp.n) H[b_index(c, 2 * pidx + 1, rp.KT)] = sn;
+    // b_index(c, 2 pidx) and b_index(c, 2 pidx + 1) within this thread's
+    // 512-byte block: lane = (c % 8) * 4 + k % 4, element (k % 8) / 4
+    const int64_t o = blk * 64 + (tl >> 2) * 8 + (tl & 1) * 4 + ((tl >> 1) & 1);
+    H[o] = cs;
+    if (2 * pidx + 1 < rp.n) H[o + 2] = sn;
   }
 }
 
