@@ -126,6 +126,7 @@ struct mhar_ctx {
   int* rexp = nullptr;
   int64_t KS = 0, i8_row_tiles = 0;
   int i8_clusters = 0;  // co-resident clusters of the int8 kernel
+  int i8_group = 16;    // int8 kernel rasterisation band (row groups); MHAR_I8_GROUP overrides
   bool dmma_refresh = false;  // MHAR_DMMA_REFRESH=1: tcgen05 engines refresh with the fused DMMA pass
   // CUDA graph of one steady iterate (multi-kernel path, MHAR_NO_GRAPHS=1 disables):
   // the kernels read the Philox iterate counter from d_iter
@@ -453,6 +454,8 @@ int launch_i8(mhar_ctx* c) {
   p.err = c->err;
   p.row_tiles = c->i8_row_tiles;
   p.walk_tiles = c->tc_walk_tiles;
+  p.sched = c->sched + 2;  // its own ticket pair (chord2 uses sched[0..1])
+  p.group = c->i8_group;
   p.KS = c->KS;
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
@@ -1127,7 +1130,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       (st = dalloc(c, &c->first_bad, 1)) || (st = dalloc(c, &c->err, 1)) ||
       (st = dalloc(c, &c->redraw_total, 1)) || (st = dalloc(c, &c->col_state, c->z_pad)) ||
       (st = dalloc(c, &c->theta_state, 1)) || (st = dalloc(c, &c->x0, c->n)) ||
-      (st = dalloc(c, &c->injected_u, c->z_pad)) || (st = dalloc(c, &c->sched, 2)))
+      (st = dalloc(c, &c->injected_u, c->z_pad)) || (st = dalloc(c, &c->sched, 4)))
     return bail(st);
   c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
   if (const char* g = std::getenv("MHAR_GROUP_M")) c->group_m = std::max(1, std::atoi(g));
@@ -1135,6 +1138,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   if (const char* g = std::getenv("MHAR_TC_GROUP")) c->tc_group_n = std::max(1, std::atoi(g));
   if (const char* g = std::getenv("MHAR_TC_APOL")) c->tc_a_policy = std::atoi(g) % 3;
   if (const char* g = std::getenv("MHAR_TC_F16")) c->tc_f16 = std::atoi(g) != 0;
+  if (const char* g = std::getenv("MHAR_I8_GROUP")) c->i8_group = std::max(1, std::atoi(g));
   if ((st = dalloc(c, &c->redraw_scratch, (size_t)c->redraw_grid * 3 * c->n))) return bail(st);
   if (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) {
     const size_t cache = (size_t)c->m_pad * c->z_pad;

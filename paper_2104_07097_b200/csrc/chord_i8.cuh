@@ -186,16 +186,51 @@ struct I8Params {
   int64_t z;           // live walks
   double eps_dir;
   unsigned long long* prof;  // optional per-CTA wait-cycle counters (MHAR_I8_PROFILE), or null
+  unsigned* sched;     // unit tickets [next, finished clusters]; zero between launches
+  int group;           // rasterisation band: row groups per band (1: walk pairs innermost)
 };
 
-// cluster unit u -> (row tile of pair pp, walk-tile pair): walk pairs inner,
-// so the clusters in flight share a few A tiles and every direction tile stays
-// L2-resident; the pairs of a cluster take adjacent row tiles
+constexpr int I8_UQ = 8;  // announced-unit queue per CTA (> the producer's lead in units)
+
+// Ticketed unit order (as chord2_kernel): the cluster's CTA 0 producer draws
+// the next cluster unit from a global counter and announces it -- or the end,
+// -1 -- to every CTA of the cluster (a DSMEM store into each CTA's queue slot
+// and a release arrive on its slot barrier); every role of every CTA follows
+// that queue.  Units stay in order across the clusters, so the direction
+// slices and the A slices in flight stay L2-resident (the static order drifted
+// apart over ~340 units per cluster).
+__device__ inline long long i8_next_unit(const I8Params& p, int64_t n_units) {
+  const long long u = (long long)atomicAdd(p.sched, 1u);
+  if (u < n_units) return u;
+  if (atomicAdd(p.sched + 1, 1u) == gridDim.x / I8_CL - 1) {
+    p.sched[0] = 0u;
+    p.sched[1] = 0u;
+  }
+  return -1;
+}
+__device__ inline void st_cluster_s64(uint32_t addr, long long v) {
+  asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ inline void mbar_arrive_remote_release(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
+               : "memory");
+}
+
+// cluster unit u -> (row tile of pair pp, walk-tile pair): bands of `group`
+// row groups, row groups inner -- the units in flight cover the band's A
+// slices and a few walk pairs' direction slices, each read from DRAM about
+// once per band (group 1: walk pairs innermost, every row tile sweeping all
+// direction slices); the pairs of a cluster take adjacent row tiles
 __device__ inline void i8_unit(int64_t u, int pp, const I8Params& p, int64_t* rt, int64_t* wp) {
   const int64_t pairs = p.walk_tiles / 2;
-  const int64_t rg = u / pairs;
-  *rt = rg * I8_PAIRS + pp;
-  *wp = u - rg * pairs;
+  const int64_t rgs = p.row_tiles / I8_PAIRS;
+  const int64_t band_units = (int64_t)p.group * pairs;
+  const int64_t band = u / band_units;
+  const int64_t in_band = u - band * band_units;
+  const int64_t start = band * p.group;
+  const int64_t h = (rgs - start < p.group) ? rgs - start : p.group;
+  *rt = (start + in_band % h) * I8_PAIRS + pp;
+  *wp = in_band / h;
 }
 
 __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
@@ -211,7 +246,9 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
   uint64_t* tempty = tfull + 1;             // a pass's accumulators drained (leader, 32 warps)
   uint64_t* sr_full = tempty + 1;           // [I8_SR_SLOTS] slack/rate chunk landed
   uint64_t* sr_empty = sr_full + I8_SR_SLOTS;  // [I8_SR_SLOTS] chunk consumed (4 warps)
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(sr_empty + I8_SR_SLOTS);
+  uint64_t* uready = sr_empty + I8_SR_SLOTS;     // [I8_UQ] unit announced
+  long long* uq = reinterpret_cast<long long*>(uready + I8_UQ);  // [I8_UQ] the units
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(uq + I8_UQ);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t crank = cluster_rank();
@@ -220,10 +257,13 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
   const uint32_t lead = crank & ~1u;        // the pair's MMA-issuing CTA
   const unsigned short pair_mask = (unsigned short)(3u << (2 * pp));
   const unsigned short all_mask = (unsigned short)((1u << I8_CL) - 1);
-  const int64_t cl = blockIdx.x / I8_CL, ncl = gridDim.x / I8_CL;
   const int64_t n_units = p.row_tiles / I8_PAIRS * (p.walk_tiles / 2);
-  const int my_units = (cl < n_units) ? (int)((n_units - 1 - cl) / ncl + 1) : 0;
   const int KS = (int)p.KS;
+  // the cluster's ui-th unit (waits for its announcement; -1: no more)
+  auto unit_at = [&](int ui) -> long long {
+    mbar_wait(&uready[ui % I8_UQ], (uint32_t)((ui / I8_UQ) & 1));
+    return uq[ui % I8_UQ];
+  };
 
   if (tid == 0) {
     for (int s = 0; s < I8_STAGES; ++s) {
@@ -237,6 +277,7 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
       mbar_init(&sr_full[s], 1);
       mbar_init(&sr_empty[s], 4);
     }
+    for (int s = 0; s < I8_UQ; ++s) mbar_init(&uready[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -258,9 +299,24 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
       const uint64_t apol = policy_evict_normal();
       int stage = 0, round = 0;
       long long w_empty = 0;
-      for (int ui = 0; ui < my_units; ++ui) {
+      auto announce = [&](int k, long long u) {  // cluster CTA 0 only
+        const int slot = k % I8_UQ;
+        uq[slot] = u;
+        for (uint32_t r = 1; r < (uint32_t)I8_CL; ++r) {
+          uint32_t ra, rb;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&uq[slot])), "r"(r));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&uready[slot])), "r"(r));
+          st_cluster_s64(ra, u);
+          mbar_arrive_remote_release(rb);
+        }
+        mbar_arrive(&uready[slot]);
+      };
+      if (crank == 0) announce(0, i8_next_unit(p, n_units));
+      for (int ui = 0;; ++ui) {
+        const long long u = unit_at(ui);
+        if (u < 0) break;
         int64_t rt, wp;
-        i8_unit(cl + (int64_t)ui * ncl, pp, p, &rt, &wp);
+        i8_unit(u, pp, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
 #if MHAR_I8_PREFETCH
         {
@@ -301,6 +357,8 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
                 ++round;
               }
             }
+        // this unit's loads are queued: draw the next one for the cluster
+        if (crank == 0) announce(ui + 1, i8_next_unit(p, n_units));
       }
       if (p.prof) p.prof[8 * blockIdx.x + 4] = (unsigned long long)w_empty;
     } else if (warp == 1 && lane == 0 && rank == 0) {
@@ -308,7 +366,7 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
       int stage = 0, phase = 0;
       long long w_tempty = 0, w_full = 0, w_peer = 0;
       const long long t_start = clock64();
-      for (int ui = 0; ui < my_units; ++ui) {
+      for (int ui = 0; unit_at(ui) >= 0; ++ui) {
         for (int pi = 0; pi < 2; ++pi) {  // the long pass (levels 4..7) first
           const int pass = 1 - pi;
           const int ph = 2 * ui + pi;  // accumulator phase
@@ -379,21 +437,23 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
     } else if (warp == 1 && lane == 0) {
       // ---------------- relay (odd CTA): my slot landed -> leader ----------------
       int stage = 0, phase = 0;
-      const int slots = my_units * 3 * KS;  // short pass: 1 slot per k step, long pass: 2
-      for (int i = 0; i < slots; ++i) {
-        mbar_wait(&full[stage], (uint32_t)phase);
-        mbar_arrive_remote(&peer_full[stage], lead);
-        if (++stage == I8_STAGES) {
-          stage = 0;
-          phase ^= 1;
+      for (int ui = 0; unit_at(ui) >= 0; ++ui)
+        for (int i = 0; i < 3 * KS; ++i) {  // short pass: 1 slot per k step, long pass: 2
+          mbar_wait(&full[stage], (uint32_t)phase);
+          mbar_arrive_remote(&peer_full[stage], lead);
+          if (++stage == I8_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
         }
-      }
     } else if (warp == 2 && lane == 0) {
       // ---------------- loader: this CTA's slack/rate blocks -> smem ----------------
       const uint64_t stream_policy = MHAR_STREAM_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();
-      for (int ui = 0; ui < my_units; ++ui) {
+      for (int ui = 0;; ++ui) {
+        const long long u = unit_at(ui);
+        if (u < 0) break;
         int64_t rt, wp;
-        i8_unit(cl + (int64_t)ui * ncl, pp, p, &rt, &wp);
+        i8_unit(u, pp, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
         const int64_t cb = (rt * p.walk_tiles + wt) * (int64_t)(I8_N * I8_M);
         for (int j = 0; j < I8_ROWS_PER_WARP / I8_SR_ROWS; ++j)
@@ -428,9 +488,11 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
           mbar_arrive_remote(tempty, lead);
       }
     };
-    for (int ui = 0; ui < my_units; ++ui) {
+    for (int ui = 0;; ++ui) {
+      const long long u = unit_at(ui);
+      if (u < 0) break;
       int64_t rt, wp;
-      i8_unit(cl + (int64_t)ui * ncl, pp, p, &rt, &wp);
+      i8_unit(u, pp, p, &rt, &wp);
       const int64_t wt = 2 * wp + rank;
       const int64_t c = wt * I8_M + wl;
       const int64_t r0 = rt * I8_N + rq * I8_ROWS_PER_WARP;

@@ -1,6 +1,12 @@
-libs=${LIBS:-"tools/ab_i8p1.so paper_2104_07097_b200/lib/libmhar_b200.so"}
-for i in 1 2 3; do
-  for lib in $libs; do
-    MHAR_LIB=$lib timeout 120 python bench.py --f64-engine int8 --no-i8 --no-fp32 --no-cpu --e2e-steps 1 --steps 10 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().splitlines()[-1]);print('$lib', round(d['roofline']['avg_launch_ms'],3), d['clocks']['sm_mhz'])"
+# A/B of the int8-slice engine between engine builds (LIBS), 2 rounds, + ncu traffic per build
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct
+for lib in ${LIBS:-tools/ab_base.so}; do
+  MHAR_LIB=$lib ncu --metrics $M --clock-control none -k regex:chord_i8 --launch-skip 2 -c 1 --csv \
+    --log-file gpurun_out/i8_$(basename $lib .so).csv python bench.py --f64-engine int8 --steps 4 \
+    --warmup 3 --no-cpu --no-fp32 --no-i8 --e2e-steps 1 > /dev/null 2>&1
+done
+for i in 1 2; do
+  for lib in ${LIBS:-tools/ab_base.so}; do
+    MHAR_LIB=$lib timeout 300 python bench.py --f64-engine int8 --no-i8 --no-fp32 --no-cpu --e2e-steps 1 --steps 10 2>/dev/null | python -c "import json,sys;d=json.loads(sys.stdin.read().splitlines()[-1]);print('$lib', round(d['roofline']['avg_launch_ms'],3), d['clocks']['sm_mhz'], round(d['value']))"
   done
 done
