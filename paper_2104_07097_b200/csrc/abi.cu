@@ -411,6 +411,7 @@ int launch_tc32(mhar_ctx* c) {
   p.tmDhi = c->tm_dhi;
   p.tmDlo = c->tm_dlo;
   p.use_tma = c->tc_tma ? 1 : 0;
+  p.sched = c->sched + 4;  // its own ticket pair
   if (c->tc_prof) cudaMemsetAsync(c->tc_prof, 0, kProfWords * sizeof(unsigned long long) * c->num_sms, c->stream);
   const int64_t units = p.row_tiles * (p.walk_tiles / 2);  // (row tile, walk-tile pair)
   const int grid = 2 * (int)std::min<int64_t>(units, c->num_sms / 2);  // CTA pairs
@@ -1130,7 +1131,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
       (st = dalloc(c, &c->first_bad, 1)) || (st = dalloc(c, &c->err, 1)) ||
       (st = dalloc(c, &c->redraw_total, 1)) || (st = dalloc(c, &c->col_state, c->z_pad)) ||
       (st = dalloc(c, &c->theta_state, 1)) || (st = dalloc(c, &c->x0, c->n)) ||
-      (st = dalloc(c, &c->injected_u, c->z_pad)) || (st = dalloc(c, &c->sched, 4)))
+      (st = dalloc(c, &c->injected_u, c->z_pad)) || (st = dalloc(c, &c->sched, 6)))
     return bail(st);
   c->redraw_grid = (int)std::min<int64_t>(c->z, c->num_sms);
   if (const char* g = std::getenv("MHAR_GROUP_M")) c->group_m = std::max(1, std::atoi(g));

@@ -190,31 +190,9 @@ struct I8Params {
   int group;           // rasterisation band: row groups per band (1: walk pairs innermost)
 };
 
-constexpr int I8_UQ = 8;  // announced-unit queue per CTA (> the producer's lead in units)
-
-// Ticketed unit order (as chord2_kernel): the cluster's CTA 0 producer draws
-// the next cluster unit from a global counter and announces it -- or the end,
-// -1 -- to every CTA of the cluster (a DSMEM store into each CTA's queue slot
-// and a release arrive on its slot barrier); every role of every CTA follows
-// that queue.  Units stay in order across the clusters, so the direction
-// slices and the A slices in flight stay L2-resident (the static order drifted
-// apart over ~340 units per cluster).
-__device__ inline long long i8_next_unit(const I8Params& p, int64_t n_units) {
-  const long long u = (long long)atomicAdd(p.sched, 1u);
-  if (u < n_units) return u;
-  if (atomicAdd(p.sched + 1, 1u) == gridDim.x / I8_CL - 1) {
-    p.sched[0] = 0u;
-    p.sched[1] = 0u;
-  }
-  return -1;
-}
-__device__ inline void st_cluster_s64(uint32_t addr, long long v) {
-  asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
-__device__ inline void mbar_arrive_remote_release(uint32_t remote_bar) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
-               : "memory");
-}
+// the ticketed unit order of the tcgen05 kernels (chord_tc32.cuh
+// cluster_next_unit / cluster_announce / cluster_unit_at), one queue per CTA
+constexpr int I8_UQ = TC_UQ;
 
 // cluster unit u -> (row tile of pair pp, walk-tile pair): bands of `group`
 // row groups, row groups inner -- the units in flight cover the band's A
@@ -260,10 +238,7 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
   const int64_t n_units = p.row_tiles / I8_PAIRS * (p.walk_tiles / 2);
   const int KS = (int)p.KS;
   // the cluster's ui-th unit (waits for its announcement; -1: no more)
-  auto unit_at = [&](int ui) -> long long {
-    mbar_wait(&uready[ui % I8_UQ], (uint32_t)((ui / I8_UQ) & 1));
-    return uq[ui % I8_UQ];
-  };
+  auto unit_at = [&](int ui) -> long long { return cluster_unit_at(uq, uready, ui); };
 
   if (tid == 0) {
     for (int s = 0; s < I8_STAGES; ++s) {
@@ -299,19 +274,9 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
       const uint64_t apol = policy_evict_normal();
       int stage = 0, round = 0;
       long long w_empty = 0;
-      auto announce = [&](int k, long long u) {  // cluster CTA 0 only
-        const int slot = k % I8_UQ;
-        uq[slot] = u;
-        for (uint32_t r = 1; r < (uint32_t)I8_CL; ++r) {
-          uint32_t ra, rb;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&uq[slot])), "r"(r));
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&uready[slot])), "r"(r));
-          st_cluster_s64(ra, u);
-          mbar_arrive_remote_release(rb);
-        }
-        mbar_arrive(&uready[slot]);
-      };
-      if (crank == 0) announce(0, i8_next_unit(p, n_units));
+      const unsigned nclusters = gridDim.x / I8_CL;
+      auto announce = [&](int k, long long u) { cluster_announce(uq, uready, k, u, I8_CL); };
+      if (crank == 0) announce(0, cluster_next_unit(p.sched, n_units, nclusters));
       for (int ui = 0;; ++ui) {
         const long long u = unit_at(ui);
         if (u < 0) break;
@@ -358,7 +323,7 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
               }
             }
         // this unit's loads are queued: draw the next one for the cluster
-        if (crank == 0) announce(ui + 1, i8_next_unit(p, n_units));
+        if (crank == 0) announce(ui + 1, cluster_next_unit(p.sched, n_units, nclusters));
       }
       if (p.prof) p.prof[8 * blockIdx.x + 4] = (unsigned long long)w_empty;
     } else if (warp == 1 && lane == 0 && rank == 0) {

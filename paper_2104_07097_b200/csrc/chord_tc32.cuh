@@ -253,6 +253,7 @@ struct TcParams {
   // lands on the LEADER's full barrier -- no relay hop through the odd CTA.
   CUtensorMap tmAhi, tmAlo, tmDhi, tmDlo;
   int use_tma;
+  unsigned* sched;  // unit tickets [next, finished pairs]; zero between launches
 };
 
 // one 8 KB piece (float offset `off`, a multiple of 2048) into this CTA's
@@ -265,6 +266,51 @@ __device__ inline void tma_piece_2cta(void* dst, const CUtensorMap* tm, int64_t 
       ".L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(dst)),
       "l"(tm), "r"(0), "r"((int)(off >> 6)), "r"(bar_leader), "l"(policy)
       : "memory");
+}
+
+// ---- ticketed unit order shared by the tcgen05 kernels (chord_tc32, chord_i8) ----
+// The cluster's CTA 0 producer draws the next unit from a global counter and
+// announces it (or the end, -1) to every CTA of its cluster: a DSMEM store
+// into each CTA's queue slot and a release arrive on its slot barrier; every
+// role of every CTA follows that queue.  Units stay in order across clusters,
+// so the operand tiles in flight stay L2-resident (a static unit-per-cluster
+// assignment drifts apart over a few hundred units).  The last cluster to
+// draw past the end rewinds the counter for the next launch.
+constexpr int TC_UQ = 8;  // announced-unit queue per CTA (> the producer's lead in units)
+__device__ inline long long cluster_next_unit(unsigned* sched, int64_t n_units, unsigned nclusters) {
+  const long long u = (long long)atomicAdd(sched, 1u);
+  if (u < n_units) return u;
+  if (atomicAdd(sched + 1, 1u) == nclusters - 1) {
+    sched[0] = 0u;
+    sched[1] = 0u;
+  }
+  return -1;
+}
+__device__ inline void st_cluster_s64(uint32_t addr, long long v) {
+  asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ inline void mbar_arrive_remote_release(uint32_t remote_bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote_bar)
+               : "memory");
+}
+// unit u into queue slot k % TC_UQ of all `ncta` CTAs of the cluster (caller: CTA 0)
+__device__ inline void cluster_announce(long long* uq, uint64_t* uready, int k, long long u,
+                                        int ncta) {
+  const int slot = k % TC_UQ;
+  uq[slot] = u;
+  for (int r = 1; r < ncta; ++r) {
+    uint32_t ra, rb;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32(&uq[slot])), "r"(r));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(smem_u32(&uready[slot])), "r"(r));
+    st_cluster_s64(ra, u);
+    mbar_arrive_remote_release(rb);
+  }
+  mbar_arrive(&uready[slot]);
+}
+// the cluster's k-th unit (waits for its announcement; -1: no more)
+__device__ inline long long cluster_unit_at(const long long* uq, uint64_t* uready, int k) {
+  mbar_wait(&uready[k % TC_UQ], (uint32_t)((k / TC_UQ) & 1));
+  return uq[k % TC_UQ];
 }
 
 // unit u -> (row tile, walk-tile pair), banded over group_n row tiles; with
@@ -308,13 +354,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* peer_full = empty + kStages;  // leader: the odd CTA's stage landed
   uint64_t* tfull = peer_full + kStages;  // [2] accumulator ready (both CTAs)
   uint64_t* tempty = tfull + 2;             // [2] accumulator drained (leader, 8 warps)
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* uready = tempty + 2;            // [TC_UQ] unit announced
+  long long* uq = reinterpret_cast<long long*>(uready + TC_UQ);  // [TC_UQ] the units
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(uq + TC_UQ);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
-  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const int64_t n_units = p.row_tiles * (p.walk_tiles / 2);
-  const int my_units = (pair < n_units) ? (int)((n_units - 1 - pair) / npairs + 1) : 0;
   const int KT = (int)p.KT;
 
   if (tid == 0) {
@@ -327,6 +373,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 2 * TC_EPI_WARPS);  // every epilogue warp of both CTAs
     }
+    for (int s = 0; s < TC_UQ; ++s) mbar_init(&uready[s], 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -349,9 +396,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                                               : policy_evict_normal();
       int stage = 0, round = 0;
       long long w_empty = 0;
-      for (int ui = 0; ui < my_units; ++ui) {
+      const unsigned npairs = gridDim.x >> 1;
+      if (rank == 0) cluster_announce(uq, uready, 0, cluster_next_unit(p.sched, n_units, npairs), 2);
+      for (int ui = 0;; ++ui) {
+        const long long u = cluster_unit_at(uq, uready, ui);
+        if (u < 0) break;
         int64_t rt, wp;
-        tc_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+        tc_unit(u, p, &rt, &wp);
         const int64_t wt = 2 * wp + rank;
 #if MHAR_TC_PREFETCH
         {
@@ -396,6 +447,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             ++round;
           }
         }
+        // this unit's loads are queued: draw the pair's next unit
+        if (rank == 0)
+          cluster_announce(uq, uready, ui + 1, cluster_next_unit(p.sched, n_units, npairs), 2);
       }
       if (p.prof) p.prof[8 * blockIdx.x + 4] = (unsigned long long)w_empty;
     }
@@ -405,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       int stage = 0, phase = 0;
       long long w_tempty = 0, w_full = 0, w_peer = 0;
       const long long t_start = clock64();
-      for (int ui = 0; ui < my_units; ++ui) {
+      for (int ui = 0; cluster_unit_at(uq, uready, ui) >= 0; ++ui) {
         const int ab = ui & 1;
         const long long t0 = clock64();
         if (ui >= 2) mbar_wait_relaxed(&tempty[ab], (uint32_t)(((ui >> 1) - 1) & 1));
@@ -463,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     } else if (lane == 0 && !p.use_tma) {
       // ---------------- relay (odd CTA): my stage landed -> leader ----------------
       int stage = 0, phase = 0;
-      for (int ui = 0; ui < my_units; ++ui)
+      for (int ui = 0; cluster_unit_at(uq, uready, ui) >= 0; ++ui)
         for (int kt = 0; kt < KT; ++kt) {
           mbar_wait(&full[stage], (uint32_t)phase);
           mbar_arrive_remote(&peer_full[stage], 0);
@@ -480,9 +534,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     const int wl = q * 32 + lane;                // walk within this CTA's tile
     const uint64_t stream_policy = MHAR_STREAM_EVICT_FIRST ? policy_evict_first() : policy_evict_normal();  // the slack stream must not evict A
     const float eps = (float)p.eps_dir, mu = (float)p.margin;
-    for (int ui = 0; ui < my_units; ++ui) {
+    for (int ui = 0;; ++ui) {
+      const long long u = cluster_unit_at(uq, uready, ui);
+      if (u < 0) break;
       int64_t rt, wp;
-      tc_unit(pair + (int64_t)ui * npairs, p, &rt, &wp);
+      tc_unit(u, p, &rt, &wp);
       const int64_t wt = 2 * wp + rank;
       const int ab = ui & 1;
       const long long e0 = clock64();

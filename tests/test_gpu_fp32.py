@@ -182,3 +182,19 @@ def test_fp32_with_equalities_stays_on_the_slice_and_inside():
         X = eng.get_state()
     assert np.abs(a_eq @ X).max() <= 1e-9
     assert np.abs(X).max() > 0.05
+
+
+def test_fp32_relay_path_without_tma(monkeypatch, form):
+    # MHAR_TC_TMA=0: plain bulk copies and the odd CTA's "stage landed" relay
+    # (the round-1 protocol) -- the same trajectory as the 2-CTA TMA loads
+    p = workloads.random_polytope(300, 5000, seed=21)
+    out = {}
+    for tma in ("1", "0"):
+        monkeypatch.setenv("MHAR_TC_TMA", tma)
+        with mh.Engine(p, 512, seed=8, precision=32) as eng:
+            eng.set_state(np.zeros((300, 512)))
+            eng.step(12)
+            out[tma] = eng.get_state()
+            bad, viol, _ = eng.check_state(1e-9)
+            assert bad == -1 and viol.max() <= 0.0
+    np.testing.assert_array_equal(out["1"], out["0"])
