@@ -112,3 +112,30 @@ def test_group_errors():
         with pytest.raises(mh.MharError) as e1:
             eng.step(1)
     assert str(e.value) == str(e1.value)
+
+
+def test_group_state_round_trip_and_no_collection():
+    p = workloads.random_polytope(30, 500, seed=2)
+    z = 97
+    X = np.asfortranarray(np.random.default_rng(0).uniform(-0.01, 0.01, (30, z)))
+    with mh.Group(p, z, [0, 0, 0], seed=3) as g:
+        g.set_state(X)
+        assert np.array_equal(g.get_state(), X)
+        S, st = g.run(np.zeros(30), phi=5, windows=2, collect=False)
+        assert S is None and st.iterate_count == z * 5 * 2
+        with pytest.raises(mh.MharError) as e:
+            g.set_state(np.zeros((30, z + 1)))
+        assert e.value.code == mh.ErrorCode.dimension_mismatch
+        with pytest.raises(mh.MharError):
+            g.run(np.zeros(29), phi=5, windows=1)
+
+
+def test_group_reference_streams_single_device():
+    # one device may keep the reference's own streams (bit-exact uniforms):
+    # the group over [0] equals a context on the same streams
+    p = mh.make_hypercube(4)
+    with mh.Engine(p, 3, seed=99, rng="reference") as eng:
+        ref, _ = eng.run(np.zeros(4), phi=10, windows=3, burn_in=10)
+    with mh.Group(p, 3, [0], seed=99, rng="reference") as g:
+        got, _ = g.run(np.zeros(4), phi=10, windows=3, burn_in=10)
+    assert np.array_equal(got, ref)
