@@ -23,6 +23,7 @@
 
 #include "../../include/mhar_b200.h"
 #include "chord_kernel.cuh"
+#include "chord3_kernel.cuh"
 #include "engine_internal.h"
 #include "host_linalg.h"
 #include "lp.h"
@@ -101,6 +102,8 @@ struct mhar_ctx {
   int *first_reject = nullptr, *first_bad = nullptr;
   unsigned long long *err = nullptr, *redraw_total = nullptr;
   unsigned* sched = nullptr;  // chord2 unit tickets (chord_kernel.cuh next_unit)
+  bool c3 = false;            // incremental DMMA chord on chord3_kernel (MHAR_CHORD3=0: chord2)
+  unsigned long long* c3_prof = nullptr;  // MHAR_C3_PROFILE: chord3 phase counters, 16 per CTA
   uint64_t *col_state = nullptr, *theta_state = nullptr;
   int redraw_grid = 1;
   int group_m = 16;  // chord-kernel rasterisation band (m tiles); MHAR_GROUP_M overrides
@@ -291,6 +294,8 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   p.cache_rows = c->cache_rows;
   p.rate_f32 = c->Ahi != nullptr;
   p.sched = c->sched;
+  p.c3_tiles = c->c3 ? c->z_pad / C3_BW : 0;
+  p.prof = c->c3_prof;
   return p;
 }
 
@@ -357,7 +362,15 @@ int launch_chord(mhar_ctx* c, int mode, const double* X) {
       chord_kernel<FUSED_STORE><<<grid, CHORD_THREADS, CHORD_SMEM, c->stream>>>(p);
       break;
     case INCREMENTAL:
-      chord2_kernel<INCREMENTAL><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
+      if (c->c3) {
+        const int g3 = (int)std::min<int64_t>(p.m_tiles * p.c3_tiles, c->num_sms);
+        if (p.prof)
+          chord3_kernel<true><<<g3, C3_THREADS, C3_SMEM, c->stream>>>(p);
+        else
+          chord3_kernel<false><<<g3, C3_THREADS, C3_SMEM, c->stream>>>(p);
+      }
+      else
+        chord2_kernel<INCREMENTAL><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
       break;
     case SLACK_STORE:
       chord2_kernel<SLACK_STORE><<<grid, CHORD_THREADS, CHORD2_SMEM, c->stream>>>(p);
@@ -561,6 +574,7 @@ int launch_redraw(mhar_ctx* c) {
   rp.R = (c->opt.slack_mode == MHAR_SLACK_INCREMENTAL) ? c->R : nullptr;
   rp.ct64 = c->ct64;
   rp.tc_walk_tiles = c->tc_walk_tiles;
+  rp.c3_tiles = c->c3 ? c->z_pad / C3_BW : 0;
   rp.cache_rows = c->cache_rows;
   rp.rate_f32 = c->Ahi != nullptr;
   rp.scratch = c->redraw_scratch;
@@ -1102,7 +1116,18 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   c->KT = c->n_pad / BK;
   c->m_pad = round_up(c->m, fp32 ? TC_N : i8 ? (int64_t)I8_N * I8_PAIRS : BM);
   c->m_tiles = c->m_pad / BM;
-  c->z_pad = round_up(c->z, tiles ? 2 * TC_M : 64);  // tcgen05: whole CTA-pair walk tiles
+  // the incremental DMMA chord runs chord3_kernel (128-walk units, TMEM
+  // hand-off to separate epilogue warps) when the dimension is large enough
+  // for the unit's MMA time to cover its epilogue (n_pad >= 768; measured:
+  // n = 1000 / 2000 gain 3.5 / 1.7 points of DMMA peak, n = 500 loses 2.4),
+  // else chord2 (64-walk units, in-register epilogue).  MHAR_CHORD3=0 / 1
+  // forces either.
+  {
+    const char* c3e = std::getenv("MHAR_CHORD3");
+    const bool eligible = !tiles && diag_coef.empty() && c->opt.slack_mode == MHAR_SLACK_INCREMENTAL;
+    c->c3 = eligible && (c3e ? std::atoi(c3e) != 0 : c->n_pad >= 768);
+  }
+  c->z_pad = round_up(c->z, tiles ? 2 * TC_M : c->c3 ? C3_BW : 64);  // whole kernel walk tiles
   c->ct64 = c->z_pad / 64;
   if (tiles) {
     c->tc_row_tiles = c->m_pad / TC_N;
@@ -1347,6 +1372,10 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   cudaFuncSetAttribute(chord_kernel<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
   cudaFuncSetAttribute(chord_kernel<FUSED_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD_SMEM);
   cudaFuncSetAttribute(chord2_kernel<INCREMENTAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
+  cudaFuncSetAttribute(chord3_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C3_SMEM);
+  cudaFuncSetAttribute(chord3_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C3_SMEM);
+  if (c->c3 && std::getenv("MHAR_C3_PROFILE") && (st = dalloc(c, &c->c3_prof, 16 * (size_t)c->num_sms)))
+    return bail(st);
   cudaFuncSetAttribute(chord2_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   cudaFuncSetAttribute(chord2_kernel<SLACK_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   if (c->Acm) {
@@ -1374,6 +1403,23 @@ int mhar_ctx_destroy(mhar_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graph(c);
   if (c->tc_prof) report_tc_profile(c);
+  if (c->c3_prof) {
+    // chord3 phase cycles summed over every launch of this context (MMA warps
+    // and epilogue warps, each counter per warp, summed over the CTAs)
+    std::vector<unsigned long long> h(16 * (size_t)c->num_sms);
+    if (cudaMemcpy(h.data(), c->c3_prof, h.size() * 8, cudaMemcpyDeviceToHost) == cudaSuccess) {
+      double t[6] = {0, 0, 0, 0, 0, 0};
+      for (int b = 0; b < c->num_sms; ++b)
+        for (int k = 0; k < 6; ++k) t[k] += (double)h[16 * b + k];
+      const double mma = t[0] + t[2] + t[3];
+      std::fprintf(stderr,
+                   "[chord3 profile] MMA warps: mainloop %.1f%% (of which full-barrier waits "
+                   "%.1f%%), TMEM-empty waits %.1f%%, TMEM stores %.1f%%; epilogue warps: waiting "
+                   "for tiles %.1f%%, working %.1f%%\n",
+                   100 * t[0] / mma, 100 * t[1] / mma, 100 * t[2] / mma, 100 * t[3] / mma,
+                   100 * t[4] / (t[4] + t[5]), 100 * t[5] / (t[4] + t[5]));
+    }
+  }
   for (auto& ev : c->pending) {
     cudaEventDestroy(ev.first);
     cudaEventDestroy(ev.second);

@@ -91,11 +91,14 @@ struct ChordParams {
   int64_t cache_rows;     // its row tile: 256 (fp32 variant, fp32 rates) or 64 (int8 slices)
   int rate_f32;           // 1: the rate cache holds fp32 (fp32 variant)
   unsigned* sched;        // chord2 unit tickets [next, finished CTAs]; zero between launches
+  int64_t c3_tiles;       // > 0: the DMMA slack cache is chord3's (c3_index over 128-walk tiles)
+  unsigned long long* prof;  // chord3 per-CTA phase cycle counters (MHAR_C3_PROFILE), or null
 };
 
 // Slack-cache index for FUSED_STORE: the layout of whichever kernel consumes it.
 __device__ inline int64_t cache_index(int64_t r, int64_t c, const ChordParams& p) {
   if (p.tc_walk_tiles > 0) return tile_cache_index(r, c, p.tc_walk_tiles, p.cache_rows);
+  if (p.c3_tiles > 0) return c3_index(r, c, p.c3_tiles);
   return s_index(r, c, p.col_tiles);
 }
 
@@ -145,6 +148,49 @@ __device__ __forceinline__ void scan_row(double sl, double ad, double eps, doubl
       lo = q > lo ? q : lo;
     }
   }
+}
+
+// scan_row with the fp64 pipe kept free for the tensor cores.  DMMA and the
+// fp64 SIMT instructions (DFMA, DSETP) issue on the same fp64 datapath, so an
+// epilogue doing its comparisons in fp64 takes cycles from the MMAs of the
+// co-resident warps.  Here the sign and |ad| > eps tests are integer compares
+// of the bit patterns, and an integer log-domain estimate skips rows whose
+// ratio is provably beyond the current bound: for positive normal x the bit
+// pattern B(x) / 2^52 - 1023 is within 0.0861 below log2 x, so
+// B(sl) - B(ad) > B(bound) - B(1) + 0.2 * 2^52 implies sl / ad > bound
+// exactly (the row cannot move it).  Every other row takes scan_row's exact
+// path (fma filter, division), so the bounds are bit-identical to scan_row.
+__device__ __forceinline__ void scan_row_int(double sl, double ad, long long epsb, double& hi,
+                                             double& lo, unsigned& sd) {
+  constexpr long long kOne = 0x3FF0000000000000LL;     // B(1.0)
+  constexpr long long kMargin = 0x0003333333333333LL;  // 0.2 in log2 units
+  constexpr long long kInf = 0x7FF0000000000000LL;
+  const long long A = __double_as_longlong(ad), S = __double_as_longlong(sl);
+  const long long Aabs = A & 0x7FFFFFFFFFFFFFFFLL;
+  if (Aabs <= epsb) return;  // |ad| <= eps_dir: the row is skipped (chord_scan)
+  if (A > 0) {
+    sd |= 1u;
+    const long long H = __double_as_longlong(hi);
+    if (S >= 0 && H < kInf && S - A > H - kOne + kMargin) return;
+    if (!(fma(-hi, ad, sl) > 0.0)) {
+      const double q = sl / ad;
+      hi = q < hi ? q : hi;
+    }
+  } else {
+    sd |= 2u;
+    const long long L = __double_as_longlong(lo) & 0x7FFFFFFFFFFFFFFFLL;
+    if (S >= 0 && L < kInf && S - Aabs > L - kOne + kMargin) return;
+    if (!(fma(-lo, ad, sl) >= 0.0)) {
+      const double q = sl / ad;
+      lo = q > lo ? q : lo;
+    }
+  }
+}
+// running max of -s as an order-preserving integer key (no fp64 instruction)
+__device__ __forceinline__ void viol_key_update(long long& vk, double s) {
+  const long long b = __double_as_longlong(s) ^ (long long)0x8000000000000000ULL;  // bits of -s
+  const long long k = b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
+  vk = k > vk ? k : vk;
 }
 
 // Warp reduction over the 8 row lanes sharing (lane & 3), then one atomic per

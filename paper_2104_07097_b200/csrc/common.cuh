@@ -71,6 +71,17 @@ __host__ __device__ inline int64_t tile_cache_index(int64_t r, int64_t c, int64_
   return (((r / rows) * WT + c / 128) * rows + r % rows) * 128 + c % 128;
 }
 
+// Slack/rate cache of chord3_kernel (128-row x 128-walk units, 8 warps of
+// 64 x 32 DMMA tiles): [unit][warp(8)][i(8)][j(4)][lane(32)][2] -- the
+// accumulator fragment order, one coalesced 512-byte block per (warp, i, j).
+__host__ __device__ inline int64_t c3_index(int64_t r, int64_t c, int64_t CT128) {
+  const int64_t mt = r / 128, rr = r % 128, wm = rr / 64, i = (rr % 64) / 8, rq = rr % 8;
+  const int64_t ct = c / 128, cc = c % 128, wn = cc / 32, j = (cc % 32) / 8, cq = (cc % 8) / 2,
+                e = cc % 2;
+  const int64_t warp = wm * 4 + wn, lane = rq * 4 + cq;
+  return (((((mt * CT128 + ct) * 8 + warp) * 8 + i) * 4 + j) * 32 + lane) * 2 + e;
+}
+
 __host__ __device__ inline int64_t s_index(int64_t r, int64_t c, int64_t CT64) {
   const int64_t mt = r / BM, rr = r % BM, wm = rr / 32, i = (rr % 32) / 8, rq = rr % 8;
   const int64_t ct = c / BC, cc = c % BC, wn = cc / 32, j = (cc % 32) / 8, cq = (cc % 8) / 2,

@@ -319,6 +319,7 @@ struct RedrawParams {
   double* R;              // incremental rate cache (s_index) or null
   int64_t ct64;
   int64_t tc_walk_tiles;  // > 0: tcgen05 tile cache layout (tile_cache_index)
+  int64_t c3_tiles;       // > 0: chord3's cache layout (c3_index)
   int64_t cache_rows;     // its row tile
   int rate_f32;           // 1: fp32 rate cache (fp32 variant)
   double* scratch;        // 3 n doubles per CTA
@@ -437,6 +438,8 @@ __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
               (float)ad;
         else if (rp.R && rp.tc_walk_tiles > 0)  // int8-slice engine: fp64 rates, tile layout
           rp.R[tile_cache_index(r, c, rp.tc_walk_tiles, rp.cache_rows)] = ad;
+        else if (rp.R && rp.c3_tiles > 0)
+          rp.R[c3_index(r, c, rp.c3_tiles)] = ad;
         else if (rp.R)
           rp.R[s_index(r, c, rp.ct64)] = ad;
         if (ad > rp.eps_dir) {

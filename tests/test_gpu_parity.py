@@ -272,6 +272,28 @@ def test_incremental_matches_recompute():
     assert np.abs(out["incremental"] - out["recompute"]).max() <= 1e-9
 
 
+@pytest.mark.parametrize("n,m,z", [(64, 3000, 300), (200, 5000, 1000), (800, 9000, 257)])
+def test_chord3_equals_chord2(monkeypatch, n, m, z):
+    # The two incremental DMMA chord kernels (chord3: 128-walk units with the
+    # accumulator handed through TMEM to epilogue warps and an integer
+    # log-domain ratio prefilter; chord2: 64-walk units, in-register
+    # epilogue) accumulate every rate in the same k order and find the same
+    # bounds, so the trajectories are bit-identical, refresh passes included.
+    pol = workloads.random_polytope(n, m, seed=n)
+    X0 = np.zeros((n, z), order="F")
+    out = {}
+    for flag in ["0", "1"]:
+        monkeypatch.setenv("MHAR_CHORD3", flag)
+        with mh.Engine(pol, z, seed=7, refresh_every=8) as eng:
+            eng.set_state(X0)
+            eng.step(20)
+            out[flag] = eng.get_state()
+            assert eng.stats()["chord_launches"] > 0
+            bad, _, _ = eng.check_state(1e-9)
+            assert bad == -1
+    assert np.array_equal(out["0"], out["1"])
+
+
 def test_run_box_moments_and_containment(orc):
     # proj/tests/test_sampler.cpp:320-336 + acceptance #4 bounds
     p = mh.make_hypercube(5)
