@@ -518,7 +518,7 @@ def run_engine(args, world, rank, local):
         offset = rank * z
     # the committed ncu captures (NCU_FILE) are of this workload
     captured = args.config == 5 and z == 4096
-    traffic = {k: ncu_traffic(k) for k in ("chord2_full", "tc32_full", "i8_full")}
+    traffic = {k: ncu_traffic(k) for k in ("chord2_full", "chord3_full", "tc32_full", "i8_full")}
     traffic_source = ncu_source()
     projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
     reproject = args.reproject if p.num_equalities() else 0
@@ -588,6 +588,8 @@ def run_engine(args, world, rank, local):
 
     fpi = eng.flops_per_iterate()
     chord_avg_ms = st["chord_ms"] / max(st["chord_timed"], 1)
+    chord_kernel = st["chord_kernel"]  # chord3_kernel from n_pad >= 768, else chord2_kernel
+    chord_capture = "chord3_full" if chord_kernel == "chord3_kernel" else "chord2_full"
     achieved = st["chord_flops"] / max(st["chord_ms"] * 1e-3, 1e-30) / 1e12
     peak = fp64_peak()
     eng.close()
@@ -694,13 +696,16 @@ def run_engine(args, world, rank, local):
                    "l2": "inputs larger than L2 (A_I is %.1f GB)" % (p.a_in.nbytes / 1e9)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak if peak else None,
-                     "traffic": traffic["chord2_full"] if captured else None,
+                     "traffic": traffic[chord_capture] if captured else None,
                      "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
                      "traffic_source": traffic_source,
                      "algorithmic_bytes_GB": (p.a_in.nbytes + 4 * 8 * z * p.num_inequalities()
                                               + 8 * z * p.dim()) / 1e9,
-                     "kernel": "chord2_kernel<INCREMENTAL> (DMMA A_I D + streamed slack cache, "
-                               "fused chord reduce)",
+                     "kernel": (("chord3_kernel (DMMA A_I D, accumulators handed through TMEM "
+                                 "to epilogue warps: streamed slack cache, fused chord reduce)")
+                                if chord_kernel == "chord3_kernel" else
+                                f"{chord_kernel}<INCREMENTAL> (DMMA A_I D + streamed slack cache, "
+                                "fused chord reduce)"),
                      "avg_launch_ms": chord_avg_ms, "launches": st["chord_timed"],
                      "peak_source": "fp64 DMMA microbench, profiles/fp64_peaks_r01.json",
                      "peak_note": "builder-measured mma.sync.m8n8k4.f64 throughput on this pool's "

@@ -253,7 +253,18 @@ typedef struct {
   double chord_flops;      /* algorithmic flops of those timed launches */
   int64_t refreshes;       /* fused refresh passes (incremental mode) */
   int64_t z, z_padded, m_padded, n_padded;
+  int64_t chord_kernel;    /* the kernel computing the chords (mhar_chord_kernel) */
 } mhar_ctx_stats;
+
+/* mhar_ctx_stats.chord_kernel */
+enum mhar_chord_kernel {
+  MHAR_CHORD_SMALL = 1,  /* small_kernel: whole iterate per walk in one launch */
+  MHAR_CHORD_DMMA = 2,   /* chord_kernel / chord2_kernel: DMMA, 64-walk units */
+  MHAR_CHORD_DMMA3 = 3,  /* chord3_kernel: DMMA, 128-walk units, TMEM hand-off */
+  MHAR_CHORD_TC32 = 4,   /* chord_tc32_kernel: fp32 variant on tcgen05 */
+  MHAR_CHORD_INT8 = 5,   /* chord_i8_kernel: fp64 from int8 slices on tcgen05 */
+  MHAR_CHORD_DIAG = 6    /* diag_chord_kernel: stacked diagonal blocks */
+};
 
 int mhar_get_stats(mhar_ctx* ctx, mhar_ctx_stats* out);
 /* 1 = record CUDA events around every chord launch (on the launching stream) */

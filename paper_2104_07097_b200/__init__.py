@@ -118,7 +118,12 @@ class _CtxStats(C.Structure):
                 ("chord_ms", C.c_double), ("chord_timed", C.c_int64),
                 ("chord_flops", C.c_double), ("refreshes", C.c_int64),
                 ("z", C.c_int64), ("z_padded", C.c_int64), ("m_padded", C.c_int64),
-                ("n_padded", C.c_int64)]
+                ("n_padded", C.c_int64), ("chord_kernel", C.c_int64)]
+
+
+# mhar_chord_kernel (include/mhar_b200.h)
+CHORD_KERNELS = {1: "small_kernel", 2: "chord2_kernel", 3: "chord3_kernel",
+                 4: "chord_tc32_kernel", 5: "chord_i8_kernel", 6: "diag_chord_kernel"}
 
 
 _dp = C.POINTER(C.c_double)
@@ -649,7 +654,9 @@ class Engine:
     def stats(self) -> dict:
         s = _CtxStats()
         _check(lib().mhar_get_stats(self._h, C.byref(s)))
-        return {f[0]: getattr(s, f[0]) for f in s._fields_}
+        d = {f[0]: getattr(s, f[0]) for f in s._fields_}
+        d["chord_kernel"] = CHORD_KERNELS.get(d["chord_kernel"], str(d["chord_kernel"]))
+        return d
 
     def set_timing(self, on: bool):
         _check(lib().mhar_set_timing(self._h, 1 if on else 0))

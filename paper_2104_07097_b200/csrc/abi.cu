@@ -1872,6 +1872,12 @@ int mhar_get_stats(mhar_ctx* c, mhar_ctx_stats* out) {
   out->z_padded = c->z_pad;
   out->m_padded = c->m_pad;
   out->n_padded = c->n_pad;
+  out->chord_kernel = c->small_grid > 0 ? MHAR_CHORD_SMALL
+                      : c->diag_coef    ? MHAR_CHORD_DIAG
+                      : c->A8           ? MHAR_CHORD_INT8
+                      : c->Ahi          ? MHAR_CHORD_TC32
+                      : c->c3           ? MHAR_CHORD_DMMA3
+                                        : MHAR_CHORD_DMMA;
   return 0;
 }
 

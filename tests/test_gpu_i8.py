@@ -250,6 +250,7 @@ def test_env_switch_selects_the_int8_engine(monkeypatch):
     monkeypatch.setenv("MHAR_F64_ENGINE", "int8")
     with mh.Engine(p, 100) as eng:
         assert eng.stats()["z_padded"] == 256
+        assert eng.stats()["chord_kernel"] == "chord_i8_kernel"
         eng.set_state(np.zeros((50, 100)))
         eng.step(5)
         assert eng.check_state(1e-9)[0] == -1

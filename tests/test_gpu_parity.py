@@ -288,10 +288,16 @@ def test_chord3_equals_chord2(monkeypatch, n, m, z):
             eng.set_state(X0)
             eng.step(20)
             out[flag] = eng.get_state()
-            assert eng.stats()["chord_launches"] > 0
+            st = eng.stats()
+            assert st["chord_launches"] > 0
+            assert st["chord_kernel"] == ("chord3_kernel" if flag == "1" else "chord2_kernel")
             bad, _, _ = eng.check_state(1e-9)
             assert bad == -1
     assert np.array_equal(out["0"], out["1"])
+    # default choice: chord3 from n_pad >= 768 on
+    monkeypatch.delenv("MHAR_CHORD3")
+    with mh.Engine(pol, z, seed=7) as eng:
+        assert eng.stats()["chord_kernel"] == ("chord3_kernel" if n >= 768 else "chord2_kernel")
 
 
 def test_run_box_moments_and_containment(orc):

@@ -51,13 +51,15 @@ if __name__ == "__main__":
     import datetime
     import os
     dest = sys.argv[1] if len(sys.argv) > 1 else "profiles/ncu_full_r02.json"
-    names = [n for n in ("chord2_full", "tc32_full", "tc32r_full", "i8_full")
+    names = [n for n in ("chord3_full", "chord2_full", "tc32_full", "tc32r_full", "i8_full")
              if os.path.exists(f"gpurun_out/{n}.ncu-rep")]
     doc = {name: summarize(f"gpurun_out/{name}.ncu-rep") for name in names}
     commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
                             text=True).stdout.strip()
     doc["_meta"] = {"captured": datetime.date.today().isoformat(), "commit": commit,
-                    "kernels": {"chord2_full": "chord2_kernel<INCREMENTAL> (DMMA headline)",
+                    "kernels": {"chord3_full": "chord3_kernel (DMMA headline, n_pad >= 768)",
+                                "chord2_full": "chord2_kernel<INCREMENTAL> (MHAR_CHORD3=0; "
+                                               "the DMMA kernel below n_pad 768)",
                                 "tc32_full": "chord_tc32_kernel, fp32 variant, split direction",
                                 "tc32r_full": "chord_tc32_kernel, fp32 variant, rounded direction",
                                 "i8_full": "chord_i8_kernel (int8-slice fp64 engine)"}}
