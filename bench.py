@@ -588,7 +588,7 @@ def run_engine(args, world, rank, local):
 
     fpi = eng.flops_per_iterate()
     chord_avg_ms = st["chord_ms"] / max(st["chord_timed"], 1)
-    chord_kernel = st["chord_kernel"]  # chord3_kernel from n_pad >= 768, else chord2_kernel
+    chord_kernel = st["chord_kernel"]  # chord3_kernel from n_pad >= 384, else chord2_kernel
     chord_capture = "chord3_full" if chord_kernel == "chord3_kernel" else "chord2_full"
     achieved = st["chord_flops"] / max(st["chord_ms"] * 1e-3, 1e-30) / 1e12
     peak = fp64_peak()

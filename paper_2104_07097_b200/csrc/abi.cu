@@ -1118,14 +1118,15 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   c->m_tiles = c->m_pad / BM;
   // the incremental DMMA chord runs chord3_kernel (128-walk units, TMEM
   // hand-off to separate epilogue warps) when the dimension is large enough
-  // for the unit's MMA time to cover its epilogue (n_pad >= 768; measured:
-  // n = 1000 / 2000 gain 3.5 / 1.7 points of DMMA peak, n = 500 loses 2.4),
+  // for the unit's MMA time to cover its epilogue (n_pad >= 384; measured,
+  // profiles/c3_sweep_r02.jsonl and bench: n = 500 / 1000 / 2000 gain 3.8 /
+  // 3.4 / 1.7 points of DMMA peak, n = 384 breaks even, n <= 256 loses),
   // else chord2 (64-walk units, in-register epilogue).  MHAR_CHORD3=0 / 1
   // forces either.
   {
     const char* c3e = std::getenv("MHAR_CHORD3");
     const bool eligible = !tiles && diag_coef.empty() && c->opt.slack_mode == MHAR_SLACK_INCREMENTAL;
-    c->c3 = eligible && (c3e ? std::atoi(c3e) != 0 : c->n_pad >= 768);
+    c->c3 = eligible && (c3e ? std::atoi(c3e) != 0 : c->n_pad >= 384);
   }
   c->z_pad = round_up(c->z, tiles ? 2 * TC_M : c->c3 ? C3_BW : 64);  // whole kernel walk tiles
   c->ct64 = c->z_pad / 64;

@@ -22,6 +22,11 @@
 //   one CTA was in its epilogue the other's 8 warps could not fill the DMMA
 //   pipe alone (config 3: 79.6 % of peak); 64 x 32 tiles saturate it with
 //   two warps per sub-partition (tools/microbench_dmma_tile.cu).
+// - the epilogue carries the bounds as integer keys and tests rows with
+//   integer compares (scan_row_key, reduce_and_publish_keys): its only fp64
+//   instruction per element is the slack update, so it no longer queues
+//   behind the MMAs on the shared fp64 pipe (ncu stall_math; config 3 went
+//   from 75.6 % to 83.5 % of DMMA peak with it).
 // - units in ticket order (next_unit, chord_kernel.cuh), banded over group_m
 //   row tiles.  The slack / rate cache is stored in this kernel's fragment
 //   order (c3_index): every epilogue access is a coalesced 512-byte warp
@@ -304,15 +309,16 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
         const int64_t c0 = ct * C3_BW + wn * 32 + j * 8;
         const int64_t c = c0 + 2 * (lane & 3);
         const double2 th = *reinterpret_cast<const double2*>(p.theta_prev + c);
-        double hi[1][2], lo[1][2], viol[1][2];
-        unsigned sd[1][2] = {{0u, 0u}};
+        // the bounds as keys throughout (scan_row_key): no fp64 instruction
+        // besides the slack update and the rare exact ratio
+        long long hk[2], lk[2], vk[2];
+        unsigned sd[2] = {0u, 0u};
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          hi[0][e] = keyd(*(volatile long long*)(p.hi_key + c + e));
-          lo[0][e] = keyd(*(volatile long long*)(p.lo_key + c + e));
-          viol[0][e] = __longlong_as_double((long long)0xFFF0000000000000ULL);
+          hk[e] = *(volatile long long*)(p.hi_key + c + e);
+          lk[e] = *(volatile long long*)(p.lo_key + c + e);
+          vk[e] = dkey(__longlong_as_double((long long)0xFFF0000000000000ULL));
         }
-        long long vk0 = dkey(viol[0][0]), vk1 = dkey(viol[0][1]);
         const long long epsb = __double_as_longlong(p.eps_dir);
 #pragma unroll
         for (int i0 = 0; i0 < 8; i0 += 2) {
@@ -341,16 +347,13 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
             const double s1 = fma(-th.y, ro[i].y, so[i].y);
             st_policy2(p.S + base, s0, s1, stream_policy);
             st_policy2(p.R + base, a0, a1, stream_policy);
-            viol_key_update(vk0, s0);
-            viol_key_update(vk1, s1);
-            scan_row_int(s0, a0, epsb, hi[0][0], lo[0][0], sd[0][0]);
-            scan_row_int(s1, a1, epsb, hi[0][1], lo[0][1], sd[0][1]);
+            viol_key_update(vk[0], s0);
+            viol_key_update(vk[1], s1);
+            scan_row_key(s0, a0, epsb, hk[0], lk[0], sd[0]);
+            scan_row_key(s1, a1, epsb, hk[1], lk[1], sd[1]);
           }
         }
-        viol[0][0] = keyd(vk0);
-        viol[0][1] = keyd(vk1);
-        const int64_t cc[1] = {c0};
-        reduce_and_publish<1, true>(hi, lo, viol, sd, cc, lane, p);
+        reduce_and_publish_keys(hk, lk, vk, sd, c0, lane, p);
       }
       t_work += pclock() - te1;
     }

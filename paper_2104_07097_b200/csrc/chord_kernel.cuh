@@ -150,39 +150,54 @@ __device__ __forceinline__ void scan_row(double sl, double ad, double eps, doubl
   }
 }
 
-// scan_row with the fp64 pipe kept free for the tensor cores.  DMMA and the
-// fp64 SIMT instructions (DFMA, DSETP) issue on the same fp64 datapath, so an
-// epilogue doing its comparisons in fp64 takes cycles from the MMAs of the
-// co-resident warps.  Here the sign and |ad| > eps tests are integer compares
-// of the bit patterns, and an integer log-domain estimate skips rows whose
-// ratio is provably beyond the current bound: for positive normal x the bit
-// pattern B(x) / 2^52 - 1023 is within 0.0861 below log2 x, so
-// B(sl) - B(ad) > B(bound) - B(1) + 0.2 * 2^52 implies sl / ad > bound
-// exactly (the row cannot move it).  Every other row takes scan_row's exact
-// path (fma filter, division), so the bounds are bit-identical to scan_row.
-__device__ __forceinline__ void scan_row_int(double sl, double ad, long long epsb, double& hi,
-                                             double& lo, unsigned& sd) {
-  constexpr long long kOne = 0x3FF0000000000000LL;     // B(1.0)
-  constexpr long long kMargin = 0x0003333333333333LL;  // 0.2 in log2 units
+// scan_row with the fp64 pipe kept free for the tensor cores (chord3's
+// epilogue).  DMMA and the fp64 SIMT instructions (DFMA, DADD, DSETP) issue
+// on the same fp64 datapath, so an epilogue doing its tests in fp64 waits
+// behind the co-resident warps' MMAs (ncu: stall_math).  Here the bounds are
+// carried as their order-preserving keys (dkey) and every test is an integer
+// compare of bit patterns:
+// - |ad| > eps and the sign of ad from the bits (the mask through PTX: the
+//   compiler would turn a C-level `& 0x7FF..F` of a double's bits back into a
+//   DADD |x|);
+// - an integer log-domain estimate skips rows whose ratio is provably beyond
+//   the current bound: for positive normal x the bit pattern
+//   B(x) / 2^52 - 1023 is within 0.0861 below log2 x, so with sl normal
+//   B(sl) - B(ad) > B(bound) - B(1) + 0.2 * 2^52 implies sl / ad > bound
+//   (the row cannot move it; a negative or subnormal operand only makes the
+//   test more conservative).
+// Every other row takes scan_row's exact path (fma filter, division), so the
+// bounds equal scan_row's.
+__device__ __forceinline__ long long abs_bits(long long x) {
+  long long r;
+  asm("and.b64 %0, %1, 0x7FFFFFFFFFFFFFFF;" : "=l"(r) : "l"(x));
+  return r;
+}
+__device__ __forceinline__ void scan_row_key(double sl, double ad, long long epsb, long long& hk,
+                                             long long& lk, unsigned& sd) {
+  constexpr long long kOne = 0x3FF0000000000000LL;        // B(1.0)
+  constexpr long long kMargin = 0x0003333333333333LL;     // 0.2 in log2 units
   constexpr long long kInf = 0x7FF0000000000000LL;
+  constexpr long long kMinNormal = 0x0010000000000000LL;  // B(DBL_MIN)
   const long long A = __double_as_longlong(ad), S = __double_as_longlong(sl);
-  const long long Aabs = A & 0x7FFFFFFFFFFFFFFFLL;
+  const long long Aabs = abs_bits(A);
   if (Aabs <= epsb) return;  // |ad| <= eps_dir: the row is skipped (chord_scan)
   if (A > 0) {
     sd |= 1u;
-    const long long H = __double_as_longlong(hi);
-    if (S >= 0 && H < kInf && S - A > H - kOne + kMargin) return;
+    // hk >= 0: hk is B(hi)
+    if (S >= kMinNormal && hk >= 0 && hk < kInf && S - A > hk - kOne + kMargin) return;
+    const double hi = keyd(hk);
     if (!(fma(-hi, ad, sl) > 0.0)) {
       const double q = sl / ad;
-      hi = q < hi ? q : hi;
+      if (q < hi) hk = dkey(q);
     }
   } else {
     sd |= 2u;
-    const long long L = __double_as_longlong(lo) & 0x7FFFFFFFFFFFFFFFLL;
-    if (S >= 0 && L < kInf && S - Aabs > L - kOne + kMargin) return;
+    const long long L = abs_bits(lk < 0 ? ~lk : lk);  // B(|lo|)
+    if (S >= kMinNormal && L < kInf && S - Aabs > L - kOne + kMargin) return;
+    const double lo = keyd(lk);
     if (!(fma(-lo, ad, sl) >= 0.0)) {
       const double q = sl / ad;
-      lo = q > lo ? q : lo;
+      if (q > lo) lk = dkey(q);
     }
   }
 }
@@ -191,6 +206,37 @@ __device__ __forceinline__ void viol_key_update(long long& vk, double s) {
   const long long b = __double_as_longlong(s) ^ (long long)0x8000000000000000ULL;  // bits of -s
   const long long k = b >= 0 ? b : (b ^ 0x7FFFFFFFFFFFFFFFLL);
   vk = k > vk ? k : vk;
+}
+
+// reduce_and_publish for bounds carried as keys (scan_row_key): integer
+// min / max through the shuffles, no fp64 instruction.  One walk group.
+__device__ __forceinline__ void reduce_and_publish_keys(long long (&hk)[2], long long (&lk)[2],
+                                                        long long (&vk)[2], unsigned (&sd)[2],
+                                                        int64_t c0, int lane,
+                                                        const ChordParams& p) {
+#pragma unroll
+  for (int e = 0; e < 2; ++e)
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      const long long h = __shfl_xor_sync(0xFFFFFFFFu, hk[e], off);
+      const long long l = __shfl_xor_sync(0xFFFFFFFFu, lk[e], off);
+      const long long v = __shfl_xor_sync(0xFFFFFFFFu, vk[e], off);
+      hk[e] = h < hk[e] ? h : hk[e];
+      lk[e] = l > lk[e] ? l : lk[e];
+      vk[e] = v > vk[e] ? v : vk[e];
+      sd[e] |= __shfl_xor_sync(0xFFFFFFFFu, sd[e], off);
+    }
+  if (lane < 4) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int64_t c = c0 + 2 * lane + e;
+      if (c >= p.z) continue;
+      atomicMax(p.viol_key + c, vk[e]);
+      atomicMin(p.hi_key + c, hk[e]);
+      atomicMax(p.lo_key + c, lk[e]);
+      if (sd[e]) atomicOr(p.sides + c, sd[e]);
+    }
+  }
 }
 
 // Warp reduction over the 8 row lanes sharing (lane & 3), then one atomic per

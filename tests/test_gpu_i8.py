@@ -256,4 +256,4 @@ def test_env_switch_selects_the_int8_engine(monkeypatch):
         assert eng.check_state(1e-9)[0] == -1
     big = workloads.random_polytope(4700, 4, seed=1)  # beyond n <= 4608: stays on DMMA
     with mh.Engine(big, 8) as eng:
-        assert eng.stats()["z_padded"] == 128  # chord3's 128-walk units (n_pad >= 768)
+        assert eng.stats()["z_padded"] == 128  # chord3's 128-walk units (n_pad >= 384)

@@ -294,10 +294,10 @@ def test_chord3_equals_chord2(monkeypatch, n, m, z):
             bad, _, _ = eng.check_state(1e-9)
             assert bad == -1
     assert np.array_equal(out["0"], out["1"])
-    # default choice: chord3 from n_pad >= 768 on
+    # default choice: chord3 from n_pad >= 384 on
     monkeypatch.delenv("MHAR_CHORD3")
     with mh.Engine(pol, z, seed=7) as eng:
-        assert eng.stats()["chord_kernel"] == ("chord3_kernel" if n >= 768 else "chord2_kernel")
+        assert eng.stats()["chord_kernel"] == ("chord3_kernel" if n >= 384 else "chord2_kernel")
 
 
 def test_run_box_moments_and_containment(orc):

@@ -57,9 +57,9 @@ if __name__ == "__main__":
     commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
                             text=True).stdout.strip()
     doc["_meta"] = {"captured": datetime.date.today().isoformat(), "commit": commit,
-                    "kernels": {"chord3_full": "chord3_kernel (DMMA headline, n_pad >= 768)",
+                    "kernels": {"chord3_full": "chord3_kernel (DMMA headline, n_pad >= 384)",
                                 "chord2_full": "chord2_kernel<INCREMENTAL> (MHAR_CHORD3=0; "
-                                               "the DMMA kernel below n_pad 768)",
+                                               "the DMMA kernel below n_pad 384)",
                                 "tc32_full": "chord_tc32_kernel, fp32 variant, split direction",
                                 "tc32r_full": "chord_tc32_kernel, fp32 variant, rounded direction",
                                 "i8_full": "chord_i8_kernel (int8-slice fp64 engine)"}}
