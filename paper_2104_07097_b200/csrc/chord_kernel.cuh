@@ -172,6 +172,25 @@ __device__ __forceinline__ long long abs_bits(long long x) {
   asm("and.b64 %0, %1, 0x7FFFFFFFFFFFFFFF;" : "=l"(r) : "l"(x));
   return r;
 }
+// scan_row's exact test and division for one row, out of line: rows reach
+// it rarely once the bounds have tightened, and sixteen inlined copies of the
+// division sequence would bloat the epilogue's code
+__device__ __noinline__ long long scan_exact_hi(double sl, double ad, long long hk) {
+  const double hi = keyd(hk);
+  if (!(fma(-hi, ad, sl) > 0.0)) {
+    const double q = sl / ad;
+    if (q < hi) return dkey(q);
+  }
+  return hk;
+}
+__device__ __noinline__ long long scan_exact_lo(double sl, double ad, long long lk) {
+  const double lo = keyd(lk);
+  if (!(fma(-lo, ad, sl) >= 0.0)) {
+    const double q = sl / ad;
+    if (q > lo) return dkey(q);
+  }
+  return lk;
+}
 __device__ __forceinline__ void scan_row_key(double sl, double ad, long long epsb, long long& hk,
                                              long long& lk, unsigned& sd) {
   constexpr long long kOne = 0x3FF0000000000000LL;        // B(1.0)
@@ -185,20 +204,12 @@ __device__ __forceinline__ void scan_row_key(double sl, double ad, long long eps
     sd |= 1u;
     // hk >= 0: hk is B(hi)
     if (S >= kMinNormal && hk >= 0 && hk < kInf && S - A > hk - kOne + kMargin) return;
-    const double hi = keyd(hk);
-    if (!(fma(-hi, ad, sl) > 0.0)) {
-      const double q = sl / ad;
-      if (q < hi) hk = dkey(q);
-    }
+    hk = scan_exact_hi(sl, ad, hk);
   } else {
     sd |= 2u;
     const long long L = abs_bits(lk < 0 ? ~lk : lk);  // B(|lo|)
     if (S >= kMinNormal && L < kInf && S - Aabs > L - kOne + kMargin) return;
-    const double lo = keyd(lk);
-    if (!(fma(-lo, ad, sl) >= 0.0)) {
-      const double q = sl / ad;
-      if (q > lo) lk = dkey(q);
-    }
+    lk = scan_exact_lo(sl, ad, lk);
   }
 }
 // running max of -s as an order-preserving integer key (no fp64 instruction)
