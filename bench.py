@@ -518,7 +518,8 @@ def run_engine(args, world, rank, local):
         offset = rank * z
     # the committed ncu captures (NCU_FILE) are of this workload
     captured = args.config == 5 and z == 4096
-    traffic = {k: ncu_traffic(k) for k in ("chord2_full", "chord3_full", "tc32_full", "i8_full")}
+    traffic = {k: ncu_traffic(k) for k in ("chord2_full", "chord3_full", "tc32_full", "tc32r_full",
+                                           "i8_full")}
     traffic_source = ncu_source()
     projector = mh.compute_projection(p.a_eq) if p.num_equalities() else None
     reproject = args.reproject if p.num_equalities() else 0
@@ -652,7 +653,8 @@ def run_engine(args, world, rank, local):
                              "unit": tc_unit, "frac": tc_exec / tc_peak,
                              "frac_vs_mma_probe": (tc_exec / f16_probe_peak()
                                                    if tc_form() == "f16" else None),
-                             "traffic": traffic["tc32_full"] if captured else None,
+                             "traffic": (traffic["tc32_full" if direction == "split" else
+                                                 "tc32r_full"] if captured else None),
                              "traffic_unit": "GB DRAM read+write per launch (ncu --set full)",
                              "avg_launch_ms": s32["chord_ms"] / max(s32["chord_timed"], 1),
                              "peak_source": tc_src},
