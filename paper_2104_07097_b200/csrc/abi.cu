@@ -144,7 +144,8 @@ struct mhar_ctx {
   // structure-aware paths (fastpath.cuh)
   double* diag_coef = nullptr;  // stacked diagonal blocks: per-row coefficient (m)
   int64_t diag_blocks = 0;
-  double* proj_g = nullptr;     // factored projection: G A_E H per walk (m_E x z_pad)
+  double* proj_g = nullptr;     // factored projection: split partials of A_E H (J x m_E x z_pad)
+  double* norm_part = nullptr;  // split partials of ||d||^2 for the collapse test (J x z_pad)
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
   double* rows2 = nullptr;
   double* pinned[2] = {nullptr, nullptr};
@@ -318,6 +319,8 @@ int launch_diag(mhar_ctx* c, int mode, const double* X) {
   p.eps_dir = c->opt.eps_dir;
   p.bounds = mode == CHECK ? 0 : 1;
   // one 1024-thread CTA per SM (the register budget allows one), one wave
+  // (more CTAs per SM -- 32 registers -- or more waves measured slower: more
+  // spills, more cross-CTA bound atomics per walk; tools/ab_diag.sh)
   const int64_t splits = std::max<int64_t>(
       1, std::min<int64_t>(c->KT, (int64_t)c->num_sms / c->ct64));
   p.kt_per_cta = (c->KT + splits - 1) / splits;
@@ -544,23 +547,42 @@ int launch_normals(mhar_ctx* c, double* out) {
 
 // D = P H and collapse flags (sampler.cpp:244-250).
 int launch_projection(mhar_ctx* c) {
+  // per-walk reductions as split partials over (walk tile, k range) CTAs
+  // (fastpath.cuh): deterministic, independent of z and the sharding
+  const int64_t J = dot_splits(c->KT);
+  const dim3 dgrid((unsigned)c->ct64, (unsigned)J);
   if (c->proj_g) {
     // factored: D = H - A_E' (G (A_E H)), O(m_E n z)
-    proj_factor_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
-        c->AE, c->G, c->H, c->me, c->n, c->z, c->KT, c->proj_g, c->err);
-    LAUNCH_OK(c, "proj_factor_kernel");
-    const int64_t total = c->z_pad * c->KT * BK;
-    proj_correct_kernel<<<blocks_for(total, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-        c->AE, c->proj_g, c->H, c->D, c->me, c->n, c->z, total, c->KT, c->err);
-    LAUNCH_OK(c, "proj_correct_kernel");
+#define MHAR_PROJ_ME(ME)                                                                       \
+  case ME:                                                                                     \
+    proj_dot_kernel<ME><<<dgrid, B_PIECE, 0, c->stream>>>(c->AE, c->H, c->n, c->KT, c->z_pad,  \
+                                                          c->proj_g, c->err);                  \
+    LAUNCH_OK(c, "proj_dot_kernel");                                                           \
+    proj_apply_kernel<ME><<<dgrid, B_PIECE, 0, c->stream>>>(c->AE, c->G, c->H, c->D,           \
+                                                            c->proj_g, c->n, c->z, c->KT,      \
+                                                            c->z_pad, c->norm_part, c->err);   \
+    LAUNCH_OK(c, "proj_apply_kernel");                                                         \
+    break;
+    switch (c->me) {
+      MHAR_PROJ_ME(1)
+      MHAR_PROJ_ME(2)
+      MHAR_PROJ_ME(3)
+      MHAR_PROJ_ME(4)
+      default:
+        return fail(MHAR_ERR_INVALID_ARGUMENT, "factored projection: m_E out of range");
+    }
+#undef MHAR_PROJ_ME
   } else {
     dim3 grid((unsigned)(c->p_rows_pad / BM), (unsigned)c->ct64);
     project_kernel<<<grid, 256, 0, c->stream>>>(c->Ppk, c->H, c->D, c->n, c->KT, c->err);
     LAUNCH_OK(c, "project_kernel");
+    norm_part_kernel<<<dgrid, B_PIECE, 0, c->stream>>>(c->D, c->n, c->z, c->KT, c->z_pad,
+                                                       c->norm_part, c->err);
+    LAUNCH_OK(c, "norm_part_kernel");
   }
-  collapse_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
-      c->D, c->n, c->z, c->KT, c->collapsed, c->err);
-  LAUNCH_OK(c, "collapse_kernel");
+  collapse_final_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
+      c->norm_part, J, c->z, c->z_pad, c->collapsed, c->err);
+  LAUNCH_OK(c, "collapse_final_kernel");
   return 0;
 }
 
@@ -1308,7 +1330,14 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         small_bytes = bytes;
       }
     }
-    if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_warps > 0) {
+    // the walk-resident kernel runs each walk's iterate in one warp: it wins
+    // while the body is small or few walks share the GPU; past that the
+    // kernel chain, parallel over walks and coordinates, is faster (measured on
+    // the paper's hypercubes / simplices, tools/small_vs_multi.sh,
+    // profiles/small_vs_multi_r02.jsonl: n = 1000 wins small at z = 1000 and
+    // chain at z = 2000; n = 2000 chain by 2x; n = 700, z = 3000 small)
+    const bool small_wins = c->n < 1800 && (c->n < 900 || c->n * c->z <= 1600000);
+    if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_warps > 0 && small_wins) {
       c->Acm = tmp;
       c->allocs.push_back(tmp);
       c->small_smem = small_bytes;
@@ -1344,7 +1373,9 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
         (st = dalloc(c, &c->eqres, (size_t)c->me * c->z)) ||
         (st = dalloc(c, &c->eqg, (size_t)c->me * c->z)) ||
         // factored projection when m_E is small against n (fastpath.cuh)
-        (factored && (st = dalloc(c, &c->proj_g, (size_t)c->me * c->z_pad))))
+        (st = dalloc(c, &c->norm_part, (size_t)dot_splits(c->KT) * c->z_pad)) ||
+        (factored &&
+         (st = dalloc(c, &c->proj_g, (size_t)dot_splits(c->KT) * c->me * c->z_pad))))
       return bail(st);
     cudaMemcpyAsync(c->Pcm, P.data(), sizeof(double) * P.size(), cudaMemcpyHostToDevice, c->stream);
     cudaMemcpyAsync(c->AE, p->a_eq, sizeof(double) * c->me * c->n, cudaMemcpyHostToDevice,

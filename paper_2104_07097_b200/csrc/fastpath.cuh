@@ -119,55 +119,195 @@ __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagPara
   }
 }
 
-// Factored projection, step 1 (one warp per walk): g_c = G (A_E h_c), m_E <= kMaxFactorEq.
-constexpr int kMaxFactorEq = 4;
-__global__ void proj_factor_kernel(const double* __restrict__ AE /*me x n col-major*/,
-                                   const double* __restrict__ G /*me x me*/,
-                                   const double* __restrict__ H, int64_t me, int64_t n,
-                                   int64_t z, int64_t KT, double* __restrict__ g /*me x z*/,
-                                   const unsigned long long* err) {
-  if (*err != kNoError) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (c >= z) return;
-  double r[kMaxFactorEq] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-  for (int64_t k = lane; k < n; k += 32) {
-    const double h = H[b_index(c, k, KT)];
+constexpr int kMaxFactorEq = 4;  // m_E bound of the factored projection
+
+// ---------------------------------------------------------------------------
+// Per-walk reductions over the packed layout at full HBM rate (round 2).  The
+// round-1 warp-per-walk forms put z warps on a strided walk through each
+// column: at z = 1000 that is ~7 warps per SM, latency bound (simplex
+// n = 5000: 98 us for A_E H, 51 us for the collapse norms, 40 MB each).  Here a CTA owns one 64-walk tile and a fixed
+// range of kDotKt k tiles (grid = walk tiles x J, J = ceil(KT / kDotKt));
+// thread t owns packed element t of every piece, i.e. one (walk, k-offset)
+// slot (the diag kernel's mapping), so every load is a coalesced piece.  The
+// CTA reduces its 16 slots per walk in smem in a fixed order and writes one
+// partial per (split, walk); the consumer sums the J partials in split order.
+// The order depends on n alone: deterministic and independent of z, the
+// grid and the sharding (walk c's result uses only walk c's data).
+constexpr int kDotKt = 8;  // k tiles (128 coordinates) per CTA
+__host__ __device__ inline int64_t dot_splits(int64_t KT) { return (KT + kDotKt - 1) / kDotKt; }
+
+// slot of packed element t within a piece: walk wc (0..63), k offset kof (0..15)
+__device__ __forceinline__ void piece_slot(int t, int* wc, int* kof) {
+  *wc = ((t >> 6) & 7) * 8 + ((t >> 3) & 7);
+  *kof = ((t >> 9) & 1) * 8 + (t & 1) * 4 + ((t >> 1) & 3);
+}
+
+// partial sums of NS values per walk, reduced over the CTA's 16 slots per
+// walk in kof order: out[(j * NS + i) * z_pad + walk]
+template <int NS>
+__device__ __forceinline__ void cta_walk_reduce(double (&v)[NS], double (*red)[BC][BK], int wc,
+                                                int kof, int64_t ct, int64_t j, int64_t z_pad,
+                                                double* out) {
 #pragma unroll
-    for (int i = 0; i < kMaxFactorEq; ++i)
-      if (i < me) r[i] = fma(AE[i + k * me], h, r[i]);
-  }
-#pragma unroll
-  for (int i = 0; i < kMaxFactorEq; ++i)
-    for (int off = 16; off > 0; off >>= 1) r[i] += __shfl_xor_sync(0xFFFFFFFFu, r[i], off);
-  if (lane < me) {
+  for (int i = 0; i < NS; ++i) red[i][wc][kof] = v[i];
+  __syncthreads();
+  const int t = threadIdx.x;
+  if (t < NS * BC) {
+    const int i = t / BC, w = t % BC;
     double s = 0.0;
 #pragma unroll
-    for (int j = 0; j < kMaxFactorEq; ++j)
-      if (j < me) s = fma(G[lane + j * me], r[j], s);
-    g[lane + c * me] = s;
+    for (int q = 0; q < BK; ++q) s += red[i][w][q];
+    out[(j * NS + i) * z_pad + ct * BC + w] = s;
   }
 }
 
-// Factored projection, step 2 (thread per packed element): d = h - A_E' g_c.
-__global__ void proj_correct_kernel(const double* __restrict__ AE, const double* __restrict__ g,
-                                    const double* __restrict__ H, double* __restrict__ D,
-                                    int64_t me, int64_t n, int64_t z, int64_t total,
-                                    int64_t KT, const unsigned long long* err) {
+// (1) r = A_E h per walk, split partials (m_E <= kMaxFactorEq; padded slots 0)
+template <int ME>
+__global__ void __launch_bounds__(B_PIECE) proj_dot_kernel(const double* __restrict__ AE,
+                                                           const double* __restrict__ H,
+                                                           int64_t n, int64_t KT, int64_t z_pad,
+                                                           double* __restrict__ part,
+                                                           const unsigned long long* err) {
   if (*err != kNoError) return;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t c, k;
-    b_coords(e, KT, &c, &k);
-    if (c >= z || k >= n) {
+  __shared__ double red[ME][BC][BK];
+  const int t = threadIdx.x;
+  const int64_t ct = blockIdx.x, j = blockIdx.y;
+  int wc, kof;
+  piece_slot(t, &wc, &kof);
+  double r[ME];
+#pragma unroll
+  for (int i = 0; i < ME; ++i) r[i] = 0.0;
+  // all kDotKt loads in flight, then the sums in k order
+  double h[kDotKt];
+#pragma unroll
+  for (int u = 0; u < kDotKt; ++u) {
+    const int64_t kt = j * kDotKt + u, k = kt * BK + kof;
+    h[u] = (kt < KT && k < n) ? H[(ct * KT + kt) * B_PIECE + t] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kDotKt; ++u) {
+    const int64_t k = (j * kDotKt + u) * BK + kof;
+    if (k < n) {
+#pragma unroll
+      for (int i = 0; i < ME; ++i) r[i] = fma(__ldg(AE + i + k * ME), h[u], r[i]);
+    }
+  }
+  cta_walk_reduce<ME>(r, red, wc, kof, ct, j, z_pad, part);
+}
+
+// (2) d = h - A_E' g with g = G r (r summed over the splits in order), and the
+// split partials of ||d||^2 for the collapse test
+template <int ME>
+__global__ void __launch_bounds__(B_PIECE, 2) proj_apply_kernel(
+    const double* __restrict__ AE, const double* __restrict__ G, const double* __restrict__ H,
+    double* __restrict__ D, const double* __restrict__ part, int64_t n, int64_t z, int64_t KT,
+    int64_t z_pad, double* __restrict__ npart, const unsigned long long* err) {
+  if (*err != kNoError) return;
+  __shared__ double red[ME][BK][BC];  // also the split sums: [i][split group][walk]
+  __shared__ double sg[ME][BC];
+  const int t = threadIdx.x;
+  const int64_t ct = blockIdx.x, j = blockIdx.y;
+  const int64_t J = dot_splits(KT);
+  {
+    // r = sum of the J split partials: thread (group q0, walk w) adds splits
+    // q0, q0 + 16, ..., then walk w's 16 group sums in group order
+    const int w = t % BC, q0 = t / BC;
+#pragma unroll
+    for (int i = 0; i < ME; ++i) {
+      double s = 0.0;
+      for (int64_t q = q0; q < J; q += BK) s += part[(q * ME + i) * z_pad + ct * BC + w];
+      red[i][q0][w] = s;
+    }
+  }
+  __syncthreads();
+  if (t < BC) {
+    double r[ME];
+#pragma unroll
+    for (int i = 0; i < ME; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < BK; ++q) s += red[i][q][t];
+      r[i] = s;
+    }
+#pragma unroll
+    for (int i = 0; i < ME; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < ME; ++q) s = fma(__ldg(G + i + q * ME), r[q], s);
+      sg[i][t] = s;
+    }
+  }
+  __syncthreads();
+  int wc, kof;
+  piece_slot(t, &wc, &kof);
+  const bool live = ct * BC + wc < z;
+  double nrm[1] = {0.0};
+  double h[kDotKt];
+#pragma unroll
+  for (int u = 0; u < kDotKt; ++u) {
+    const int64_t kt = j * kDotKt + u, k = kt * BK + kof;
+    h[u] = (live && kt < KT && k < n) ? H[(ct * KT + kt) * B_PIECE + t] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kDotKt; ++u) {
+    const int64_t kt = j * kDotKt + u, k = kt * BK + kof;
+    if (kt >= KT) break;
+    const int64_t e = (ct * KT + kt) * B_PIECE + t;
+    if (!live || k >= n) {
       D[e] = 0.0;
       continue;
     }
     double s = 0.0;
-    for (int64_t i = 0; i < me; ++i) s = fma(AE[i + k * me], g[i + c * me], s);
-    D[e] = H[e] - s;
+#pragma unroll
+    for (int i = 0; i < ME; ++i) s = fma(__ldg(AE + i + k * ME), sg[i][wc], s);
+    const double d = h[u] - s;
+    D[e] = d;
+    nrm[0] = fma(d, d, nrm[0]);
   }
+  __shared__ double nred[1][BC][BK];
+  cta_walk_reduce<1>(nrm, nred, wc, kof, ct, j, z_pad, npart);
+}
+
+// split partials of ||d||^2 from D (the dense-P path)
+__global__ void __launch_bounds__(B_PIECE) norm_part_kernel(const double* __restrict__ D,
+                                                            int64_t n, int64_t z, int64_t KT,
+                                                            int64_t z_pad,
+                                                            double* __restrict__ npart,
+                                                            const unsigned long long* err) {
+  if (*err != kNoError) return;
+  __shared__ double red[1][BC][BK];
+  const int t = threadIdx.x;
+  const int64_t ct = blockIdx.x, j = blockIdx.y;
+  int wc, kof;
+  piece_slot(t, &wc, &kof);
+  double nrm[1] = {0.0};
+  const bool live = ct * BC + wc < z;
+  double d[kDotKt];
+#pragma unroll
+  for (int u = 0; u < kDotKt; ++u) {
+    const int64_t kt = j * kDotKt + u, k = kt * BK + kof;
+    d[u] = (live && kt < KT && k < n) ? D[(ct * KT + kt) * B_PIECE + t] : 0.0;
+  }
+#pragma unroll
+  for (int u = 0; u < kDotKt; ++u) nrm[0] = fma(d[u], d[u], nrm[0]);
+  cta_walk_reduce<1>(nrm, red, wc, kof, ct, j, z_pad, npart);
+}
+
+// ||d_c|| <= 1e-12 -> collapsed (sampler.cpp:247-249), from the split
+// partials: one warp per walk, lane-strided over the splits, then a fixed
+// shuffle tree (deterministic; the splits depend on n alone)
+__global__ void collapse_final_kernel(const double* __restrict__ npart, int64_t J, int64_t z,
+                                      int64_t z_pad, unsigned* __restrict__ collapsed,
+                                      const unsigned long long* err) {
+  if (*err != kNoError) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= z) return;
+  double s = 0.0;
+  for (int64_t q = lane; q < J; q += 32) s += npart[q * z_pad + c];
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
+  if (lane == 0) collapsed[c] = (sqrt(s) <= kNearZeroDirection) ? 1u : 0u;
 }
 
 }  // namespace mhar_dev

@@ -208,8 +208,9 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
         __syncwarp();
         bool collapsed = false;
         if (p.P && p.factored) {
-          // d = h - A_E' G (A_E h), the reduction order of proj_factor_kernel /
-          // proj_correct_kernel / collapse_kernel (fastpath.cuh)
+          // d = h - A_E' G (A_E h), the formula of proj_dot_kernel /
+          // proj_apply_kernel (fastpath.cuh); the sums here run lane-strided
+          // over the walk's coordinates, so the two paths agree to rounding
           for (int64_t i = 0; i < me; ++i) {
             double r = 0.0;
             for (int64_t k = lane; k < n; k += 32) r = fma(AEs[i * ns + k], hs[k], r);

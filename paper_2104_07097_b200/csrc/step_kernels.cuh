@@ -231,23 +231,6 @@ __global__ void __launch_bounds__(256) project_kernel(const double* __restrict__
   }
 }
 
-// ||d_k|| <= 1e-12 -> collapsed (sampler.cpp:247-249).  One warp per walk,
-// fixed reduction order (deterministic).
-__global__ void collapse_kernel(const double* __restrict__ D, int64_t n, int64_t z, int64_t KT,
-                                unsigned* __restrict__ collapsed, const unsigned long long* err) {
-  if (*err != kNoError) return;
-  const int lane = threadIdx.x & 31;
-  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (w >= z) return;
-  double s = 0.0;
-  for (int64_t k = lane; k < n; k += 32) {
-    const double v = D[b_index(w, k, KT)];
-    s = fma(v, v, s);
-  }
-  for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xFFFFFFFFu, s, off);
-  if (lane == 0) collapsed[w] = (sqrt(s) <= kNearZeroDirection) ? 1u : 0u;
-}
-
 // --------------------------------------------------------- finalize --------
 // Turns the reduced keys into LambdaIntervals (sampler.cpp:182-200): no side
 // -> degenerate with (0, 0); one side -> UNBOUNDED_POLYTOPE; width <= 1e-14
