@@ -126,6 +126,12 @@ CHORD_KERNELS = {1: "small_kernel", 2: "chord2_kernel", 3: "chord3_kernel",
                  4: "chord_tc32_kernel", 5: "chord_i8_kernel", 6: "diag_chord_kernel"}
 
 
+def _stats_dict(s: "_CtxStats") -> dict:
+    d = {f[0]: getattr(s, f[0]) for f in s._fields_}
+    d["chord_kernel"] = CHORD_KERNELS.get(d["chord_kernel"], str(d["chord_kernel"]))
+    return d
+
+
 _dp = C.POINTER(C.c_double)
 _u8p = C.POINTER(C.c_uint8)
 _i64p = C.POINTER(C.c_int64)
@@ -654,9 +660,7 @@ class Engine:
     def stats(self) -> dict:
         s = _CtxStats()
         _check(lib().mhar_get_stats(self._h, C.byref(s)))
-        d = {f[0]: getattr(s, f[0]) for f in s._fields_}
-        d["chord_kernel"] = CHORD_KERNELS.get(d["chord_kernel"], str(d["chord_kernel"]))
-        return d
+        return _stats_dict(s)
 
     def set_timing(self, on: bool):
         _check(lib().mhar_set_timing(self._h, 1 if on else 0))
@@ -666,6 +670,23 @@ class Engine:
 
     def flops_per_iterate(self) -> float:
         return lib().mhar_flops_per_iterate(self._h)
+
+
+def _prefer_bundled_nccl():
+    """Point MHAR_NCCL_LIB (csrc/group.cu) at the NCCL that torch bundles, so
+    the group and a later `import torch` share one libnccl.so.2."""
+    if os.environ.get("MHAR_NCCL_LIB"):
+        return
+    import importlib.util
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["MHAR_NCCL_LIB"] = cand
+            return
 
 
 class Group:
@@ -681,6 +702,7 @@ class Group:
                  chain_offset: int = 0, small_path: bool = True, precision: int = 64,
                  fp32_margin: float = 0.0, f64_engine: str = "dmma",
                  fp32_direction: str = "split", rng: str = "philox"):
+        _prefer_bundled_nccl()
         L = lib()
         self.p = p
         self.n = p.dim()
@@ -757,7 +779,7 @@ class Group:
             raise MharError(ErrorCode.invalid_argument, f"group has no shard {i}")
         s = _CtxStats()
         _check(lib().mhar_get_stats(C.c_void_p(h), C.byref(s)))
-        return {f[0]: getattr(s, f[0]) for f in s._fields_}
+        return _stats_dict(s)
 
 
 # ------------------------------------------------ reference-style calls ----

@@ -144,6 +144,8 @@ struct mhar_ctx {
   // structure-aware paths (fastpath.cuh)
   double* diag_coef = nullptr;  // stacked diagonal blocks: per-row coefficient (m)
   int64_t diag_blocks = 0;
+  bool diag_uniform = false;    // every block: one coefficient and one bound (DiagParams uc/ub)
+  double diag_uc[kDiagUniMax] = {}, diag_ub[kDiagUniMax] = {};
   double* proj_g = nullptr;     // factored projection: split partials of A_E H (J x m_E x z_pad)
   double* norm_part = nullptr;  // split partials of ||d||^2 for the collapse test (J x z_pad)
   // run(): overlapped collection (second rows buffer, pinned staging, side stream)
@@ -318,6 +320,10 @@ int launch_diag(mhar_ctx* c, int mode, const double* X) {
   p.z = c->z;
   p.eps_dir = c->opt.eps_dir;
   p.bounds = mode == CHECK ? 0 : 1;
+  for (int j = 0; j < kDiagUniMax; ++j) {
+    p.uc[j] = c->diag_uc[j];
+    p.ub[j] = c->diag_ub[j];
+  }
   // one 1024-thread CTA per SM (the register budget allows one), one wave
   // (more CTAs per SM -- 32 registers -- or more waves measured slower: more
   // spills, more cross-CTA bound atomics per walk; tools/ab_diag.sh)
@@ -330,7 +336,11 @@ int launch_diag(mhar_ctx* c, int mode, const double* X) {
     ev = take_events(c);
     cudaEventRecord(ev.first, c->stream);
   }
-  if (c->diag_blocks == 2)
+  if (c->diag_uniform && c->diag_blocks == 2)
+    diag_chord_kernel<2, true><<<grid, kDiagThreads, 0, c->stream>>>(p);
+  else if (c->diag_uniform && c->diag_blocks == 1)
+    diag_chord_kernel<1, true><<<grid, kDiagThreads, 0, c->stream>>>(p);
+  else if (c->diag_blocks == 2)
     diag_chord_kernel<2><<<grid, kDiagThreads, 0, c->stream>>>(p);
   else if (c->diag_blocks == 1)
     diag_chord_kernel<1><<<grid, kDiagThreads, 0, c->stream>>>(p);
@@ -1351,6 +1361,18 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     if (!diag_coef.empty()) {
       if ((st = dalloc(c, &c->diag_coef, diag_coef.size()))) return bail(st);
       c->diag_blocks = c->m / c->n;
+      // uniform blocks (hypercube, simplex): constants instead of per-row loads
+      if (c->diag_blocks <= kDiagUniMax) {
+        bool uni = true;
+        for (int64_t j = 0; j < c->diag_blocks && uni; ++j) {
+          c->diag_uc[j] = diag_coef[j * c->n];
+          c->diag_ub[j] = p->b_in[j * c->n];
+          for (int64_t k = 0; k < c->n && uni; ++k)
+            uni = std::memcmp(&diag_coef[j * c->n + k], &c->diag_uc[j], sizeof(double)) == 0 &&
+                  std::memcmp(&p->b_in[j * c->n + k], &c->diag_ub[j], sizeof(double)) == 0;
+        }
+        c->diag_uniform = uni;
+      }
       cudaMemcpyAsync(c->diag_coef, diag_coef.data(), sizeof(double) * diag_coef.size(),
                       cudaMemcpyHostToDevice, c->stream);
     }

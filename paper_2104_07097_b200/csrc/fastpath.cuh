@@ -21,6 +21,7 @@
 namespace mhar_dev {
 
 constexpr int kDiagThreads = 1024;  // = B_PIECE: one packed element per thread
+constexpr int kDiagUniMax = 2;      // blocks of the uniform instantiations
 
 struct DiagParams {
   const double* coef;  // m per-row coefficients (row r: column r % n)
@@ -36,6 +37,9 @@ struct DiagParams {
   int64_t kt_per_cta;  // k tiles per CTA (grid.y splits the coordinates)
   double eps_dir;
   int bounds;          // 0: containment only (max_i (A x - b)_i)
+  // UNIFORM instantiations: every row of block j has coefficient uc[j] and
+  // bound ub[j] (hypercube [I; -I] <= 1, simplex -I <= 0): no per-row loads
+  double uc[kDiagUniMax], ub[kDiagUniMax];
 };
 
 // grid = (walk tiles of 64, coordinate splits); thread t owns packed element t
@@ -43,8 +47,9 @@ struct DiagParams {
 // and walks its k tiles four at a time with all eight loads in flight.
 // BLOCKS > 0: the block count known at compile time (1: simplex -I, 2: the
 // hypercube's [I; -I]) so the row loop unrolls; 0: p.blocks at run time.
-template <int BLOCKS>
+template <int BLOCKS, bool UNIFORM = false>
 __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagParams p) {
+  static_assert(!UNIFORM || (BLOCKS >= 1 && BLOCKS <= kDiagUniMax), "uniform blocks");
   if (*p.err != kNoError) return;
   __shared__ long long s_hi[BC], s_lo[BC], s_viol[BC];
   __shared__ unsigned s_sd[BC];
@@ -86,10 +91,11 @@ __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagPara
       for (int blk = 0; blk < (BLOCKS > 0 ? BLOCKS : 1); ++blk) {
         for (int bb = blk; bb < (BLOCKS > 0 ? blk + 1 : nblk); ++bb) {
           const int r = bb * n32 + k;
-          const double cf = __ldg(p.coef + r);
+          const double cf = UNIFORM ? p.uc[bb] : __ldg(p.coef + r);
+          const double bv = UNIFORM ? p.ub[bb] : __ldg(p.b + r);
           // -(x c) + b and d c, one rounding each (sampler.cpp:168-170; no FMA
           // contraction, so the bounds equal the one-term dot products')
-          const double sl = __dsub_rn(__ldg(p.b + r), __dmul_rn(x[u], cf));
+          const double sl = __dsub_rn(bv, __dmul_rn(x[u], cf));
           viol = fmax(viol, -sl);
           if (p.bounds) scan_row(sl, __dmul_rn(d[u], cf), p.eps_dir, ehi, elo, sd);
         }

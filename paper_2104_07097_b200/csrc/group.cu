@@ -49,7 +49,12 @@ struct Nccl {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 
   bool load() {
-    handle = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    // MHAR_NCCL_LIB names the library to use.  The Python package points it
+    // at the NCCL that torch bundles: a process that imports torch later
+    // resolves torch's libnccl.so.2 dependency by soname to whichever copy is
+    // loaded first, and torch needs its own (newer) version's symbols.
+    const char* path = std::getenv("MHAR_NCCL_LIB");
+    handle = dlopen(path && *path ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
     if (!handle) return false;
     auto sym = [&](auto& f, const char* name) {
       f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(handle, name));

@@ -48,12 +48,22 @@ def test_diag_blocks_injected_step_matches_oracle_bitwise(orc):
     assert np.abs(Xg - Xr).max() <= 1e-15
 
 
-def test_diag_blocks_trajectory_equals_general_product():
-    # three stacked blocks with mixed coefficients: [2I; -I; 0.5 I] x <= b
+@pytest.mark.parametrize("body", ["three_blocks", "box_ragged_bounds", "box_uniform"])
+def test_diag_blocks_trajectory_equals_general_product(body):
+    # stacked diagonal blocks: three with mixed coefficients [2I; -I; 0.5 I]
+    # (per-row loads), a box with per-coordinate bounds [I; -I] x <= [u; -l]
+    # (per-row bounds), a uniform box (the constant-block instantiation)
     n, z = 260, 200
     rng = np.random.default_rng(5)
-    a = np.vstack([2.0 * np.eye(n), -np.eye(n), 0.5 * np.eye(n)])
-    b = np.concatenate([np.full(n, 2.0), np.full(n, 1.0), np.full(n, 0.7)])
+    if body == "three_blocks":
+        a = np.vstack([2.0 * np.eye(n), -np.eye(n), 0.5 * np.eye(n)])
+        b = np.concatenate([np.full(n, 2.0), np.full(n, 1.0), np.full(n, 0.7)])
+    elif body == "box_ragged_bounds":
+        a = np.vstack([np.eye(n), -np.eye(n)])
+        b = np.concatenate([rng.uniform(0.5, 2.0, n), rng.uniform(0.5, 2.0, n)])
+    else:
+        a = np.vstack([3.0 * np.eye(n), -3.0 * np.eye(n)])
+        b = np.full(2 * n, 1.5)
     p = mh.Polytope(a, b)
     out = {}
     for fast in (True, False):  # the general path recomputes the slack like the fast path

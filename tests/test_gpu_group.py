@@ -72,6 +72,21 @@ def test_group_run_large_body_multikernel_path():
     assert np.array_equal(got, ref)
 
 
+def test_group_run_chord3_shards():
+    # n_pad >= 384: every shard runs chord3_kernel (128-walk units, ragged
+    # shard sizes 151 + 150 pad to 256 each)
+    p = workloads.random_polytope(400, 3000, seed=6)
+    z, seed = 301, 9
+    x0 = np.zeros(400)
+    with mh.Engine(p, z, seed=seed, refresh_every=8) as eng:
+        assert eng.stats()["chord_kernel"] == "chord3_kernel"
+        ref, _ = eng.run(x0, phi=6, windows=3)
+    with mh.Group(p, z, [0, 0], seed=seed, refresh_every=8) as g:
+        got, _ = g.run(x0, phi=6, windows=3)
+        assert g.context_stats(1)["chord_kernel"] == "chord3_kernel"
+    assert np.array_equal(got, ref)
+
+
 def test_group_nccl_gather_at_world_one(monkeypatch):
     # the NCCL path (grouped send/recv gather + all-reduce of diagnostics)
     # through real NCCL on the one GPU
