@@ -119,3 +119,43 @@ def test_caught_error_then_same_state_refreshes_the_slack_cache(kw):
     ref = _quadrant_path("recompute")
     got = _quadrant_path("incremental", **kw)
     np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
+
+
+def _quadrant3_path(slack):
+    # the quadrant with a redundant third row (m % n != 0: not the diagonal
+    # fast path, so the incremental DMMA chord kernels run); one-sided
+    # directions (UNBOUNDED) are frequent and the caller hands back the
+    # unchanged state after each
+    quadrant = mh.Polytope(np.array([[-1.0, 0.0], [0.0, -1.0], [-1.0, -1.0]]), np.zeros(3))
+    errors = 0
+    with mh.Engine(quadrant, 1, seed=23, slack=slack, refresh_every=1000,
+                   small_path=False) as eng:
+        x = np.ones((2, 1))
+        eng.set_state(x)
+        traj = []
+        for _ in range(60):
+            try:
+                eng.step(1)
+            except mh.MharError as e:
+                assert e.code == mh.ErrorCode.unbounded_polytope
+                assert "walk 0" in str(e)
+                errors += 1
+                eng.set_state(x)
+            x = eng.get_state()
+            assert x.min() >= -1e-12
+            traj.append(x.copy())
+        kernel = eng.stats()["chord_kernel"]
+    assert 5 < errors < 55
+    return np.array(traj), kernel
+
+
+@pytest.mark.parametrize("chord3", ["0", "1"])
+def test_unbounded_and_cache_reset_on_both_dmma_chord_kernels(monkeypatch, chord3):
+    # one-sided walks raise UNBOUNDED from the incremental kernels' side bits
+    # (chord2's fp64 scan, chord3's integer-key scan), and the slack cache is
+    # rebuilt after every caught error: equal to the recompute path
+    monkeypatch.setenv("MHAR_CHORD3", chord3)
+    got, kernel = _quadrant3_path("incremental")
+    assert kernel == ("chord3_kernel" if chord3 == "1" else "chord2_kernel")
+    ref, _ = _quadrant3_path("recompute")
+    np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12)
