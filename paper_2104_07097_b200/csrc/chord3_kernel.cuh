@@ -39,6 +39,12 @@ namespace mhar_dev {
 
 constexpr int C3_THREADS = 512;   // 8 MMA warps + 8 epilogue warps
 constexpr int C3_BW = 128;        // walks per unit (two packed 64-walk tiles)
+#ifndef MHAR_C3_APOL
+#define MHAR_C3_APOL 1  // L2 policy of the A_I stream: 0 normal, 1 evict_last (tools/ab_c3pol.sh)
+#endif
+#ifndef MHAR_C3_DPOL
+#define MHAR_C3_DPOL 0  // of the direction tiles: 0 evict_last, 1 normal
+#endif
 #ifndef MHAR_C3_STAGES
 #define MHAR_C3_STAGES 6
 #endif
@@ -177,8 +183,16 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
       if (pr.round > 0) mbar_wait(&empty[stage], (uint32_t)((pr.round - 1) & 1));
       double* st = ring + (size_t)stage * C3_STAGE;
       mbar_arrive_expect_tx(&full[stage], C3_STAGE * 8);
+#if MHAR_C3_DPOL == 1
+      const uint64_t keep = policy_evict_normal();
+#else
       const uint64_t keep = policy_evict_last();
+#endif
+#if MHAR_C3_APOL == 1
+      bulk_g2s_hint(st, pr.a, A_PIECE * 8, &full[stage], policy_evict_last());
+#else
       bulk_g2s(st, pr.a, A_PIECE * 8, &full[stage]);
+#endif
       bulk_g2s_hint(st + A_PIECE, pr.b0, B_PIECE * 8, &full[stage], keep);
       bulk_g2s_hint(st + A_PIECE + B_PIECE, pr.b1, B_PIECE * 8, &full[stage], keep);
       pr.a += A_PIECE;
