@@ -51,20 +51,22 @@ if __name__ == "__main__":
     import datetime
     import os
     dest = sys.argv[1] if len(sys.argv) > 1 else "profiles/ncu_full_r02.json"
-    names = [n for n in ("chord3_full", "chord2_full", "tc32_full", "tc32r_full", "i8_full")
+    names = [n for n in ("chord3_full", "chord3_c3_full", "chord2_full", "tc32_full",
+                         "tc32r_full", "i8_full")
              if os.path.exists(f"gpurun_out/{n}.ncu-rep")]
     doc = {name: summarize(f"gpurun_out/{name}.ncu-rep") for name in names}
     commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
                             text=True).stdout.strip()
     doc["_meta"] = {"captured": datetime.date.today().isoformat(), "commit": commit,
                     "kernels": {"chord3_full": "chord3_kernel (DMMA headline, n_pad >= 384)",
+                                "chord3_c3_full": "chord3_kernel at BASELINE config 3 (n = 500)",
                                 "chord2_full": "chord2_kernel<INCREMENTAL> (MHAR_CHORD3=0; "
                                                "the DMMA kernel below n_pad 384)",
                                 "tc32_full": "chord_tc32_kernel, fp32 variant, split direction",
                                 "tc32r_full": "chord_tc32_kernel, fp32 variant, rounded direction",
                                 "i8_full": "chord_i8_kernel (int8-slice fp64 engine)"}}
     doc["_how"] = ("tools/ncu_capture.sh: ncu --set full --clock-control none --import-source on "
-                   "-k <kernel> --launch-skip 1 -c 1 python bench.py ... (config 5, 4096 walks); "
+                   "-k <kernel> --launch-skip 1 -c 1 python bench.py ... (config 5, 4096 walks; chord3_c3_full: config 3); "
                    "numbers per launch; summarised by tools/ncu_summarize.py")
     with open(dest, "w") as f:
         json.dump(doc, f, indent=1)
