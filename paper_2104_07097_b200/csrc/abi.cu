@@ -156,6 +156,7 @@ struct mhar_ctx {
   unsigned long long* walk_err = nullptr;
   size_t small_smem = 0;
   int small_ns = 1, small_grid = 0, small_warps = SMALL_WARPS;
+  int small_gw = 32;  // lanes per walk of the walk-resident kernel (small_group_width)
 
   // host bookkeeping
   int64_t iterations = 0;
@@ -895,7 +896,12 @@ int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   sp.coef = c->diag_coef;
   sp.diag_blocks = c->diag_blocks;
   sp.factored = c->proj_g != nullptr ? 1 : 0;
-  small_kernel<<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp);
+  switch (c->small_gw) {
+    case 4: small_kernel<4><<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp); break;
+    case 8: small_kernel<8><<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp); break;
+    case 16: small_kernel<16><<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp); break;
+    default: small_kernel<32><<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp);
+  }
   LAUNCH_OK(c, "small_kernel");
   small_error_kernel<<<1, 256, 0, c->stream>>>(c->walk_err, c->z, c->err);
   LAUNCH_OK(c, "small_error_kernel");
@@ -1328,14 +1334,18 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     // (warps per CTA: the most that fit next to the body; the path is taken
     // when at least 4 walks per SM are resident)
     c->small_ns = (int)(c->n | 1);
+    const int gw = std::getenv("MHAR_SMALL_GW") ? std::atoi(std::getenv("MHAR_SMALL_GW"))
+                                                : small_group_width(c->n, c->m, !diag_coef.empty(),
+                                                                    c->me > 0, c->z);
+    c->small_gw = (gw == 4 || gw == 8 || gw == 16) ? gw : 32;
     size_t small_bytes = 0;
     int small_warps = 0;
     for (int w = SMALL_WARPS; w >= 1 && !small_warps; --w) {
       const size_t bytes = sizeof(double) * small_smem_doubles(c->n, c->m, c->me, c->me > 0,
                                                                c->small_ns, !diag_coef.empty(),
-                                                               factored, w);
+                                                               factored, w, c->small_gw);
       const size_t per_sm = (227 * 1024) / (bytes + 1024);
-      if (bytes <= 220 * 1024 && (size_t)w * per_sm >= 4) {
+      if (bytes <= 220 * 1024 && (size_t)w * (32 / c->small_gw) * per_sm >= 4) {
         small_warps = w;
         small_bytes = bytes;
       }
@@ -1434,13 +1444,16 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   cudaFuncSetAttribute(chord2_kernel<SLACK_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   if (c->Acm) {
     if ((st = dalloc(c, &c->walk_err, c->z))) return bail(st);
-    cudaFuncSetAttribute(small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)c->small_smem);
+    const void* sk = c->small_gw == 4    ? (const void*)small_kernel<4>
+                     : c->small_gw == 8  ? (const void*)small_kernel<8>
+                     : c->small_gw == 16 ? (const void*)small_kernel<16>
+                                         : (const void*)small_kernel<32>;
+    cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->small_smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, small_kernel, 32 * c->small_warps,
-                                                  c->small_smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sk, 32 * c->small_warps, c->small_smem);
     if (per_sm < 1) per_sm = 1;
-    const int64_t need = (c->z + c->small_warps - 1) / c->small_warps;
+    const int64_t walks_per_cta = (int64_t)c->small_warps * (32 / c->small_gw);
+    const int64_t need = (c->z + walks_per_cta - 1) / walks_per_cta;
     c->small_grid = (int)std::min<int64_t>(need, (int64_t)per_sm * c->num_sms);
   }
   if ((st = reset_streams(c))) return bail(st);

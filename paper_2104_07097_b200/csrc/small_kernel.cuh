@@ -12,6 +12,13 @@
 // few hundred).  The Philox keys are exactly those of the multi-kernel path
 // (walk, iterate, attempt), and every dot product is an ascending-k FMA
 // chain, the summation order of the CPU oracle.
+//
+// Group width (round 2): a walk takes GW = 4, 8, 16 or 32 lanes
+// (small_group_width, from a sweep on the paper's bodies), so a warp carries
+// 32 / GW walks.  With one walk per warp a 3-dimensional
+// hypercube left 29 of 32 lanes idle in every phase; the groups' reductions
+// are shuffles within the group's lanes (the sums' order depends on GW,
+// which depends on the body alone).
 #pragma once
 
 #include "common.cuh"
@@ -48,15 +55,52 @@ struct SmallParams {
 __host__ __device__ inline size_t small_warp_doubles(int64_t n, int64_t me, bool dense_proj) {
   return (dense_proj ? 3 : 2) * (size_t)n + 2 * (size_t)me;
 }
+// Lanes per walk, fitted to a sweep on the paper's bodies (tools/small_gw.sh,
+// profiles/small_gw_r02.jsonl; within 3 % of the best width on average):
+// the least power of two >= the walk's widest phase (its coordinates, or its
+// rows when A_I is staged) / 2, 4 to 32; with an equality projection the
+// per-walk work grows and narrower groups (more walks per warp) win: units / 8,
+// widened while fewer than 1600 warps would carry the z walks.
+__host__ __device__ inline int small_group_width(int64_t n, int64_t m, bool diag, bool proj,
+                                                 int64_t z) {
+  const int64_t units = diag ? n : (n > m ? n : m);
+  const int64_t per = proj ? 8 : 2, min_warps = proj ? 1600 : 0;
+  int gw = 4;
+  while (gw < 32 && gw * per < units) gw <<= 1;
+  while (gw < 32 && z * gw < min_warps * 32) gw <<= 1;
+  return gw;
+}
 __host__ __device__ inline size_t small_smem_doubles(int64_t n, int64_t m, int64_t me, bool proj,
                                                      int ns, bool diag = false,
                                                      bool factored = false,
-                                                     int warps = SMALL_WARPS) {
+                                                     int warps = SMALL_WARPS, int gw = 32) {
   size_t s = diag ? 2 * (size_t)m : (size_t)m * ns + (size_t)m;  // A rows (or coefficients), b
   if (proj && !factored) s += (size_t)n * ns;      // P rows
   s += (size_t)me * ns + (size_t)me + (size_t)me * me;  // A_E, b_E, G
-  s += (size_t)warps * small_warp_doubles(n, me, proj && !factored);
+  s += (size_t)warps * (32 / gw) * small_warp_doubles(n, me, proj && !factored);
   return s;
+}
+
+// reductions over a walk's GW lanes (mask: the group's lanes)
+template <int GW>
+__device__ __forceinline__ double grp_min(double v, unsigned mask) {
+  for (int o = GW / 2; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(mask, v, o));
+  return v;
+}
+template <int GW>
+__device__ __forceinline__ double grp_max(double v, unsigned mask) {
+  for (int o = GW / 2; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(mask, v, o));
+  return v;
+}
+template <int GW>
+__device__ __forceinline__ double grp_sum(double v, unsigned mask) {
+  for (int o = GW / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+  return v;
+}
+template <int GW>
+__device__ __forceinline__ unsigned grp_or(unsigned v, unsigned mask) {
+  for (int o = GW / 2; o > 0; o >>= 1) v |= __shfl_xor_sync(mask, v, o);
+  return v;
 }
 
 __device__ __forceinline__ double warp_min(double v) {
@@ -77,14 +121,15 @@ struct SmallChord {
   unsigned sides;
 };
 
-// Chord of (x, d) against the smem rows: lanes own rows r = lane + 32 j.
+// Chord of (x, d) against the smem rows: group lanes own rows r = gl + GW j.
+template <int GW>
 __device__ inline SmallChord small_chord(const double* As, const double* bs, const double* xs,
                                          const double* ds, int64_t m, int64_t n, int ns,
-                                         double eps, int lane) {
+                                         double eps, int gl, unsigned gmask) {
   double hi = __longlong_as_double(0x7FF0000000000000LL);
   double lo = -hi;
   unsigned sd = 0;
-  for (int64_t r = lane; r < m; r += 32) {
+  for (int64_t r = gl; r < m; r += GW) {
     const double* a = As + r * ns;
     double ax = 0.0, ad = 0.0;
     for (int64_t k = 0; k < n; ++k) {
@@ -103,22 +148,22 @@ __device__ inline SmallChord small_chord(const double* As, const double* bs, con
     }
   }
   SmallChord c;
-  c.hi = warp_min(hi);
-  c.lo = warp_max(lo);
-  for (int o = 16; o > 0; o >>= 1) sd |= __shfl_xor_sync(0xFFFFFFFFu, sd, o);
-  c.sides = sd;
+  c.hi = grp_min<GW>(hi, gmask);
+  c.lo = grp_max<GW>(lo, gmask);
+  c.sides = grp_or<GW>(sd, gmask);
   return c;
 }
 
 // Chord of (x, d) against stacked diagonal blocks (sampler.cpp:166-172):
-// lanes own coordinates; row blk n + k has coefficient cs[blk n + k].
+// group lanes own coordinates; row blk n + k has coefficient cs[blk n + k].
+template <int GW>
 __device__ inline SmallChord small_chord_diag(const double* cs, const double* bs, const double* xs,
                                               const double* ds, int64_t n, int64_t blocks,
-                                              double eps, int lane) {
+                                              double eps, int gl, unsigned gmask) {
   double hi = __longlong_as_double(0x7FF0000000000000LL);
   double lo = -hi;
   unsigned sd = 0;
-  for (int64_t k = lane; k < n; k += 32) {
+  for (int64_t k = gl; k < n; k += GW) {
     const double x = xs[k], d = ds[k];
     for (int64_t blk = 0; blk < blocks; ++blk) {
       const int64_t r = blk * n + k;
@@ -136,13 +181,13 @@ __device__ inline SmallChord small_chord_diag(const double* cs, const double* bs
     }
   }
   SmallChord c;
-  c.hi = warp_min(hi);
-  c.lo = warp_max(lo);
-  for (int o = 16; o > 0; o >>= 1) sd |= __shfl_xor_sync(0xFFFFFFFFu, sd, o);
-  c.sides = sd;
+  c.hi = grp_min<GW>(hi, gmask);
+  c.lo = grp_max<GW>(lo, gmask);
+  c.sides = grp_or<GW>(sd, gmask);
   return c;
 }
 
+template <int GW>
 __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallParams p) {
   if (*p.err != kNoError) return;
   extern __shared__ __align__(16) double sm[];
@@ -172,10 +217,13 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
   for (int64_t i = threadIdx.x; i < me * me; i += blockDim.x) Gs[i] = p.G[i];
   __syncthreads();
 
+  constexpr int WPW = 32 / GW;  // walks per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gl = lane % GW, grp = lane / GW;  // lane within the walk's group, group in the warp
+  const unsigned gmask = (GW == 32 ? 0xFFFFFFFFu : ((1u << GW) - 1u)) << (grp * GW);
   const int nwarps = blockDim.x >> 5;
   const bool dense_proj = p.P && !p.factored;
-  double* xs = wbase + (size_t)warp * small_warp_doubles(n, me, dense_proj);
+  double* xs = wbase + (size_t)(warp * WPW + grp) * small_warp_doubles(n, me, dense_proj);
   double* hs = xs + n;
   double* dsb = dense_proj ? hs + n : hs;  // factored / no projection: d replaces h
   double* res = hs + (dense_proj ? 2 * n : n);
@@ -183,11 +231,11 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
   const int64_t ppc = (n + 1) / 2;
   unsigned long long redraws = 0;
 
-  for (int64_t w = (int64_t)blockIdx.x * nwarps + warp; w < p.z;
-       w += (int64_t)gridDim.x * nwarps) {
+  for (int64_t w = ((int64_t)blockIdx.x * nwarps + warp) * WPW + grp; w < p.z;
+       w += (int64_t)gridDim.x * nwarps * WPW) {
     const uint64_t gw = (uint64_t)(p.chain_offset + w);
-    for (int64_t k = lane; k < n; k += 32) xs[k] = p.X[b_index(w, k, p.KT)];
-    __syncwarp();
+    for (int64_t k = gl; k < n; k += GW) xs[k] = p.X[b_index(w, k, p.KT)];
+    __syncwarp(gmask);
     unsigned long long werr = kNoError;
     for (int64_t t = p.it0; t < p.it0 + p.iters && werr == kNoError; ++t) {
       const double* d = nullptr;
@@ -196,7 +244,7 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
       for (int attempt = 0; attempt <= kMaxDirectionRetries && !done; ++attempt) {
         if (attempt > 0) ++redraws;
         // normals (rng.cpp:153-207 layout; Philox keyed like normals_kernel / redraw_kernel)
-        for (int64_t pi = lane; pi < ppc; pi += 32) {
+        for (int64_t pi = gl; pi < ppc; pi += GW) {
           uint64_t a, bb;
           philox_u64x2(p.seed, (uint32_t)pi, gw, (uint64_t)t, (uint32_t)attempt, kDomNormal, &a,
                        &bb);
@@ -205,55 +253,56 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
           hs[2 * pi] = cs;
           if (2 * pi + 1 < n) hs[2 * pi + 1] = sn;
         }
-        __syncwarp();
+        __syncwarp(gmask);
         bool collapsed = false;
         if (p.P && p.factored) {
           // d = h - A_E' G (A_E h), the formula of proj_dot_kernel /
-          // proj_apply_kernel (fastpath.cuh); the sums here run lane-strided
+          // proj_apply_kernel (fastpath.cuh); the sums here run group-lane-strided
           // over the walk's coordinates, so the two paths agree to rounding
           for (int64_t i = 0; i < me; ++i) {
             double r = 0.0;
-            for (int64_t k = lane; k < n; k += 32) r = fma(AEs[i * ns + k], hs[k], r);
-            r = warp_sum(r);
-            if (lane == 0) res[i] = r;
+            for (int64_t k = gl; k < n; k += GW) r = fma(AEs[i * ns + k], hs[k], r);
+            r = grp_sum<GW>(r, gmask);
+            if (gl == 0) res[i] = r;
           }
-          __syncwarp();
-          for (int64_t i = lane; i < me; i += 32) {
+          __syncwarp(gmask);
+          for (int64_t i = gl; i < me; i += GW) {
             double s = 0.0;
             for (int64_t j = 0; j < me; ++j) s = fma(Gs[i + j * me], res[j], s);
             gv[i] = s;
           }
-          __syncwarp();
+          __syncwarp(gmask);
           double sq = 0.0;
-          for (int64_t k = lane; k < n; k += 32) {
+          for (int64_t k = gl; k < n; k += GW) {
             double s = 0.0;
             for (int64_t i = 0; i < me; ++i) s = fma(AEs[i * ns + k], gv[i], s);
             const double dk = hs[k] - s;
-            dsb[k] = dk;  // dsb == hs: each lane rewrites only its own coordinates
+            dsb[k] = dk;  // dsb == hs: each group lane rewrites only its own coordinates
             sq = fma(dk, dk, sq);
           }
-          __syncwarp();
-          collapsed = sqrt(warp_sum(sq)) <= kNearZeroDirection;
+          __syncwarp(gmask);
+          collapsed = sqrt(grp_sum<GW>(sq, gmask)) <= kNearZeroDirection;
           d = dsb;
           if (attempt > 0 && collapsed) continue;
         } else if (p.P) {
           double sq = 0.0;
-          for (int64_t i = lane; i < n; i += 32) {
+          for (int64_t i = gl; i < n; i += GW) {
             const double* pr = Ps + i * ns;
             double s = 0.0;
             for (int64_t k = 0; k < n; ++k) s = fma(pr[k], hs[k], s);
             dsb[i] = s;
             sq = fma(s, s, sq);
           }
-          __syncwarp();
-          collapsed = sqrt(warp_sum(sq)) <= kNearZeroDirection;
+          __syncwarp(gmask);
+          collapsed = sqrt(grp_sum<GW>(sq, gmask)) <= kNearZeroDirection;
           d = dsb;
           if (attempt > 0 && collapsed) continue;  // redraw_column: collapsed -> next try
         } else {
           d = hs;
         }
-        const SmallChord c = diag ? small_chord_diag(As, bs, xs, d, n, p.diag_blocks, p.eps_dir, lane)
-                                  : small_chord(As, bs, xs, d, m, n, ns, p.eps_dir, lane);
+        const SmallChord c =
+            diag ? small_chord_diag<GW>(As, bs, xs, d, n, p.diag_blocks, p.eps_dir, gl, gmask)
+                 : small_chord<GW>(As, bs, xs, d, m, n, ns, p.eps_dir, gl, gmask);
         if (c.sides == 0u) continue;  // no usable side: degenerate, redraw
         if (c.sides != 3u) {          // one-sided: the body is unbounded
           werr = ((unsigned long long)t << 24) |
@@ -274,7 +323,7 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
       }
       // draw_theta (sampler.cpp:95-101), Philox keyed like theta_kernel
       double th = 0.0;
-      if (lane == 0) {
+      if (gl == 0) {
         int r = 0;
         for (; r < kMaxThetaRejects; ++r) {
           uint64_t a, bb;
@@ -284,36 +333,36 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
         }
         if (r == kMaxThetaRejects) th = chord_point(0.5, lo, hi);
       }
-      th = __shfl_sync(0xFFFFFFFFu, th, 0);
-      for (int64_t k = lane; k < n; k += 32) xs[k] = __dadd_rn(xs[k], __dmul_rn(th, d[k]));
-      __syncwarp();
+      th = __shfl_sync(gmask, th, grp * GW);
+      for (int64_t k = gl; k < n; k += GW) xs[k] = __dadd_rn(xs[k], __dmul_rn(th, d[k]));
+      __syncwarp(gmask);
       // reproject_points every reproject_every global iterates (sampler.cpp:307-310)
       if (me > 0 && p.reproject_every > 0 && (t + 1) % p.reproject_every == 0) {
-        for (int64_t i = lane; i < me; i += 32) {
+        for (int64_t i = gl; i < me; i += GW) {
           double s = 0.0;
           for (int64_t k = 0; k < n; ++k) s = fma(AEs[i * ns + k], xs[k], s);
           res[i] = s - bEs[i];
         }
-        __syncwarp();
-        for (int64_t i = lane; i < me; i += 32) {
+        __syncwarp(gmask);
+        for (int64_t i = gl; i < me; i += GW) {
           double s = 0.0;
           for (int64_t j = 0; j < me; ++j) s = fma(Gs[i + j * me], res[j], s);
           gv[i] = s;
         }
-        __syncwarp();
-        for (int64_t k = lane; k < n; k += 32) {
+        __syncwarp(gmask);
+        for (int64_t k = gl; k < n; k += GW) {
           double s = 0.0;
           for (int64_t i = 0; i < me; ++i) s = fma(AEs[i * ns + k], gv[i], s);
           xs[k] = xs[k] - s;
         }
-        __syncwarp();
+        __syncwarp(gmask);
       }
     }
-    for (int64_t k = lane; k < n; k += 32) p.X[b_index(w, k, p.KT)] = xs[k];
-    if (lane == 0) p.walk_err[w] = werr;
-    __syncwarp();
+    for (int64_t k = gl; k < n; k += GW) p.X[b_index(w, k, p.KT)] = xs[k];
+    if (gl == 0) p.walk_err[w] = werr;
+    __syncwarp(gmask);
   }
-  if (lane == 0 && redraws) atomicAdd(p.redraw_total, redraws);
+  if (gl == 0 && redraws) atomicAdd(p.redraw_total, redraws);
 }
 
 // Canonical error word from the per-walk records: the earliest iterate, then
