@@ -58,6 +58,20 @@ def test_graph_trajectories_bit_identical(kw):
     assert np.abs(a[-1]).max() > 0.05
 
 
+def test_graph_chord3_bit_identical():
+    # n_pad >= 384: the graph replays chord3_kernel (its unit ticket counter
+    # is rewound by the last CTA of every launch), across refreshes and a
+    # state reset
+    p = workloads.random_polytope(400, 4000, seed=8)
+    chunks = [30, 70, 40]
+    a, sa = _trajectory(p, 300, True, chunks, reset_at=1)
+    b, _ = _trajectory(p, 300, False, chunks, reset_at=1)
+    assert sa["chord_kernel"] == "chord3_kernel"
+    for xa, xb in zip(a, b):
+        np.testing.assert_array_equal(xa, xb)
+    assert np.abs(a[-1]).max() > 0.05
+
+
 def test_graph_structured_path_with_reprojection_and_reset():
     n = 3000
     p = mh.make_simplex(n)
