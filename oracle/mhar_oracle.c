@@ -152,7 +152,8 @@ int orc_box_muller(double u1, double u2, double* c, double* s) {
 void orc_fill_standard_normal(uint64_t* state, double* out, int64_t n) {
   const size_t pairs = (size_t)(n + 1) / 2;
   if (pairs == 0) return;
-  double* buf = (double*)malloc(sizeof(double) * 6 * pairs);
+  double* buf = (double*)calloc(6 * pairs, sizeof(double));
+  if (!buf) return;
   double *u1 = buf, *u2 = buf + pairs, *r = buf + 2 * pairs, *sn = buf + 3 * pairs,
          *cs = buf + 4 * pairs, *ang = buf + 5 * pairs;
   for (size_t p = 0; p < pairs; ++p) {
@@ -173,7 +174,8 @@ void orc_fill_standard_normal_matrix(uint64_t* col_states, int64_t z, double* ou
   const size_t ppc = (size_t)(n + 1) / 2;
   const size_t pairs = ppc * (size_t)z;
   if (pairs == 0) return;
-  double* buf = (double*)malloc(sizeof(double) * 6 * pairs);
+  double* buf = (double*)calloc(6 * pairs, sizeof(double));
+  if (!buf) return;
   double *u1 = buf, *u2 = buf + pairs, *r = buf + 2 * pairs, *sn = buf + 3 * pairs,
          *cs = buf + 4 * pairs, *ang = buf + 5 * pairs;
   for (int64_t k = 0; k < z; ++k) {
