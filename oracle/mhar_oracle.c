@@ -902,13 +902,17 @@ int orc_step_philox(const double* A, const double* b, int64_t m, int64_t n, cons
                     double eps_dir, uint64_t seed, int64_t chain_offset, uint64_t iterate,
                     double* X, int64_t z, int64_t* redraws, int64_t* err_chain) {
   const size_t nz = (size_t)(n * z);
-  double* h = (double*)malloc(sizeof(double) * nz);
-  double* d = (double*)malloc(sizeof(double) * nz);
-  double* lo = (double*)malloc(sizeof(double) * (size_t)z);
-  double* hi = (double*)malloc(sizeof(double) * (size_t)z);
-  uint8_t* degen = (uint8_t*)malloc((size_t)z);
-  uint8_t* collapsed = (uint8_t*)calloc((size_t)z, 1);
+  double* h = (double*)calloc(nz ? nz : 1, sizeof(double));
+  double* d = (double*)malloc(sizeof(double) * (nz ? nz : 1));
+  double* lo = (double*)malloc(sizeof(double) * (size_t)(z > 0 ? z : 1));
+  double* hi = (double*)malloc(sizeof(double) * (size_t)(z > 0 ? z : 1));
+  uint8_t* degen = (uint8_t*)malloc((size_t)(z > 0 ? z : 1));
+  uint8_t* collapsed = (uint8_t*)calloc((size_t)(z > 0 ? z : 1), 1);
   int st = ST_OK;
+  if (!h || !d || !lo || !hi || !degen || !collapsed) {
+    st = ST_NUMERICAL_FAILURE;
+    goto done;
+  }
 
   for (int64_t k = 0; k < z; ++k)
     orc_philox_normals(seed, (uint64_t)(chain_offset + k), iterate, 0, h + k * n, n);
