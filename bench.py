@@ -526,7 +526,7 @@ def run_engine(args, world, rank, local):
     eng = mh.Engine(p, z, seed=args.seed, projector=projector, slack=args.slack,
                     refresh_every=args.refresh, device=local, chain_offset=offset,
                     precision=args.precision, f64_engine=args.f64_engine,
-                    fp32_direction=args.fp32_direction)
+                    fp32_direction=args.fp32_direction, z_plan=total_walks)
     X0 = np.zeros((p.dim(), z), order="F")
     X0[:] = w.x0[:, None]
     eng.set_state(X0)

@@ -115,6 +115,10 @@ typedef struct {
                             direction is rounded to one fp16 (per-walk scale) / TF32 operand
                             and the walk moves along that rounded direction (one MMA fewer
                             per k step); bodies with equalities always split */
+  int64_t z_plan;        /* 0 (default): z.  The walk count the kernel choices are made for
+                            (walk-resident kernel or chain, its lanes per walk): a shard of a
+                            larger run passes the run's total so every sharding takes the same
+                            kernels and the samples stay bit-identical (mhar_group sets it) */
 } mhar_options;
 
 #define MHAR_FP32_DIR_SPLIT 0

@@ -99,7 +99,7 @@ class _Options(C.Structure):
                 ("eps_dir", C.c_double), ("eps_feas", C.c_double), ("rng", C.c_int),
                 ("slack_mode", C.c_int), ("refresh_every", C.c_int64), ("device", C.c_int),
                 ("small_path", C.c_int), ("precision", C.c_int), ("fp32_margin", C.c_double),
-                ("f64_engine", C.c_int), ("fp32_direction", C.c_int)]
+                ("f64_engine", C.c_int), ("fp32_direction", C.c_int), ("z_plan", C.c_int64)]
 
 
 class _RunConfig(C.Structure):
@@ -415,7 +415,8 @@ class SampleSet:
 # ------------------------------------------------------------- engine ------
 
 def _context_args(p, z, seed, projector, eps_dir, eps_feas, rng, slack, refresh_every, device,
-                  chain_offset, small_path, precision, fp32_margin, f64_engine, fp32_direction):
+                  chain_offset, small_path, precision, fp32_margin, f64_engine, fp32_direction,
+                  z_plan=0):
     """(polytope struct, options struct, P, G) for mhar_ctx_create /
     mhar_group_create; the returned arrays back the struct pointers."""
     L = lib()
@@ -444,6 +445,7 @@ def _context_args(p, z, seed, projector, eps_dir, eps_feas, rng, slack, refresh_
     opt.fp32_margin = float(fp32_margin)
     opt.f64_engine = {"dmma": F64_DMMA, "int8": F64_INT8}[f64_engine]
     opt.fp32_direction = {"split": 0, "rounded": 1}[fp32_direction]
+    opt.z_plan = int(z_plan)
     P = G = None
     if projector is not None:
         P = _f(projector.p)
@@ -474,7 +476,10 @@ class Engine:
                  slack: str = "incremental", refresh_every: int = 128, device: int = 0,
                  chain_offset: int = 0, small_path: bool = True, precision: int = 64,
                  fp32_margin: float = 0.0, f64_engine: str = "dmma",
-                 fp32_direction: str = "split"):
+                 fp32_direction: str = "split", z_plan: int = 0):
+        # z_plan: the whole run's walk count when this context is one shard
+        # of it (mhar_options.z_plan): every sharding then takes the same
+        # kernels, so the samples do not depend on the placement
         L = lib()
         self.p = p
         self.n = p.dim()
@@ -482,7 +487,8 @@ class Engine:
         self._keep = []
         poly, opt, P, G = _context_args(p, z, seed, projector, eps_dir, eps_feas, rng, slack,
                                         refresh_every, device, chain_offset, small_path,
-                                        precision, fp32_margin, f64_engine, fp32_direction)
+                                        precision, fp32_margin, f64_engine, fp32_direction,
+                                        z_plan)
         self.precision = int(precision)
         self.f64_engine = f64_engine
         self.rng = rng

@@ -1336,7 +1336,9 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     c->small_ns = (int)(c->n | 1);
     const int gw = std::getenv("MHAR_SMALL_GW") ? std::atoi(std::getenv("MHAR_SMALL_GW"))
                                                 : small_group_width(c->n, c->m, !diag_coef.empty(),
-                                                                    c->me > 0, c->z);
+                                                                    c->me > 0,
+                                                                    opt->z_plan > 0 ? opt->z_plan
+                                                                                    : c->z);
     c->small_gw = (gw == 4 || gw == 8 || gw == 16) ? gw : 32;
     size_t small_bytes = 0;
     int small_warps = 0;
@@ -1356,7 +1358,8 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
     // the paper's hypercubes / simplices, tools/small_vs_multi.sh,
     // profiles/small_vs_multi_r02.jsonl: n = 1000 wins small at z = 1000 and
     // chain at z = 2000; n = 2000 chain by 2x; n = 700, z = 3000 small)
-    const bool small_wins = c->n < 1800 && (c->n < 900 || c->n * c->z <= 1600000);
+    const int64_t zp = opt->z_plan > 0 ? opt->z_plan : c->z;  // the run's walks (mhar_options)
+    const bool small_wins = c->n < 1800 && (c->n < 900 || c->n * zp <= 1600000);
     if (c->opt.small_path && c->opt.rng == MHAR_RNG_PHILOX && small_warps > 0 && small_wins) {
       c->Acm = tmp;
       c->allocs.push_back(tmp);

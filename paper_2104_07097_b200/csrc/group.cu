@@ -196,6 +196,7 @@ int mhar_group_create(const mhar_polytope* p, const double* projector, const dou
   int st = for_each_device(g, [&](int i) {
     mhar_options o = *opt;
     o.z = g->z[i];
+    o.z_plan = opt->z_plan > 0 ? opt->z_plan : opt->z;  // kernel choices of the whole run
     o.chain_offset = opt->chain_offset + g->off[i];
     o.device = devices[i];
     return mhar_ctx_create(p, projector, gram_inverse, &o, &g->ctx[i]);

@@ -139,6 +139,7 @@ class ShardedSampler:
         self.z_counts = [shard_walks(z_total, world, r)[0] for r in range(world)]
         self.n = polytope.dim()
         self.device = local_rank
+        engine_kw.setdefault("z_plan", z_total)  # same kernels for every world size
         self.engine = Engine(polytope, self.z, seed=seed, projector=projector, device=local_rank,
                              chain_offset=self.offset, **engine_kw)
 

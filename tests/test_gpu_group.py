@@ -87,6 +87,26 @@ def test_group_run_chord3_shards():
     assert np.array_equal(got, ref)
 
 
+def test_group_kernel_choice_follows_the_whole_run():
+    # simplex n = 1000: 2000 walks take the kernel chain, a 1000-walk shard
+    # alone would take the walk-resident kernel (mhar_options.z_plan): the
+    # group's shards plan for the run's 2000 walks, so the samples equal one
+    # context's bit for bit
+    n, z, seed = 1000, 2000, 5
+    p = mh.make_simplex(n)
+    op = mh.compute_projection(p.a_eq)
+    x0 = np.full(n, 1.0 / n)
+    with mh.Engine(p, z, seed=seed, projector=op) as eng:
+        assert eng.stats()["chord_kernel"] == "diag_chord_kernel"
+        ref, _ = eng.run(x0, phi=4, windows=2, reproject_every=3)
+    with mh.Engine(p, z // 2, seed=seed, projector=op) as half:
+        assert half.stats()["chord_kernel"] == "small_kernel"  # what a shard would pick alone
+    with mh.Group(p, z, [0, 0], seed=seed, projector=op) as g:
+        assert g.context_stats(0)["chord_kernel"] == "diag_chord_kernel"
+        got, _ = g.run(x0, phi=4, windows=2, reproject_every=3)
+    assert np.array_equal(got, ref)
+
+
 def test_group_nccl_gather_at_world_one(monkeypatch):
     # the NCCL path (grouped send/recv gather + all-reduce of diagnostics)
     # through real NCCL on the one GPU
