@@ -306,7 +306,17 @@ typedef struct {
   int64_t offset[MHAR_GROUP_MAX_DEV];  /* global id of each shard's first walk */
   double last_max_violation;  /* max_k max_i (A x - b)_i of the last collection, all shards */
   int64_t last_redraws;       /* redraw attempts of the last run, all shards */
+  int gather;                 /* how windows reach devices[0] (mhar_group_gather) */
 } mhar_group_info_t;
+
+/* mhar_group_info_t.gather; MHAR_GROUP_GATHER=direct|nccl|copy overrides the
+ * default (direct wherever every shard's device can reach devices[0]). */
+enum mhar_group_gather {
+  MHAR_GATHER_COPY = 0,   /* rows staged per shard, copy-engine peer copy to the root */
+  MHAR_GATHER_NCCL = 1,   /* rows staged per shard, grouped ncclSend / ncclRecv + ncclAllReduce */
+  MHAR_GATHER_DIRECT = 2  /* each shard's containment-check + unpack kernel stores its rows
+                             straight into the root's window buffer over NVLink peer memory */
+};
 
 int mhar_group_create(const mhar_polytope* p, const double* projector, const double* gram_inverse,
                       const mhar_options* opt, const int* devices, int ndev, mhar_group** out);

@@ -164,7 +164,11 @@ class _GroupInfo(C.Structure):
     _fields_ = [("ndev", C.c_int), ("uses_nccl", C.c_int), ("z_total", C.c_int64),
                 ("devices", C.c_int * MHAR_GROUP_MAX_DEV), ("z", C.c_int64 * MHAR_GROUP_MAX_DEV),
                 ("offset", C.c_int64 * MHAR_GROUP_MAX_DEV), ("last_max_violation", C.c_double),
-                ("last_redraws", C.c_int64)]
+                ("last_redraws", C.c_int64), ("gather", C.c_int)]
+
+
+# mhar_group_gather (include/mhar_b200.h)
+GROUP_GATHER = {0: "copy", 1: "nccl", 2: "direct"}
 
 
 class _LpStats(C.Structure):
@@ -749,7 +753,7 @@ class Group:
         return {"ndev": nd, "uses_nccl": bool(gi.uses_nccl), "z_total": gi.z_total,
                 "devices": list(gi.devices[:nd]), "z": list(gi.z[:nd]),
                 "offset": list(gi.offset[:nd]), "last_max_violation": gi.last_max_violation,
-                "last_redraws": gi.last_redraws}
+                "last_redraws": gi.last_redraws, "gather": GROUP_GATHER.get(gi.gather, "?")}
 
     def set_state(self, x):
         x = _f(x)

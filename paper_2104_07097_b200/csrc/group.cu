@@ -8,11 +8,14 @@
 // count) all-reduced with ncclAllReduce -- the only traffic between GPUs,
 // as the north star names it.  Reference run(): sampler.cpp:274-335.
 //
-// NCCL is loaded at group creation (dlopen libnccl.so.2); with one device,
-// with a device listed twice (several shards sharing a GPU -- the test
-// configuration on a one-GPU box) or without libnccl, the gather is a
-// peer-to-peer copy engine transfer (cudaMemcpyPeerAsync) into the root's
-// window buffer and the diagnostics are reduced on the host.
+// Where every shard's device can reach devices[0] (NVLink peer access; a
+// device listed twice, the test configuration on a one-GPU box, trivially
+// can) the gather is fused into the collection: each shard's containment
+// check + unpack kernel stores its rows straight into the root's window
+// buffer over peer memory (MHAR_GATHER_DIRECT) -- no staging copy, no
+// separate transfer.  Otherwise NCCL (loaded at group creation with dlopen)
+// between distinct devices, or copy-engine peer copies; without NCCL the
+// diagnostics are reduced on the host.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -122,6 +125,7 @@ struct mhar_group {
   std::vector<int64_t> z, off;  // shard sizes and global offsets
   int64_t z_total = 0, n = 0, chain_offset = 0;
   bool use_nccl = false;
+  int gather_mode = MHAR_GATHER_COPY;  // mhar_group_gather
   std::vector<ncclComm_t> comms;
   // per device: its window rows (z_i x n row-major) and diagnostics
   // [worst violation, redraws] (doubles); root: two window buffers
@@ -204,17 +208,40 @@ int mhar_group_create(const mhar_polytope* p, const double* projector, const dou
   bool distinct = true;
   for (int i = 0; i < ndev; ++i)
     for (int j = 0; j < i; ++j) distinct = distinct && devices[i] != devices[j];
-  const char* force = std::getenv("MHAR_GROUP_NCCL");  // "0" off, "1" also for one device
-  const bool want = force ? std::atoi(force) != 0 : ndev > 1;
-  if (!st && want && distinct && nccl().handle) {
+  // how windows reach the root: DIRECT where every shard's device can store
+  // into devices[0]'s memory (peer access over NVLink; a device listed twice
+  // trivially can), else NCCL between distinct devices, else copies.
+  // MHAR_GROUP_GATHER overrides; MHAR_GROUP_NCCL=1 asks for NCCL even with
+  // one device, =0 rules it out.
+  const char* gsel = std::getenv("MHAR_GROUP_GATHER");
+  const char* force = std::getenv("MHAR_GROUP_NCCL");
+  bool direct_ok = true;
+  for (int i = 1; !st && i < ndev; ++i) {
+    if (devices[i] == devices[0]) continue;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, devices[i], devices[0]);
+    if (can) {
+      cudaSetDevice(devices[i]);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(devices[0], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) can = 0, cudaGetLastError();
+    }
+    direct_ok = direct_ok && can;
+  }
+  const std::string mode = gsel ? gsel : force ? (std::atoi(force) ? "nccl" : "noncclfallback") : "";
+  const bool want_nccl = mode == "nccl" || (mode.empty() && !direct_ok && ndev > 1);
+  if (!st && want_nccl && (distinct || mode == "nccl") && nccl().handle) {
     g->comms.assign(ndev, nullptr);
     const ncclResult_t r = nccl().CommInitAll(g->comms.data(), ndev, devices);
     if (r == ncclSuccess) {
       g->use_nccl = true;
+      g->gather_mode = MHAR_GATHER_NCCL;
     } else {
-      g->comms.clear();  // fall back to peer copies
+      g->comms.clear();  // fall back to direct stores or copies
     }
   }
+  if (!g->use_nccl && direct_ok && mode != "copy" && mode != "noncclfallback")
+    g->gather_mode = MHAR_GATHER_DIRECT;
   const size_t win = (size_t)g->z_total * g->n;
   g->rows.assign(ndev, nullptr);
   g->diag.assign(ndev, nullptr);
@@ -222,11 +249,13 @@ int mhar_group_create(const mhar_polytope* p, const double* projector, const dou
   for (int i = 0; !st && i < ndev; ++i) {
     cudaSetDevice(devices[i]);
     cudaError_t e = cudaMalloc(&g->diag[i], 4 * sizeof(double));
-    if (e == cudaSuccess && i > 0) e = cudaMalloc(&g->rows[i], sizeof(double) * g->z[i] * g->n);
+    // staging rows only where the shard does not store into the root directly
+    if (e == cudaSuccess && i > 0 && g->gather_mode != MHAR_GATHER_DIRECT)
+      e = cudaMalloc(&g->rows[i], sizeof(double) * g->z[i] * g->n);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_sent[i], cudaEventDisableTiming);
     if (e != cudaSuccess) st = cuda_fail("group_create: device buffers", e);
-    // the root reads every shard's rows: peer access where the topology has it
-    if (!st && i > 0 && devices[i] != devices[0]) {
+    // copies: the root reads every shard's rows, peer access where available
+    if (!st && i > 0 && devices[i] != devices[0] && g->gather_mode == MHAR_GATHER_COPY) {
       int can = 0;
       cudaDeviceCanAccessPeer(&can, devices[0], devices[i]);
       if (can) {
@@ -283,6 +312,7 @@ int mhar_group_info(mhar_group* g, mhar_group_info_t* info) {
   std::memset(info, 0, sizeof(*info));
   info->ndev = g->ndev;
   info->uses_nccl = g->use_nccl ? 1 : 0;
+  info->gather = g->gather_mode;
   info->z_total = g->z_total;
   for (int i = 0; i < g->ndev && i < MHAR_GROUP_MAX_DEV; ++i) {
     info->devices[i] = g->devices[i];
@@ -360,9 +390,11 @@ int mhar_group_run(mhar_group* g, const mhar_run_config* cfg, const double* x0, 
         const cudaError_t e = cudaStreamWaitEvent(s, g->ev_copied[b], 0);
         if (e != cudaSuccess) st = cuda_fail("group_run: wait for the window buffer", e);
       }
-      // the root's shard lands directly in the window buffer; the others
-      // stage their rows for the exchange
-      if (!st) st = mhar_internal::collect(c, i == 0 ? dst : g->rows[i], g->diag[i]);
+      // the root's shard lands directly in the window buffer, and with DIRECT
+      // every shard's check + unpack kernel stores its rows there over peer
+      // memory; otherwise the shards stage their rows for the exchange
+      const bool straight = i == 0 || g->gather_mode == MHAR_GATHER_DIRECT;
+      if (!st) st = mhar_internal::collect(c, straight ? dst : g->rows[i], g->diag[i]);
       if (!st) {
         cudaSetDevice(dev);
         redraws_to_double<<<1, 1, 0, s>>>(mhar_internal::redraw_counter(c), g->diag[i] + 1);
@@ -389,7 +421,7 @@ int mhar_group_run(mhar_group* g, const mhar_run_config* cfg, const double* x0, 
         const ncclResult_t r = N.GroupEnd();
         if (!st && r != ncclSuccess)
           st = set_error(MHAR_ERR_CUDA, std::string("NCCL window exchange: ") + N.GetErrorString(r));
-      } else if (i > 0 && !st) {
+      } else if (i > 0 && !st && g->gather_mode == MHAR_GATHER_COPY) {
         // peer copy of this shard's rows into the root's window buffer
         cudaSetDevice(dev);
         const cudaError_t e = cudaMemcpyPeerAsync(dst, g->devices[0], g->rows[i], dev,

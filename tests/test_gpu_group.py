@@ -25,6 +25,26 @@ def _single(p, z, seed, steps, op=None, reproject=0, **kw):
         return eng.get_state()
 
 
+@pytest.mark.parametrize("gather", ["direct", "copy"])
+def test_group_window_gather_modes(monkeypatch, gather):
+    # DIRECT (default where every device reaches devices[0]): each shard's
+    # check + unpack kernel stores its rows into the root's window buffer;
+    # COPY: staged rows and copy-engine peer copies -- the same samples
+    monkeypatch.setenv("MHAR_GROUP_GATHER", gather)
+    p = workloads.random_polytope(36, 700, seed=12)
+    z, seed = 222, 6
+    x0 = np.zeros(36)
+    with mh.Engine(p, z, seed=seed) as eng:
+        ref, rst = eng.run(x0, phi=5, windows=4)
+    with mh.Group(p, z, [0, 0, 0], seed=seed) as g:
+        assert g.info()["gather"] == gather
+        got, st = g.run(x0, phi=5, windows=4)
+        info = g.info()
+    assert np.array_equal(got, ref)
+    assert info["last_redraws"] == rst.redraw_count
+    assert info["last_max_violation"] <= 1e-9
+
+
 @pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
 def test_group_step_equals_one_context(devices):
     p = workloads.random_polytope(40, 900, seed=4)
