@@ -100,6 +100,36 @@ def test_factored_projection_injected_step_matches_oracle(orc):
     assert np.abs(Xg - Xr).max() <= 1e-9 * np.abs(Xr).max()
 
 
+@pytest.mark.parametrize("me", [2, 3, 4])
+def test_factored_projection_several_equalities(orc, me):
+    # m_E = 2..4 random equality rows: the factored projection's split-partial
+    # sums (proj_dot_kernel / proj_apply_kernel<ME>) against the oracle's
+    # dense P H on one injected step
+    n, m, z = 300, 2500, 193
+    rng = np.random.default_rng(40 + me)
+    a_in = rng.standard_normal((m, n))
+    a_in /= np.linalg.norm(a_in, axis=1, keepdims=True)
+    a_eq = rng.standard_normal((me, n))
+    p = mh.Polytope(np.asfortranarray(a_in), np.ones(m), np.asfortranarray(a_eq), np.zeros(me))
+    op = mh.compute_projection(p.a_eq)
+    X = np.asfortranarray(op.p @ rng.uniform(-0.02, 0.02, (n, z)))  # on the slice, inside
+    H = np.asfortranarray(rng.standard_normal((n, z)))
+    U = rng.uniform(0, 1, z)
+    with _engine(p, z, projector=op) as eng:
+        eng.set_state(X)
+        lo, hi, th, fl = eng.step_injected(H, U)
+        Xg = eng.get_state()
+    st, Xr, lor, hir, thr, flr, _ = orc.step_injected(p.a_in, p.b_in, op.p, EPS_DIR, X, H, U)
+    assert st == 0
+    np.testing.assert_array_equal(fl, flr)
+    ok = (flr & mh.FLAG_DEGENERATE) == 0
+    wd = np.where(ok, hir - lor, 1.0)
+    assert np.all(np.abs(lo - lor)[ok] <= 1e-9 * wd[ok])
+    assert np.all(np.abs(hi - hir)[ok] <= 1e-9 * wd[ok])
+    assert np.abs(Xg - Xr).max() <= 1e-9 * np.abs(Xr).max()
+    assert np.abs(a_eq @ Xg).max() <= 1e-12  # still on the slice
+
+
 def test_factored_projection_run_stays_on_the_slice():
     n = 400
     p = mh.make_simplex(n)
