@@ -272,7 +272,8 @@ def test_incremental_matches_recompute():
     assert np.abs(out["incremental"] - out["recompute"]).max() <= 1e-9
 
 
-@pytest.mark.parametrize("n,m,z", [(64, 3000, 300), (200, 5000, 1000), (401, 4000, 300), (800, 9000, 257)])
+@pytest.mark.parametrize("n,m,z", [(64, 3000, 300), (200, 5000, 1000), (401, 4000, 300),
+                                   (800, 9000, 257), (400, 1000, 1), (420, 1200, 5)])
 def test_chord3_equals_chord2(monkeypatch, n, m, z):
     # The two incremental DMMA chord kernels (chord3: 128-walk units with the
     # accumulator handed through TMEM to epilogue warps and an integer
