@@ -154,6 +154,7 @@ struct mhar_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_ready[2] = {nullptr, nullptr}, ev_copied[2] = {nullptr, nullptr};
   unsigned long long* walk_err = nullptr;
+  unsigned long long* walk_err_min = nullptr;  // small path: min of walk_err, kNoError between launches
   size_t small_smem = 0;
   int small_ns = 1, small_grid = 0, small_warps = SMALL_WARPS;
   int small_gw = 32;  // lanes per walk of the walk-resident kernel (small_group_width)
@@ -892,6 +893,7 @@ int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
   sp.redraw_total = c->redraw_total;
   sp.err = c->err;
   sp.walk_err = c->walk_err;
+  sp.err_min = c->walk_err_min;
   sp.ns = c->small_ns;
   sp.coef = c->diag_coef;
   sp.diag_blocks = c->diag_blocks;
@@ -903,7 +905,7 @@ int advance(mhar_ctx* c, int64_t iters, int64_t reproject_every) {
     default: small_kernel<32><<<c->small_grid, 32 * c->small_warps, c->small_smem, c->stream>>>(sp);
   }
   LAUNCH_OK(c, "small_kernel");
-  small_error_kernel<<<1, 256, 0, c->stream>>>(c->walk_err, c->z, c->err);
+  small_error_kernel<<<1, 256, 0, c->stream>>>(c->walk_err, c->z, c->walk_err_min, c->err);
   LAUNCH_OK(c, "small_error_kernel");
   c->iterations += iters;
   c->slack_valid = false;
@@ -1446,7 +1448,9 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   cudaFuncSetAttribute(chord2_kernel<CHECK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   cudaFuncSetAttribute(chord2_kernel<SLACK_STORE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CHORD2_SMEM);
   if (c->Acm) {
-    if ((st = dalloc(c, &c->walk_err, c->z))) return bail(st);
+    if ((st = dalloc(c, &c->walk_err, c->z)) || (st = dalloc(c, &c->walk_err_min, 1)))
+      return bail(st);
+    cudaMemsetAsync(c->walk_err_min, 0xFF, sizeof(unsigned long long), c->stream);  // kNoError
     const void* sk = c->small_gw == 4    ? (const void*)small_kernel<4>
                      : c->small_gw == 8  ? (const void*)small_kernel<8>
                      : c->small_gw == 16 ? (const void*)small_kernel<16>

@@ -44,6 +44,7 @@ struct SmallParams {
   unsigned long long* redraw_total;
   const unsigned long long* err;
   unsigned long long* walk_err;  // per walk: (iterate << 24) | (phase << 8) | status
+  unsigned long long* err_min;   // min over walks of walk_err (kNoError: none failed)
   int ns;                        // smem row stride (odd)
   const double* coef;            // stacked diagonal blocks (fastpath.cuh): per-row coefficient, or null
   int64_t diag_blocks;
@@ -359,7 +360,10 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
       }
     }
     for (int64_t k = gl; k < n; k += GW) p.X[b_index(w, k, p.KT)] = xs[k];
-    if (gl == 0) p.walk_err[w] = werr;
+    if (gl == 0) {
+      p.walk_err[w] = werr;
+      if (werr != kNoError) atomicMin(p.err_min, werr);  // rare: the resolver scans only then
+    }
     __syncwarp(gmask);
   }
   if (gl == 0 && redraws) atomicAdd(p.redraw_total, redraws);
@@ -369,7 +373,13 @@ __global__ void __launch_bounds__(32 * SMALL_WARPS) small_kernel(const SmallPara
 // the earliest phase, then the lowest walk -- where the reference's
 // iterate-major loop would have raised first.
 __global__ void small_error_kernel(const unsigned long long* walk_err, int64_t z,
-                                   unsigned long long* err) {
+                                   unsigned long long* err_min, unsigned long long* err) {
+  // no walk failed (the common case): nothing to resolve.  The word is read
+  // by every thread before thread 0 re-arms it for the next launch.
+  const unsigned long long any = *(volatile unsigned long long*)err_min;
+  __syncthreads();
+  if (threadIdx.x == 0) *err_min = kNoError;
+  if (any == kNoError) return;
   unsigned long long best = kNoError;
   int64_t best_w = -1;
   for (int64_t w = threadIdx.x; w < z; w += blockDim.x) {
