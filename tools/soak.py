@@ -1,6 +1,6 @@
-"""Long runs of every engine on BASELINE configs 3 and 4: containment and
-equality residuals of all walks every 100 iterates (refreshes every 128,
-reprojection every 100 on config 4)."""
+"""Long runs of every engine on BASELINE configs 3, 4 (and 5 with SOAK_CFGS):
+containment and equality residuals of all walks every 100 iterates
+(refreshes every 128, reprojection every 100 on config 4)."""
 import json, os, sys
 import numpy as np
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -8,7 +8,7 @@ import paper_2104_07097_b200 as mh
 from paper_2104_07097_b200 import workloads
 
 iters = int(sys.argv[1]) if len(sys.argv) > 1 else 600
-for cfg in (3, 4):
+for cfg in [int(c) for c in os.environ.get("SOAK_CFGS", "3 4").split()]:
     w = workloads.config(cfg)
     p = w.polytope
     proj = mh.compute_projection(p.a_eq) if p.num_equalities() else None
@@ -25,6 +25,8 @@ for cfg in (3, 4):
                 worst = max(worst, float(viol.max()))
                 worst_eq = max(worst_eq, float(eqv.max()))
             X = eng.get_state()
-        print(json.dumps({"config": cfg, "engine": kw or "dmma", "iterates": iters,
+            kernel = eng.stats()["chord_kernel"]
+        print(json.dumps({"config": cfg, "engine": kw or "dmma", "chord_kernel": kernel,
+                          "iterates": iters,
                           "max_violation": worst, "max_eq_residual": worst_eq,
                           "spread": float(np.abs(X).max())}), flush=True)
