@@ -61,7 +61,21 @@ constexpr size_t C3_SMEM = C3_BAR_OFF + 1024;
 #define MHAR_C3_MMA_REGS 208
 #endif
 constexpr int C3_MMA_REGS = MHAR_C3_MMA_REGS;
-constexpr int C3_EPI_REGS = 256 - C3_MMA_REGS;  // 512 threads share the 64K-register file
+#ifndef MHAR_C3_EPI_REGS
+#define MHAR_C3_EPI_REGS (256 - MHAR_C3_MMA_REGS)
+#endif
+constexpr int C3_EPI_REGS = MHAR_C3_EPI_REGS;  // 512 threads share the 64K-register file
+#ifndef MHAR_C3_DEC_FIRST
+// 1: the epilogue warps execute setmaxnreg.dec before the CTA's first barrier
+// and the MMA warps' .inc follows it.  With the .dec inside the epilogue
+// branch, two processes time-slicing one GPU (compute preemption of the
+// CTA) ended in an illegal memory access in every stress run
+// (tools/shared_gpu_stress.py: 0 of 13 runs failed; the original order, an
+// .inc that waits on the .dec through a named barrier, or the TMEM
+// allocation moved to an MMA warp all failed).  Cost: 0.3-0.5 %.
+#define MHAR_C3_DEC_FIRST 1
+#endif
+
 
 // tcgen05 register <-> TMEM moves, 32x32b shape: thread t of the warp owns
 // TMEM lane (quarter * 32 + t); consecutive registers go to consecutive columns
@@ -141,6 +155,11 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
                  "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+#if MHAR_C3_DEC_FIRST && !defined(MHAR_C3_NO_SETMAXNREG)
+  // the epilogue warps release their registers before the barrier, so the
+  // MMA warps' setmaxnreg.inc below never has to wait for them
+  if (warp >= 8) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C3_EPI_REGS));
+#endif
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
@@ -151,7 +170,9 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
   };
 
   if (warp < 8) {
+#ifndef MHAR_C3_NO_SETMAXNREG
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C3_MMA_REGS));
+#endif
     // ------------------------------ MMA warps ------------------------------
     const int wm = warp >> 2, wn = warp & 3;  // warp tile: 64 rows x 32 walks
     // producer (thread 0): the ring's (unit, k tile) sequence, C3_STAGES -
@@ -298,7 +319,9 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
       atomicAdd(pr + 3, (unsigned long long)t_store);
     }
   } else {
+#if !defined(MHAR_C3_NO_SETMAXNREG) && !MHAR_C3_DEC_FIRST
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C3_EPI_REGS));
+#endif
     // ---------------------------- epilogue warps ----------------------------
     const int twin = warp - 8;                   // MMA warp whose tile this warp reads
     const int wm = twin >> 2, wn = twin & 3;     // warp % 4 == wn: the same TMEM lane quarter

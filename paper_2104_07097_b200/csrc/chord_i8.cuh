@@ -261,13 +261,17 @@ __global__ void __cluster_dims__(I8_CL, 1, 1) __launch_bounds__(I8_THREADS, 1)
                  "n"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
+  // the control warps release their registers before the barrier, so the
+  // epilogue warps' setmaxnreg.inc never waits on a concurrent .dec (an .inc
+  // blocked across a preemption by another context corrupted chord3's state;
+  // same order here, chord3_kernel.cuh)
+  if (warp < 4) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(I8_CTRL_REGS));
   asm volatile("tcgen05.fence::before_thread_sync;");
   cluster_sync_all();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = *tptr;
 
   if (warp < 4) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(I8_CTRL_REGS));
     if (warp == 0 && lane == 0) {
       // ---------------- producer: this CTA's direction slices + A half ----------------
       const uint64_t keep = policy_evict_last();  // direction slices: re-read by every row tile
