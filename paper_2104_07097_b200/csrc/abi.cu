@@ -134,6 +134,7 @@ struct mhar_ctx {
   // CUDA graph of one steady iterate (multi-kernel path, MHAR_NO_GRAPHS=1 disables):
   // the kernels read the Philox iterate counter from d_iter
   bool no_graphs = false, graph_capturing = false;
+  bool pdl = true;  // iterate-chain kernels launched as programmatic dependents (MHAR_NO_PDL=1: off)
   unsigned long long* d_iter = nullptr;
   unsigned long long d_iter_value = ~0ull;  // what d_iter holds once queued work ran
   cudaGraphExec_t graph_exec = nullptr;
@@ -304,6 +305,31 @@ ChordParams chord_params(mhar_ctx* c, const double* X) {
   return p;
 }
 
+// Launches one kernel of the iterate chain.  With c->pdl it is a
+// programmatic dependent of the kernel before it on the stream (captured
+// into the iterate graph as a programmatic edge): its CTAs are scheduled
+// while the predecessor drains and wait in pdl_enter (common.cuh) for the
+// predecessor's completion.  Only kernels that call pdl_enter first go
+// through here.
+template <typename... K, typename... A>
+void launch_k(mhar_ctx* c, void (*kernel)(K...), dim3 grid, dim3 block, size_t smem, A... args) {
+  if (!c->pdl) {
+    kernel<<<grid, block, smem, c->stream>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // compute_lambda_intervals' stacked-diagonal fast path (fastpath.cuh)
 int launch_diag(mhar_ctx* c, int mode, const double* X) {
   DiagParams p;
@@ -339,15 +365,15 @@ int launch_diag(mhar_ctx* c, int mode, const double* X) {
     cudaEventRecord(ev.first, c->stream);
   }
   if (c->diag_uniform && c->diag_blocks == 2)
-    diag_chord_kernel<2, true><<<grid, kDiagThreads, 0, c->stream>>>(p);
+    launch_k(c, diag_chord_kernel<2, true>, grid, kDiagThreads, 0, p);
   else if (c->diag_uniform && c->diag_blocks == 1)
-    diag_chord_kernel<1, true><<<grid, kDiagThreads, 0, c->stream>>>(p);
+    launch_k(c, diag_chord_kernel<1, true>, grid, kDiagThreads, 0, p);
   else if (c->diag_blocks == 2)
-    diag_chord_kernel<2><<<grid, kDiagThreads, 0, c->stream>>>(p);
+    launch_k(c, diag_chord_kernel<2>, grid, kDiagThreads, 0, p);
   else if (c->diag_blocks == 1)
-    diag_chord_kernel<1><<<grid, kDiagThreads, 0, c->stream>>>(p);
+    launch_k(c, diag_chord_kernel<1>, grid, kDiagThreads, 0, p);
   else
-    diag_chord_kernel<0><<<grid, kDiagThreads, 0, c->stream>>>(p);
+    launch_k(c, diag_chord_kernel<0>, grid, kDiagThreads, 0, p);
   LAUNCH_OK(c, "diag_chord_kernel");
   ++c->chord_launches;
   if (c->timing) {
@@ -535,7 +561,7 @@ int launch_finalize(mhar_ctx* c, bool queue_redraws, bool advance_streams) {
   fp.col_state = (advance_streams && c->opt.rng == MHAR_RNG_REFERENCE) ? c->col_state : nullptr;
   fp.draws_per_walk = 2 * ((c->n + 1) / 2);
   fp.z = c->z;
-  finalize_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(fp);
+  launch_k(c, finalize_kernel, blocks_for(c->z, 256, 1 << 20), 256, 0, fp);
   LAUNCH_OK(c, "finalize_kernel");
   return 0;
 }
@@ -552,7 +578,8 @@ int launch_normals(mhar_ctx* c, double* out) {
   rp.mode = c->opt.rng;
   rp.col_state = c->col_state;
   const int64_t work = c->ct64 * c->KT * 16 * 32;
-  normals_kernel<<<blocks_for(work, 256, c->num_sms * 16), 256, 0, c->stream>>>(rp, out, c->err);
+  launch_k(c, normals_kernel, blocks_for(work, 256, c->num_sms * 16), 256, 0, rp, out,
+           (const unsigned long long*)c->err);
   LAUNCH_OK(c, "normals_kernel");
   return 0;
 }
@@ -567,12 +594,13 @@ int launch_projection(mhar_ctx* c) {
     // factored: D = H - A_E' (G (A_E H)), O(m_E n z)
 #define MHAR_PROJ_ME(ME)                                                                       \
   case ME:                                                                                     \
-    proj_dot_kernel<ME><<<dgrid, B_PIECE, 0, c->stream>>>(c->AE, c->H, c->n, c->KT, c->z_pad,  \
-                                                          c->proj_g, c->err);                  \
+    launch_k(c, proj_dot_kernel<ME>, dgrid, B_PIECE, 0, (const double*)c->AE,                \
+             (const double*)c->H, c->n, c->KT, c->z_pad, c->proj_g,                            \
+             (const unsigned long long*)c->err);                                               \
     LAUNCH_OK(c, "proj_dot_kernel");                                                           \
-    proj_apply_kernel<ME><<<dgrid, B_PIECE, 0, c->stream>>>(c->AE, c->G, c->H, c->D,           \
-                                                            c->proj_g, c->n, c->z, c->KT,      \
-                                                            c->z_pad, c->norm_part, c->err);   \
+    launch_k(c, proj_apply_kernel<ME>, dgrid, B_PIECE, 0, (const double*)c->AE,              \
+             (const double*)c->G, (const double*)c->H, c->D, (const double*)c->proj_g, c->n,   \
+             c->z, c->KT, c->z_pad, c->norm_part, (const unsigned long long*)c->err);           \
     LAUNCH_OK(c, "proj_apply_kernel");                                                         \
     break;
     switch (c->me) {
@@ -588,12 +616,13 @@ int launch_projection(mhar_ctx* c) {
     dim3 grid((unsigned)(c->p_rows_pad / BM), (unsigned)c->ct64);
     project_kernel<<<grid, 256, 0, c->stream>>>(c->Ppk, c->H, c->D, c->n, c->KT, c->err);
     LAUNCH_OK(c, "project_kernel");
-    norm_part_kernel<<<dgrid, B_PIECE, 0, c->stream>>>(c->D, c->n, c->z, c->KT, c->z_pad,
-                                                       c->norm_part, c->err);
+    launch_k(c, norm_part_kernel, dgrid, B_PIECE, 0, (const double*)c->D, c->n, c->z, c->KT,
+             c->z_pad, c->norm_part, (const unsigned long long*)c->err);
     LAUNCH_OK(c, "norm_part_kernel");
   }
-  collapse_final_kernel<<<blocks_for(c->z * 32, 256, 1 << 20), 256, 0, c->stream>>>(
-      c->norm_part, J, c->z, c->z_pad, c->collapsed, c->err);
+  launch_k(c, collapse_final_kernel, blocks_for(c->z * 32, 256, 1 << 20), 256, 0,
+           (const double*)c->norm_part, J, c->z, c->z_pad, c->collapsed,
+           (const unsigned long long*)c->err);
   LAUNCH_OK(c, "collapse_final_kernel");
   return 0;
 }
@@ -630,7 +659,7 @@ int launch_redraw(mhar_ctx* c) {
   rp.m = c->m;
   rp.KT = c->KT;
   rp.eps_dir = c->opt.eps_dir;
-  redraw_kernel<<<c->redraw_grid, 256, 0, c->stream>>>(rp);
+  launch_k(c, redraw_kernel, c->redraw_grid, 256, 0, rp);
   LAUNCH_OK(c, "redraw_kernel");
   return 0;
 }
@@ -656,15 +685,16 @@ ThetaParams theta_params(mhar_ctx* c, const double* injected_u) {
 
 int launch_theta_and_move(mhar_ctx* c, const double* injected_u) {
   ThetaParams tp = theta_params(c, injected_u);
-  theta_kernel<<<blocks_for(c->z, 256, 1 << 20), 256, 0, c->stream>>>(tp);
+  launch_k(c, theta_kernel, blocks_for(c->z, 256, 1 << 20), 256, 0, tp);
   LAUNCH_OK(c, "theta_kernel");
   if (!injected_u && c->opt.rng == MHAR_RNG_REFERENCE) {
-    theta_fixup_kernel<<<1, 1, 0, c->stream>>>(tp);
+    launch_k(c, theta_fixup_kernel, 1, 1, 0, tp);
     LAUNCH_OK(c, "theta_fixup_kernel");
   }
   const int64_t total2 = c->z_pad * c->KT * BK / 2;
-  axpy_kernel<<<blocks_for(total2, 256, c->num_sms * 16), 256, 0, c->stream>>>(
-      c->X, c->D, c->theta, total2, c->KT, c->err);
+  launch_k(c, axpy_kernel, blocks_for(total2, 256, c->num_sms * 16), 256, 0, c->X,
+           (const double*)c->D, (const double*)c->theta, total2, c->KT,
+           (const unsigned long long*)c->err);
   LAUNCH_OK(c, "axpy_kernel");
   return 0;
 }
@@ -816,7 +846,7 @@ int graph_iterate(mhar_ctx* c) {
     }
     c->graph_capturing = true;
     int s = enqueue_iterate(c, 0, false);
-    if (!s) mhar_dev::iter_inc_kernel<<<1, 1, 0, c->stream>>>(c->d_iter);
+    if (!s) launch_k(c, mhar_dev::iter_inc_kernel, 1, 1, 0, c->d_iter);
     c->graph_capturing = false;
     const cudaError_t ec = cudaStreamEndCapture(c->stream, &g);
     cudaGraphExec_t ex = nullptr;
@@ -1434,6 +1464,7 @@ int mhar_ctx_create(const mhar_polytope* p, const double* projector, const doubl
   int big = 0x7FFFFFFF;
   cudaMemcpyAsync(c->first_reject, &big, sizeof(int), cudaMemcpyHostToDevice, c->stream);
   c->no_graphs = std::getenv("MHAR_NO_GRAPHS") != nullptr;
+  c->pdl = std::getenv("MHAR_NO_PDL") == nullptr;
   if ((st = dalloc(c, &c->d_iter, 1))) return bail(st);
   fill_keys_kernel<<<blocks_for(c->z_pad, 256, 1 << 20), 256, 0, c->stream>>>(
       c->hi_key, c->lo_key, c->viol_key, c->sides, c->z_pad);

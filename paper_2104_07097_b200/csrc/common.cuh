@@ -297,6 +297,17 @@ __device__ inline void dmma884(double& d0, double& d1, double a, double b) {
 // earliest phase, then the lowest walk -- the reference raises for the first
 // walk in index order within a phase (sampler.cpp:182-200, 255-265).
 constexpr unsigned long long kNoError = ~0ULL;
+// Programmatic dependent launch (the iterate chain's kernels, launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization by abi.cu launch_k):
+// a kernel lets its successor's CTAs be scheduled as soon as all of its own
+// CTAs are running, and every kernel waits for its predecessor's completion
+// and memory before touching any of it.  Without the attribute both are
+// no-ops.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;");
+}
+
 __device__ inline unsigned long long error_word(int phase, int64_t walk, int status) {
   return ((unsigned long long)phase << 56) | ((unsigned long long)walk << 8) |
          (unsigned long long)status;

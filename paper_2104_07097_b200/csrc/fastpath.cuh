@@ -49,6 +49,7 @@ struct DiagParams {
 // hypercube's [I; -I]) so the row loop unrolls; 0: p.blocks at run time.
 template <int BLOCKS, bool UNIFORM = false>
 __global__ void __launch_bounds__(kDiagThreads) diag_chord_kernel(const DiagParams p) {
+  pdl_enter();
   static_assert(!UNIFORM || (BLOCKS >= 1 && BLOCKS <= kDiagUniMax), "uniform blocks");
   if (*p.err != kNoError) return;
   __shared__ long long s_hi[BC], s_lo[BC], s_viol[BC];
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(B_PIECE) proj_dot_kernel(const double* __restr
                                                            int64_t n, int64_t KT, int64_t z_pad,
                                                            double* __restrict__ part,
                                                            const unsigned long long* err) {
+  pdl_enter();
   if (*err != kNoError) return;
   __shared__ double red[ME][BC][BK];
   const int t = threadIdx.x;
@@ -208,6 +210,7 @@ __global__ void __launch_bounds__(B_PIECE, 2) proj_apply_kernel(
     const double* __restrict__ AE, const double* __restrict__ G, const double* __restrict__ H,
     double* __restrict__ D, const double* __restrict__ part, int64_t n, int64_t z, int64_t KT,
     int64_t z_pad, double* __restrict__ npart, const unsigned long long* err) {
+  pdl_enter();
   if (*err != kNoError) return;
   __shared__ double red[ME][BK][BC];  // also the split sums: [i][split group][walk]
   __shared__ double sg[ME][BC];
@@ -280,6 +283,7 @@ __global__ void __launch_bounds__(B_PIECE) norm_part_kernel(const double* __rest
                                                             int64_t z_pad,
                                                             double* __restrict__ npart,
                                                             const unsigned long long* err) {
+  pdl_enter();
   if (*err != kNoError) return;
   __shared__ double red[1][BC][BK];
   const int t = threadIdx.x;
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(B_PIECE) norm_part_kernel(const double* __rest
 __global__ void collapse_final_kernel(const double* __restrict__ npart, int64_t J, int64_t z,
                                       int64_t z_pad, unsigned* __restrict__ collapsed,
                                       const unsigned long long* err) {
+  pdl_enter();
   if (*err != kNoError) return;
   const int lane = threadIdx.x & 31;
   const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;

@@ -123,6 +123,7 @@ struct RngParams {
 // (fill_standard_normal_matrix, rng.cpp:153-207; odd n drops the last sine).
 __global__ void normals_kernel(const RngParams rp, double* __restrict__ H,
                                const unsigned long long* err) {
+  pdl_enter();
   if (*err != kNoError) return;
   const int64_t ppc = (rp.n + 1) / 2;
   // thread order follows the packed layout: a warp fills one (walk tile, k
@@ -255,6 +256,7 @@ struct FinalizeParams {
 };
 
 __global__ void finalize_kernel(const FinalizeParams fp) {
+  pdl_enter();
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= fp.z) return;
   const double hi = keyd(fp.hi_key[c]);
@@ -348,6 +350,7 @@ __device__ inline double block_reduce(double v, double* red, int op /*0 min 1 ma
 }
 
 __global__ void __launch_bounds__(256) redraw_kernel(const RedrawParams rp) {
+  pdl_enter();
   double* xs = rp.scratch + (size_t)blockIdx.x * 3 * rp.n;  // n
   double* hs = xs + rp.n;                                    // n
   double* ds = xs + 2 * rp.n;                                // n
@@ -493,6 +496,7 @@ __device__ inline double chord_point(double u, double lower, double upper) {
 }
 
 __global__ void theta_kernel(const ThetaParams tp) {
+  pdl_enter();
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= tp.z) return;
   if (*tp.err != kNoError) return;
@@ -534,6 +538,7 @@ __global__ void theta_kernel(const ThetaParams tp) {
 // rejected -- redo the draws sequentially from that walk on, exactly as the
 // reference's k = 0..z-1 loop consumes the single stream (sampler.cpp:267-270).
 __global__ void theta_fixup_kernel(ThetaParams tp) {
+  pdl_enter();
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   if (*tp.err != kNoError) return;
   const int first = *tp.first_reject;
@@ -567,6 +572,7 @@ __global__ void theta_fixup_kernel(ThetaParams tp) {
 __global__ void axpy_kernel(double* __restrict__ X, const double* __restrict__ D,
                             const double* __restrict__ theta, int64_t total2, int64_t KT,
                             const unsigned long long* err) {
+  pdl_enter();
   if (*err != kNoError) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total2;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -664,6 +670,9 @@ __global__ void worst_violation_kernel(const double* __restrict__ viol,
 
 // the device copy of the iterate counter (CUDA-graph replays of an iterate)
 __global__ void iter_set_kernel(unsigned long long* it, unsigned long long v) { *it = v; }
-__global__ void iter_inc_kernel(unsigned long long* it) { *it += 1ull; }
+__global__ void iter_inc_kernel(unsigned long long* it) {
+  pdl_enter();
+  *it += 1ull;
+}
 
 }  // namespace mhar_dev
