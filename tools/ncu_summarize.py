@@ -55,8 +55,11 @@ if __name__ == "__main__":
                          "tc32r_full", "i8_full")
              if os.path.exists(f"gpurun_out/{n}.ncu-rep")]
     doc = {name: summarize(f"gpurun_out/{name}.ncu-rep") for name in names}
-    commit = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
-                            text=True).stdout.strip()
+    # the captures run on the GPU box (no .git there): summarise them here, where
+    # HEAD is the commit whose kernels were snapshotted (or pass MHAR_CAPTURE_COMMIT)
+    commit = os.environ.get("MHAR_CAPTURE_COMMIT") or subprocess.run(
+        ["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True,
+        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__)))).stdout.strip() or "unknown"
     doc["_meta"] = {"captured": datetime.date.today().isoformat(), "commit": commit,
                     "kernels": {"chord3_full": "chord3_kernel (DMMA headline, n_pad >= 384)",
                                 "chord3_c3_full": "chord3_kernel at BASELINE config 3 (n = 500)",
