@@ -57,6 +57,14 @@ constexpr int C3_STAGE = A_PIECE + 2 * B_PIECE;  // doubles per stage (32 KB)
 constexpr int C3_UQ = 8;
 constexpr size_t C3_BAR_OFF = (size_t)C3_STAGES * C3_STAGE * 8;
 constexpr size_t C3_SMEM = C3_BAR_OFF + 1024;
+#ifndef MHAR_C3_PAIRBAR
+// 1: the TMEM hand-off barriers are per twin pair (MMA warp w <-> epilogue
+// warp w + 8, one arrival each) instead of one 8-arrival barrier per buffer,
+// so a slow epilogue warp holds up only its twin, which the ring's depth
+// absorbs (tools/ab_c3pair.sh)
+#define MHAR_C3_PAIRBAR 1
+#endif
+constexpr int C3_TB = MHAR_C3_PAIRBAR ? 8 : 1;  // hand-off barriers per TMEM buffer
 #ifndef MHAR_C3_MMA_REGS
 #define MHAR_C3_MMA_REGS 208
 #endif
@@ -128,9 +136,9 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C3_BAR_OFF);
   uint64_t* empty = full + C3_STAGES;
   uint64_t* uready = empty + C3_STAGES;  // [C3_UQ] unit announced
-  uint64_t* tfull = uready + C3_UQ;      // [2] a unit's accumulators in TMEM buffer b
-  uint64_t* tempty = tfull + 2;          // [2] buffer b read back by the epilogue warps
-  long long* uq = reinterpret_cast<long long*>(tempty + 2);  // [C3_UQ] the units
+  uint64_t* tfull = uready + C3_UQ;      // [2][C3_TB] a unit's accumulators in TMEM buffer b
+  uint64_t* tempty = tfull + 2 * C3_TB;  // [2][C3_TB] buffer b read back by the epilogue warps
+  long long* uq = reinterpret_cast<long long*>(tempty + 2 * C3_TB);  // [C3_UQ] the units
   uint32_t* tptr = reinterpret_cast<uint32_t*>(uq + C3_UQ);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -143,9 +151,9 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
       mbar_init(&empty[s], 8);  // the 8 MMA warps
     }
     for (int s = 0; s < C3_UQ; ++s) mbar_init(&uready[s], 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tfull[b], 8);   // the 8 MMA warps stored their tiles
-      mbar_init(&tempty[b], 8);  // the 8 epilogue warps read them
+    for (int b = 0; b < 2 * C3_TB; ++b) {
+      mbar_init(&tfull[b], 8 / C3_TB);   // the (twin) MMA warp(s) stored their tiles
+      mbar_init(&tempty[b], 8 / C3_TB);  // the (twin) epilogue warp(s) read them
     }
     fence_barrier_init();
   }
@@ -284,7 +292,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
       // b * 256 + wm * 128 + [32 j + 2 (2 i + e) + half] of lane quarter wn
       const int b = ui & 1;
       const long long tu1 = pclock();
-      if (ui >= 2) mbar_wait(&tempty[b], (uint32_t)(((ui >> 1) - 1) & 1));
+      if (ui >= 2) mbar_wait(&tempty[b * C3_TB + (C3_TB > 1 ? warp : 0)], (uint32_t)(((ui >> 1) - 1) & 1));
       const long long tu2 = pclock();
       asm volatile("tcgen05.fence::after_thread_sync;");
       const uint32_t taddr = tmem + ((uint32_t)(wn * 32) << 16) + (uint32_t)(b * 256 + wm * 128);
@@ -306,7 +314,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tfull[b]);
+      if (lane == 0) mbar_arrive(&tfull[b * C3_TB + (C3_TB > 1 ? warp : 0)]);
       t_main += tu1 - tu0;
       t_tempty += tu2 - tu1;
       t_store += pclock() - tu2;
@@ -334,7 +342,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
       c3_unit(u, p, &mt, &ct);
       const int b = ui & 1;
       const long long te0 = pclock();
-      mbar_wait(&tfull[b], (uint32_t)((ui >> 1) & 1));
+      mbar_wait(&tfull[b * C3_TB + (C3_TB > 1 ? twin : 0)], (uint32_t)((ui >> 1) & 1));
       const long long te1 = pclock();
       t_wait += te1 - te0;
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -373,7 +381,7 @@ __global__ void __launch_bounds__(C3_THREADS, 1) chord3_kernel(const ChordParams
             // every TMEM read of buffer b is complete: the MMA warps may refill it
             asm volatile("tcgen05.fence::before_thread_sync;");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[b]);
+            if (lane == 0) mbar_arrive(&tempty[b * C3_TB + (C3_TB > 1 ? twin : 0)]);
           }
 #pragma unroll
           for (int i = 0; i < 2; ++i) {
