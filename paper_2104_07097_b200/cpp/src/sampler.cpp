@@ -113,13 +113,18 @@ class Engine {
   ~Engine() { mhar_ctx_destroy(ctx_); }
   mhar_ctx* ctx() { return ctx_; }
   double eps_dir() const { return eps_dir_; }
-  // What the context was built from (step() rebinds when any of it changes).
+  // What the context was built from (step() rebinds when any of it changes):
+  // the contents' hash and where they live.
   uint64_t fingerprint = 0;
+  std::vector<uintptr_t> shape;
   // The reference streams continue across a rebind, as one WalkRng's do.
   void take_streams_from(Engine& other, int z) {
     std::vector<uint64_t> cols(static_cast<size_t>(z));
     uint64_t theta = 0;
     check(mhar_get_streams(other.ctx(), cols.data(), &theta));
+    check(mhar_set_streams(ctx_, cols.data(), &theta));
+  }
+  void set_streams(const std::vector<uint64_t>& cols, uint64_t theta) {
     check(mhar_set_streams(ctx_, cols.data(), &theta));
   }
   long long redraws() {
@@ -195,6 +200,23 @@ uint64_t engine_fingerprint(const Polytope& p, const ProjectionOperator* project
   }
   const double eps[2] = {cfg.eps_dir, cfg.eps_feas};
   return hash_words(eps, 2, h);
+}
+
+// Where the body's arrays live and how big they are, plus the tolerances: a
+// cheap check that tells a new or reallocated body from the bound one.
+std::vector<uintptr_t> body_shape(const Polytope& p, const ProjectionOperator* projector,
+                                  const SamplerConfig& cfg) {
+  uint64_t e[2];
+  std::memcpy(&e[0], &cfg.eps_dir, 8);
+  std::memcpy(&e[1], &cfg.eps_feas, 8);
+  return {reinterpret_cast<uintptr_t>(&p), reinterpret_cast<uintptr_t>(p.a_in.data()),
+          reinterpret_cast<uintptr_t>(p.b_in.data()), reinterpret_cast<uintptr_t>(p.a_eq.data()),
+          reinterpret_cast<uintptr_t>(p.b_eq.data()), (uintptr_t)p.dim(),
+          (uintptr_t)p.num_inequalities(), (uintptr_t)p.num_equalities(),
+          reinterpret_cast<uintptr_t>(projector),
+          projector ? reinterpret_cast<uintptr_t>(projector->p.data()) : 0,
+          projector ? reinterpret_cast<uintptr_t>(projector->gram_inverse.data()) : 0,
+          (uintptr_t)e[0], (uintptr_t)e[1]};
 }
 }  // namespace
 
@@ -297,15 +319,46 @@ void step(const Polytope& p, const ProjectionOperator* projector, const SamplerC
   // body (contents, projector and tolerances -- not just its address).  A
   // rebind hands the streams over, so they continue exactly as one WalkRng's
   // do in the reference (rng.hpp:42-55).
-  const uint64_t fp = engine_fingerprint(p, projector, cfg);
+  const std::vector<uintptr_t> shape = body_shape(p, projector, cfg);
+  std::vector<uint64_t> saved;  // the streams before an optimistic step
+  uint64_t saved_theta = 0;
+  uint64_t fp = 0;
+  if (rng.engine_ && rng.engine_->shape == shape) {
+    // Same arrays as the bound body: step at once and re-hash the contents
+    // on the host while the GPU works (A_I is 3.2 GB at config 5: the hash
+    // costs about half an iterate).  Only a body edited in place since the
+    // last call -- the hash differs -- discards this step and redoes it on a
+    // rebound context from the streams saved before it.
+    Engine& e = *rng.engine_;
+    saved.resize(static_cast<size_t>(rng.width()));
+    check(mhar_get_streams(e.ctx(), saved.data(), &saved_theta));
+    const long long before = e.redraws();
+    check(mhar_set_state(e.ctx(), state.x.data()));
+    int st = mhar_step(e.ctx(), 1, 0);
+    fp = engine_fingerprint(p, projector, cfg);  // overlaps the queued iterate
+    if (st == MHAR_OK) st = mhar_sync(e.ctx());
+    if (fp == e.fingerprint) {
+      state.redraws += e.redraws() - before;
+      check(st);
+      check(mhar_get_state(e.ctx(), state.x.data()));
+      ++state.j;
+      return;
+    }
+  } else {
+    fp = engine_fingerprint(p, projector, cfg);
+  }
   if (!rng.engine_ || rng.bound_ != &p || rng.engine_->fingerprint != fp) {
     auto fresh = std::make_unique<Engine>(p, projector, rng.width(), rng.seed(), cfg.eps_dir,
                                           cfg.eps_feas, MHAR_RNG_REFERENCE);
-    if (rng.engine_) fresh->take_streams_from(*rng.engine_, rng.width());
+    if (!saved.empty())
+      fresh->set_streams(saved, saved_theta);
+    else if (rng.engine_)
+      fresh->take_streams_from(*rng.engine_, rng.width());
     fresh->fingerprint = fp;
     rng.engine_ = std::move(fresh);
     rng.bound_ = &p;
   }
+  rng.engine_->shape = shape;
   mhar_ctx* ctx = rng.engine_->ctx();
   const long long before = rng.engine_->redraws();
   check(mhar_set_state(ctx, state.x.data()));

@@ -291,6 +291,42 @@ int main() {
     for (int k = 0; k < 8; ++k) CHECK(mhar::contains(body, state.x.col(k), 1e-15));
   });
 
+  run_case("a body edited in place is sampled, on the same trajectory as a rebind", [] {
+    // step() steps the bound context while it re-hashes the body; an in-place
+    // edit must discard that step and redo it from the saved streams
+    auto cfg = mhar::resolve(mhar::SamplerConfig{}, mhar::make_hypercube(3));
+    mhar::WalkRng ra(cfg.seed, 8), rb(cfg.seed, 8);
+    mhar::WalkState sa, sb;
+    sa.x = Matrix::Zero(3, 8);
+    sb.x = Matrix::Zero(3, 8);
+    mhar::Polytope body = mhar::make_hypercube(3);
+    const mhar::Polytope cube = mhar::make_hypercube(3);
+    for (int it = 0; it < 3; ++it) {
+      mhar::step(body, nullptr, cfg, ra, sa);
+      mhar::step(cube, nullptr, cfg, rb, sb);
+    }
+    const double* storage = body.b_in.data();
+    for (int i = 0; i < 6; ++i) body.b_in(i) = 0.5;  // same arrays, new contents
+    CHECK(body.b_in.data() == storage);
+    const mhar::Polytope half(cube.a_in, Vector::Constant(6, 0.5));
+    for (int k = 0; k < 8; ++k)
+      for (int i = 0; i < 3; ++i) {
+        sa.x(i, k) *= 0.25;  // inside the smaller box
+        sb.x(i, k) *= 0.25;
+      }
+    for (int it = 0; it < 4; ++it) {
+      mhar::step(body, nullptr, cfg, ra, sa);
+      mhar::step(half, nullptr, cfg, rb, sb);
+    }
+    double worst = 0.0;
+    for (int k = 0; k < 8; ++k) {
+      CHECK(mhar::contains(body, sa.x.col(k), 1e-15));
+      for (int i = 0; i < 3; ++i) worst = std::fmax(worst, std::fabs(sa.x(i, k) - sb.x(i, k)));
+    }
+    CHECK(worst == 0.0);
+    CHECK(sa.j == sb.j && sa.redraws == sb.redraws);
+  });
+
   run_case("streams continue across generate_directions and a rebind to the body", [] {
     // the reference's WalkRng keeps its streams across calls: directions drawn
     // before the first step are not replayed by it
