@@ -797,7 +797,14 @@ class Group:
 def step(p: Polytope, projector: Optional[ProjectionOperator], cfg: SamplerConfig,
          engine: Engine, state: WalkState):
     """step() (sampler.hpp:79-80) on an engine holding the walks' RNG:
-    state.x is uploaded, advanced one iterate on the device, and read back."""
+    state.x is uploaded, advanced one iterate on the device, and read back.
+    The engine holds its device copy of the body, so p must be the polytope
+    it was built for (the same object or the same arrays)."""
+    q = engine.p
+    if p is not q and not (p.a_in is q.a_in and p.b_in is q.b_in and p.a_eq is q.a_eq
+                           and p.b_eq is q.b_eq):
+        raise MharError(ErrorCode.invalid_argument,
+                        "step: the engine was built for another polytope (build an Engine for p)")
     engine.set_state(state.x)
     before = engine.stats()["redraw_count"]
     engine.step(1)

@@ -69,3 +69,20 @@ def test_select_points_uniform_along_chord_and_theta_stream(orc):
     s = orc.Stream(54, oracle.THETA_STREAM_ID)
     want = np.array([-1.0 + s.next_uniform() * 2.0 for _ in range(reps)])
     assert np.abs(moved[0] - want).max() <= 1e-15
+
+
+def test_step_runs_the_engine_body_and_rejects_another():
+    # step(p, op, cfg, engine, state): one iterate of the engine's body; a
+    # different polytope (same shape, other rows) is refused, not silently
+    # sampled with the engine's device copy
+    p = mh.make_hypercube(3)
+    cfg = mh.resolve(mh.SamplerConfig(), p)
+    with mh.Engine(p, 8, seed=5) as eng:
+        st = mh.WalkState(x=np.zeros((3, 8), order="F"))
+        mh.step(p, None, cfg, eng, st)
+        assert st.j == 1 and np.abs(st.x).max() <= 1.0 and np.abs(st.x).max() > 0.0
+        other = mh.Polytope(p.a_in.copy(), np.full(6, 0.5))
+        with pytest.raises(mh.MharError) as e:
+            mh.step(other, None, cfg, eng, st)
+        assert e.value.code == mh.ErrorCode.invalid_argument
+        assert st.j == 1
