@@ -285,6 +285,16 @@ def _f(a):
     return np.asfortranarray(np.asarray(a, dtype=np.float64))
 
 
+def _sized(what: str, a, shape, dtype=np.float64):
+    """a as a contiguous array of exactly `shape` (the C ABI reads that many
+    elements from the pointer): DIMENSION_MISMATCH otherwise."""
+    a = np.asfortranarray(np.asarray(a, dtype=dtype))
+    if a.shape != tuple(shape):
+        raise MharError(ErrorCode.dimension_mismatch,
+                        f"{what} has shape {a.shape}, expected {tuple(shape)}")
+    return a
+
+
 # -------------------------------------------------------------- types ------
 
 class Polytope:
@@ -292,14 +302,26 @@ class Polytope:
 
     def __init__(self, a_in, b_in, a_eq=None, b_eq=None):
         self.a_in = _f(a_in)
+        if self.a_in.ndim != 2:
+            raise MharError(ErrorCode.dimension_mismatch,
+                            f"polytope: a_in must be a matrix, got shape {self.a_in.shape}")
         self.b_in = np.ascontiguousarray(b_in, dtype=np.float64).reshape(-1)
         n = self.a_in.shape[1]
-        if a_eq is None:
+        if a_eq is None or np.asarray(a_eq).size == 0:
             self.a_eq = np.zeros((0, n), order="F")
-            self.b_eq = np.zeros(0)
+            self.b_eq = np.zeros(0) if b_eq is None else \
+                np.ascontiguousarray(b_eq, dtype=np.float64).reshape(-1)
         else:
             self.a_eq = _f(a_eq)
             self.b_eq = np.ascontiguousarray(b_eq, dtype=np.float64).reshape(-1)
+        # the reference constructor's checks (polytope.cpp:16-33, :90-97); the
+        # engine reads exactly these extents through the C ABI
+        for what, got, want in (("b_in length", self.b_in.size, self.a_in.shape[0]),
+                                ("a_eq width", self.a_eq.shape[1] if self.a_eq.ndim == 2 else -1, n),
+                                ("b_eq length", self.b_eq.size, self.a_eq.shape[0])):
+            if got != want:
+                raise MharError(ErrorCode.dimension_mismatch,
+                                f"polytope: {what} is {got}, expected {want}")
 
     def dim(self) -> int:
         return self.a_in.shape[1]
@@ -560,8 +582,8 @@ class Engine:
 
     def step_injected(self, H, U):
         """Test hook: returns (lower, upper, theta, flags); moves the state."""
-        H = _f(H)
-        U = np.ascontiguousarray(U, dtype=np.float64)
+        H = _sized("step_injected: H", H, (self.n, self.z))
+        U = _sized("step_injected: U", U, (self.z,))
         lo, hi, th = np.empty(self.z), np.empty(self.z), np.empty(self.z)
         fl = np.empty(self.z, np.uint8)
         _check(lib().mhar_step_injected(self._h, _d(H), _d(U), _d(lo), _d(hi), _d(th),
@@ -578,17 +600,19 @@ class Engine:
     def select_points(self, X, D, intervals: "LambdaIntervals") -> np.ndarray:
         """select_points (sampler.cpp:214-233): x + theta d, theta uniform on
         each open chord from the theta stream; DIRECTION_DEGENERATE on flags."""
-        X, D = _f(X), _f(D)
-        lo = np.ascontiguousarray(intervals.lower, dtype=np.float64)
-        hi = np.ascontiguousarray(intervals.upper, dtype=np.float64)
-        dg = np.ascontiguousarray(intervals.degenerate, dtype=np.uint8)
+        X = _sized("select_points: x", X, (self.n, self.z))
+        D = _sized("select_points: d", D, (self.n, self.z))
+        lo = _sized("select_points: lower", intervals.lower, (self.z,))
+        hi = _sized("select_points: upper", intervals.upper, (self.z,))
+        dg = _sized("select_points: degenerate", intervals.degenerate, (self.z,), np.uint8)
         out = np.empty((self.n, self.z), order="F")
         _check(lib().mhar_select_points(self._h, _d(X), _d(D), _d(lo), _d(hi),
                                         dg.ctypes.data_as(_u8p), _d(out)))
         return out
 
     def lambda_intervals(self, X, D) -> LambdaIntervals:
-        X, D = _f(X), _f(D)
+        X = _sized("compute_lambda_intervals: x", X, (self.n, self.z))
+        D = _sized("compute_lambda_intervals: d", D, (self.n, self.z))
         lo, hi = np.empty(self.z), np.empty(self.z)
         fl = np.empty(self.z, np.uint8)
         _check(lib().mhar_lambda_intervals(self._h, _d(X), _d(D), _d(lo), _d(hi),

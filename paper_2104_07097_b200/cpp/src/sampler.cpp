@@ -41,12 +41,29 @@ void check(int status) {
 }  // namespace
 
 // --------------------------------------------------------------- polytope --
+// The reference's constructor checks (polytope.cpp:16-33, :90-97): every
+// right-hand side matches its matrix, and equalities have the body's width
+// (an empty a_eq takes it).  The engine reads exactly these extents.
+static void require_shapes(const Polytope& p) {
+  auto mismatch = [](const std::string& what, Index got, Index want) {
+    raise(ErrorCode::dimension_mismatch, "polytope: " + what + " is " + std::to_string(got) +
+                                             ", expected " + std::to_string(want));
+  };
+  if (p.b_in.size() != p.a_in.rows()) mismatch("b_in length", p.b_in.size(), p.a_in.rows());
+  if (p.b_eq.size() != p.a_eq.rows()) mismatch("b_eq length", p.b_eq.size(), p.a_eq.rows());
+  if (p.a_eq.cols() != p.a_in.cols()) mismatch("a_eq width", p.a_eq.cols(), p.a_in.cols());
+}
+
 Polytope::Polytope(Matrix a_in_, Vector b_in_) : a_in(std::move(a_in_)), b_in(std::move(b_in_)) {
   a_eq = Matrix(0, a_in.cols());
+  require_shapes(*this);
 }
 Polytope::Polytope(Matrix a_in_, Vector b_in_, Matrix a_eq_, Vector b_eq_)
     : a_in(std::move(a_in_)), b_in(std::move(b_in_)), a_eq(std::move(a_eq_)),
-      b_eq(std::move(b_eq_)) {}
+      b_eq(std::move(b_eq_)) {
+  if (a_eq.rows() == 0) a_eq = Matrix(0, a_in.cols());
+  require_shapes(*this);
+}
 
 bool contains(const Polytope& p, const double* x, double eps) {
   for (Index i = 0; i < p.a_in.rows(); ++i) {

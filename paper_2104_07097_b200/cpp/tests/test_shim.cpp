@@ -291,6 +291,20 @@ int main() {
     for (int k = 0; k < 8; ++k) CHECK(mhar::contains(body, state.x.col(k), 1e-15));
   });
 
+  run_case("polytope constructor checks shapes like the reference (polytope.cpp:16-33)", [] {
+    using mhar::ErrorCode;
+    expect_error(ErrorCode::dimension_mismatch,
+                 [] { mhar::Polytope(Matrix::Zero(3, 2), Vector::Ones(2)); });
+    expect_error(ErrorCode::dimension_mismatch, [] {
+      mhar::Polytope(Matrix::Zero(3, 2), Vector::Ones(3), Matrix::Zero(1, 3), Vector::Ones(1));
+    });
+    expect_error(ErrorCode::dimension_mismatch, [] {
+      mhar::Polytope(Matrix::Zero(3, 2), Vector::Ones(3), Matrix::Zero(1, 2), Vector::Ones(2));
+    });
+    const mhar::Polytope ok(Matrix::Zero(3, 2), Vector::Ones(3), Matrix(0, 0), Vector(0));
+    CHECK(ok.a_eq.rows() == 0 && ok.a_eq.cols() == 2);
+  });
+
   run_case("a body edited in place is sampled, on the same trajectory as a rebind", [] {
     // step() steps the bound context while it re-hashes the body; an in-place
     // edit must discard that step and redo it from the saved streams
