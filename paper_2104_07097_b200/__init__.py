@@ -474,8 +474,9 @@ def _context_args(p, z, seed, projector, eps_dir, eps_feas, rng, slack, refresh_
     opt.z_plan = int(z_plan)
     P = G = None
     if projector is not None:
-        P = _f(projector.p)
-        G = _f(projector.gram_inverse)
+        me = p.num_equalities()
+        P = _sized("projector: p", projector.p, (p.dim(), p.dim()))
+        G = _sized("projector: gram_inverse", projector.gram_inverse, (me, me))
     return poly, opt, P, G
 
 
