@@ -1,8 +1,11 @@
 // C++ drop-in step() loop vs the bare C-ABI iterate at BASELINE config 5
 // (n = 2000, m_I = 2e5 unit-norm Gaussian rows, 4096 walks): what the shim's
 // per-call body check costs once it overlaps the queued iterate.
-//   g++ -O2 -std=c++20 -I../paper_2104_07097_b200/cpp/include tools/shim_step_rate.cpp \
-//       -Lpaper_2104_07097_b200/lib -lmhar_cpp -lmhar_b200 -Wl,-rpath,$PWD/paper_2104_07097_b200/lib
+// Build from the repo root (after __graft_entry__.build()):
+//   g++ -O2 -std=c++20 -Ipaper_2104_07097_b200/cpp/include tools/shim_step_rate.cpp \
+//       -Lpaper_2104_07097_b200/lib -lmhar_cpp -lmhar_b200 \
+//       -Wl,-rpath,'$ORIGIN/../paper_2104_07097_b200/lib' -o tools/shim_step_rate
+//   ./tools/shim_step_rate [iterates]
 #include <chrono>
 #include <cmath>
 #include <cstdio>
