@@ -826,8 +826,13 @@ def step(p: Polytope, projector: Optional[ProjectionOperator], cfg: SamplerConfi
     The engine holds its device copy of the body, so p must be the polytope
     it was built for (the same object or the same arrays)."""
     q = engine.p
-    if p is not q and not (p.a_in is q.a_in and p.b_in is q.b_in and p.a_eq is q.a_eq
-                           and p.b_eq is q.b_eq):
+
+    def same(a, b):  # the same array memory (or both empty of one shape)
+        return a is b or (a.shape == b.shape and (a.size == 0 or (
+            a.strides == b.strides and
+            a.__array_interface__["data"][0] == b.__array_interface__["data"][0])))
+    if p is not q and not (same(p.a_in, q.a_in) and same(p.b_in, q.b_in)
+                           and same(p.a_eq, q.a_eq) and same(p.b_eq, q.b_eq)):
         raise MharError(ErrorCode.invalid_argument,
                         "step: the engine was built for another polytope (build an Engine for p)")
     engine.set_state(state.x)

@@ -28,3 +28,20 @@ def test_valid_bodies_and_empty_equalities_take_the_width():
     assert s.a_eq.shape == (1, 5) and s.b_eq.shape == (1,)
     c = mh.make_hypercube(3)
     assert c.a_in.shape == (6, 3) and c.b_in.shape == (6,)
+
+
+def test_step_guard_tells_the_engine_body_from_another():
+    # step(p, ..., engine, state) refuses a body other than the engine's
+    # before touching the device; a re-wrap of the same arrays is the same body
+    p = mh.make_hypercube(3)
+
+    class Bound:  # stands in for an Engine: the guard runs before any device call
+        pass
+    eng = Bound()
+    eng.p = p
+    st = mh.WalkState(x=np.zeros((3, 2), order="F"))
+    with pytest.raises(mh.MharError) as e:
+        mh.step(mh.Polytope(p.a_in.copy(), p.b_in), None, None, eng, st)
+    assert e.value.code == mh.ErrorCode.invalid_argument
+    with pytest.raises(AttributeError):  # got past the guard, to the engine call
+        mh.step(mh.Polytope(p.a_in, p.b_in), None, None, eng, st)
